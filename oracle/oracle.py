@@ -1,0 +1,191 @@
+"""ctypes loader for the CPU oracle (oracle/dpf_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / ``--impl reference`` legs -- never by the product
+package ``paper_2301_10904_b200``.  Shares no code with the CUDA path.
+
+Every function here is argument marshalling around the plain C oracle; the
+citations for what each computes are in dpf_oracle.c.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "dpf_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+MAX_LOG_N = 32
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (plain C99, -O2, pthreads)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + ".tmp%d" % os.getpid()
+        subprocess.check_call(["gcc", "-std=c99", "-O2", "-fPIC", "-shared", "-Wall", "-o", tmp, _SRC,
+                               "-lpthread"])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+class OracleKey(ctypes.Structure):
+    _fields_ = [("log_n", ctypes.c_uint32), ("party", ctypes.c_uint32), ("cw_out", ctypes.c_uint32),
+                ("root", ctypes.c_uint8 * 16), ("cw", ctypes.c_uint8 * (MAX_LOG_N * 2 * 2 * 16))]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        u8p = ctypes.POINTER(ctypes.c_uint8)
+        u32p = ctypes.POINTER(ctypes.c_uint32)
+        u64p = ctypes.POINTER(ctypes.c_uint64)
+        kp = ctypes.POINTER(OracleKey)
+        L.oracle_chacha20_block.argtypes = [u8p, ctypes.c_uint32, u8p, u8p]
+        L.oracle_prf.argtypes = [u8p, ctypes.c_uint32, u8p]
+        L.oracle_key_struct_size.restype = ctypes.c_size_t
+        L.oracle_gen.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, u8p, kp, kp, u64p]
+        L.oracle_eval_point.argtypes = [kp, ctypes.c_uint64, u64p]
+        L.oracle_eval_point.restype = ctypes.c_uint32
+        L.oracle_eval_full.argtypes = [kp, u32p, u64p]
+        L.oracle_eval_full_seeds.argtypes = [kp, u8p, u64p]
+        L.oracle_contract.argtypes = [u32p, ctypes.c_uint64, u32p, ctypes.c_uint32, u32p]
+        L.oracle_answer_rows.argtypes = [kp, u32p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, u32p, u64p]
+        L.oracle_answer_batch.argtypes = [kp, ctypes.c_uint32, u32p, ctypes.c_uint64, ctypes.c_uint64,
+                                          ctypes.c_uint32, u32p, ctypes.c_uint32]
+        L.oracle_reconstruct.argtypes = [u32p, u32p, ctypes.c_uint64, u32p]
+        L.oracle_naive_pir_shares.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, u32p, u32p]
+        L.oracle_key_wire_size.argtypes = [ctypes.c_uint32]
+        L.oracle_key_wire_size.restype = ctypes.c_size_t
+        L.oracle_key_to_wire.argtypes = [kp, u8p, ctypes.c_size_t]
+        L.oracle_key_from_wire.argtypes = [u8p, ctypes.c_size_t, kp]
+        assert L.oracle_key_struct_size() == ctypes.sizeof(OracleKey)
+        _lib = L
+    return _lib
+
+
+def _u8(a: np.ndarray):
+    assert a.dtype == np.uint8 and a.flags.c_contiguous
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8))
+
+
+def _u32(a: np.ndarray):
+    assert a.dtype == np.uint32 and a.flags.c_contiguous
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32))
+
+
+def _bytes_in(b) -> np.ndarray:
+    return np.frombuffer(bytes(b), dtype=np.uint8).copy()
+
+
+# ---------------------------------------------------------------- primitives
+
+def chacha20_block(key: bytes, counter: int, nonce: bytes) -> bytes:
+    out = np.zeros(64, np.uint8)
+    lib().oracle_chacha20_block(_u8(_bytes_in(key)), counter, _u8(_bytes_in(nonce)), _u8(out))
+    return out.tobytes()
+
+
+def prf(seed: bytes, c: int) -> bytes:
+    out = np.zeros(16, np.uint8)
+    lib().oracle_prf(_u8(_bytes_in(seed)), c, _u8(out))
+    return out.tobytes()
+
+
+# ---------------------------------------------------------------- DPF
+
+def gen(log_n: int, alpha: int, beta: int, rng_seed: bytes, count_blocks: bool = False):
+    k0, k1 = OracleKey(), OracleKey()
+    blocks = ctypes.c_uint64(0)
+    rc = lib().oracle_gen(log_n, alpha, beta & 0xFFFFFFFF, _u8(_bytes_in(rng_seed)), ctypes.byref(k0),
+                          ctypes.byref(k1), ctypes.byref(blocks))
+    if rc:
+        raise ValueError("oracle_gen rejected arguments (rc=%d)" % rc)
+    return (k0, k1, blocks.value) if count_blocks else (k0, k1)
+
+
+def eval_point(k: OracleKey, j: int, count_blocks: bool = False):
+    blocks = ctypes.c_uint64(0)
+    y = lib().oracle_eval_point(ctypes.byref(k), j, ctypes.byref(blocks))
+    return (y, blocks.value) if count_blocks else y
+
+
+def eval_full(k: OracleKey, count_blocks: bool = False):
+    y = np.zeros(1 << k.log_n, np.uint32)
+    blocks = ctypes.c_uint64(0)
+    rc = lib().oracle_eval_full(ctypes.byref(k), _u32(y), ctypes.byref(blocks))
+    if rc:
+        raise RuntimeError("oracle_eval_full rc=%d" % rc)
+    return (y, blocks.value) if count_blocks else y
+
+
+def eval_full_seeds(k: OracleKey) -> np.ndarray:
+    s = np.zeros((1 << k.log_n, 16), np.uint8)
+    rc = lib().oracle_eval_full_seeds(ctypes.byref(k), _u8(s), None)
+    if rc:
+        raise RuntimeError("oracle_eval_full_seeds rc=%d" % rc)
+    return s
+
+
+def contract(y: np.ndarray, T: np.ndarray) -> np.ndarray:
+    y = np.ascontiguousarray(y, np.uint32)
+    T = np.ascontiguousarray(T, np.uint32)
+    rows, D = T.shape
+    assert y.shape[0] >= rows
+    out = np.zeros(D, np.uint32)
+    lib().oracle_contract(_u32(y), rows, _u32(T), D, _u32(out))
+    return out
+
+
+def answer_batch(keys, T: np.ndarray, row_begin: int = 0, threads: int = 1) -> np.ndarray:
+    """shares[b][d] = sum_{j in shard} Eval(keys[b], row_begin + j) T[j][d] mod 2^32."""
+    T = np.ascontiguousarray(T, np.uint32)
+    rows, D = T.shape
+    B = len(keys)
+    arr = (OracleKey * B)(*keys)
+    out = np.zeros((B, D), np.uint32)
+    rc = lib().oracle_answer_batch(arr, B, _u32(T), row_begin, rows, D, _u32(out), threads)
+    if rc:
+        raise RuntimeError("oracle_answer_batch rc=%d" % rc)
+    return out
+
+
+def reconstruct(s0: np.ndarray, s1: np.ndarray) -> np.ndarray:
+    s0 = np.ascontiguousarray(s0, np.uint32)
+    s1 = np.ascontiguousarray(s1, np.uint32)
+    out = np.zeros_like(s0)
+    lib().oracle_reconstruct(_u32(s0), _u32(s1), s0.size, _u32(out))
+    return out
+
+
+def naive_pir_shares(N: int, alpha: int, beta: int, r0: np.ndarray) -> np.ndarray:
+    r0 = np.ascontiguousarray(r0, np.uint32)
+    r1 = np.zeros(N, np.uint32)
+    lib().oracle_naive_pir_shares(N, alpha, beta & 0xFFFFFFFF, _u32(r0), _u32(r1))
+    return r1
+
+
+def key_wire_size(log_n: int) -> int:
+    return lib().oracle_key_wire_size(log_n)
+
+
+def key_to_wire(k: OracleKey) -> bytes:
+    out = np.zeros(key_wire_size(k.log_n), np.uint8)
+    n = lib().oracle_key_to_wire(ctypes.byref(k), _u8(out), out.size)
+    assert n == out.size
+    return out.tobytes()
+
+
+def key_from_wire(b: bytes) -> OracleKey:
+    k = OracleKey()
+    arr = _bytes_in(b)
+    rc = lib().oracle_key_from_wire(_u8(arr), arr.size, ctypes.byref(k))
+    if rc:
+        raise ValueError("bad key wire bytes (rc=%d)" % rc)
+    return k

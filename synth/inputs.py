@@ -1,0 +1,66 @@
+"""Synthetic workload generators (see synth/__init__.py and DESIGN.md).
+
+All streams come from numpy's PCG64 seeded with (config seed, stream id), so
+every process (oracle, CUDA path, every rank) regenerates identical inputs.
+Distributions follow the paper's workloads: embedding tables of L rows with
+D int32 words per row ("2048-bit entries"), stored as uint32 bit
+patterns uniform over all 2^32 values; query indices uniform over the rows
+(one queried index per DPF key); beta = 1 for PIR unless a test
+asks for a random beta.
+"""
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+__all__ = ["Workload", "CONFIGS", "table", "alphas", "betas", "gen_seeds", "rng"]
+
+_STREAM_TABLE, _STREAM_ALPHA, _STREAM_BETA, _STREAM_GEN = 1, 2, 3, 4
+
+
+def rng(seed: int, stream: int) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64([seed & 0xFFFFFFFF, stream]))
+
+
+def table(N: int, D: int, seed: int) -> np.ndarray:
+    """int32 embedding table T[N][D] as uint32 bit patterns, uniform."""
+    return rng(seed, _STREAM_TABLE).integers(0, 1 << 32, size=(N, D), dtype=np.uint32)
+
+
+def alphas(B: int, N: int, seed: int) -> np.ndarray:
+    """Queried row per key, uniform over [0, N)."""
+    return rng(seed, _STREAM_ALPHA).integers(0, N, size=B, dtype=np.uint64)
+
+
+def betas(B: int, seed: int, random: bool = False) -> np.ndarray:
+    if not random:
+        return np.ones(B, np.uint32)
+    return rng(seed, _STREAM_BETA).integers(0, 1 << 32, size=B, dtype=np.uint32)
+
+
+def gen_seeds(B: int, seed: int) -> list[bytes]:
+    """32-byte DRBG seed per key (the randomness Gen draws)."""
+    raw = rng(seed, _STREAM_GEN).integers(0, 256, size=(B, 32), dtype=np.uint8)
+    return [bytes(r) for r in raw]
+
+
+@dataclasses.dataclass(frozen=True)
+class Workload:
+    name: str
+    log_n: int      # tree depth n; domain 2^n
+    N: int          # table rows (<= 2^n)
+    D: int          # int32 words per row
+    B: int          # keys per batch
+    seed: int
+    note: str = ""
+
+
+# BASELINE.json "configs" (c1..c4); c5 is the grouped co-design workload (NEXT).
+CONFIGS = {
+    "c1": Workload("c1", 10, 1 << 10, 16, 1, 0x7AB1E001, "2^10 x 16, B=1, both servers in-process"),
+    "c2": Workload("c2", 16, 1 << 16, 64, 64, 0x7AB1E002, "2^16 x 64, B=64, 1 GPU"),
+    "c3": Workload("c3", 20, 1 << 20, 256, 256, 0x7AB1E003, "2^20 x 256 int32 (1 GiB), B=256, 1 GPU"),
+    "c4": Workload("c4", 24, 1 << 24, 64, 512, 0x7AB1E004, "2^24 x 64, B=512, row-sharded over G GPUs"),
+    "t5": Workload("t5", 20, 1 << 20, 64, 512, 0x7AB1E005, "Table 5 shape: 2^20 x 64, B=512 (context)"),
+}
