@@ -1,0 +1,191 @@
+/*
+ * dpfpir.h -- C ABI of libdpfpir, the B200 (sm_100a) server hot path of
+ * two-server DPF-based PIR (Lam et al., arXiv 2301.10904, "GPU-based Private
+ * Information Retrieval for On-Device Machine Learning Inference").
+ *
+ * Citations: P:n = PAPER.md line n; readings R1..R14 = DESIGN.md "Readings".
+ *
+ * The problem statement this ABI follows:
+ *   Gen(1^lambda, i) -> (k_a, k_b)                       [dpf_gen]
+ *   Eval(k, j) in F_p with Eval(k_a,j) + Eval(k_b,j) = [j = i]
+ *   each server returns T x Eval(k, {0..L-1})            [dpf_eval_batch]
+ *   the client adds the two answers to obtain T[i]       [dpf_reconstruct]
+ * Arithmetic: seeds live in F_{2^128} ("+" = XOR, R1); leaf
+ * shares, table and answers live in Z_{2^32} (all share arithmetic wraps mod
+ * 2^32; the table is int32 bit patterns, R13).  beta generalises the "1" of
+ * the contract (R11): shares reconstruct to beta * T[alpha] mod 2^32.
+ *
+ * Conventions: all multi-byte integers are little-endian.  Every function
+ * returns a dpf_status code (never aborts, never throws across the ABI).
+ * Buffers are always owned by the caller; the library keeps no global mutable
+ * state and allocates nothing on the evaluation path (the device workspace is
+ * caller-provided), so all entry points are thread-safe and reentrant.
+ * "device" pointers are CUDA device (or managed) pointers on the current
+ * device; `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ * stream).  Device-side entry points are asynchronous on `stream` unless
+ * stated otherwise: configuration errors are reported synchronously, device
+ * faults surface at the caller's next synchronisation.
+ */
+#ifndef DPFPIR_H
+#define DPFPIR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DPF_MAX_LOG_N 32
+#define DPF_KEY_MAGIC 0x4B465044u /* bytes 'D','P','F','K' read as LE u32 */
+#define DPF_KEY_VERSION 1
+
+/* PRF of the tree.  ChaCha20 (Table 5) is the hot-path
+ * PRF; AES-128 is a later row. */
+enum dpf_prf { DPF_PRF_CHACHA20 = 1, DPF_PRF_AES128 = 2 };
+
+enum dpf_status {
+  DPF_OK = 0,
+  DPF_EINVAL = -1,       /* bad argument: NULL pointer, size/range/alignment violation */
+  DPF_EKEY = -2,         /* malformed key: magic/version/party/log_n/prf mismatch */
+  DPF_ENOMEM = -3,       /* workspace too small */
+  DPF_ECUDA = -4,        /* CUDA launch/config error (reported synchronously) */
+  DPF_EUNSUPPORTED = -6  /* feature not built (e.g. DPF_PRF_AES128), no sm_100 device */
+};
+
+/* One party's DPF key (two codeword matrices C_0, C_1; P:349 root
+ * P(0,0) = C_0[0,0]).  Reading R3: the root (column 0) is stored separately
+ * and is party-specific; columns d = 1..log_n are cw[d-1][t][c] = C_t[c, d],
+ * shared by both parties (R4).  cw_out is the final Z_2^32 correction (R7).
+ * POD, fixed size, caller-owned.  Invariant: lsb(root[0]) == party. */
+typedef struct dpf_key {
+  uint32_t magic;        /* DPF_KEY_MAGIC */
+  uint8_t version;       /* DPF_KEY_VERSION */
+  uint8_t prf;           /* enum dpf_prf */
+  uint8_t party;         /* 0 or 1 */
+  uint8_t log_n;         /* tree depth n, 1..DPF_MAX_LOG_N; domain 2^n rows */
+  uint32_t cw_out;       /* final correction word in Z_2^32 */
+  uint32_t reserved;     /* 0 */
+  uint8_t root[16];      /* s^(0) = P(0,0) */
+  uint8_t cw[DPF_MAX_LOG_N][2][2][16];
+} dpf_key;
+
+/* ---------------------------------------------------------------- client */
+
+/* Gen (construction per [dpf_1], written out in
+ * DESIGN.md "Gen").  Builds k0 (party 0) and k1 (party 1) so that for every
+ * j < 2^log_n: Eval(k0,j) + Eval(k1,j) = beta if j == alpha else 0 (mod 2^32).
+ * rng_seed: 32 bytes keying the ChaCha20 DRBG that draws the roots and
+ * codewords (deterministic for tests); NULL draws the seed from getrandom().
+ * Cost: 2*log_n ChaCha20 blocks.  Errors: DPF_EINVAL if log_n not in
+ * [1, 32], alpha >= 2^log_n, k0/k1 NULL; DPF_EUNSUPPORTED if prf is not
+ * DPF_PRF_CHACHA20. */
+int dpf_gen(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t prf, const uint8_t *rng_seed,
+            dpf_key *k0, dpf_key *k1);
+
+/* Wire size of a key: 32-byte header + 64*log_n payload bytes.  The payload
+ * equals Table 4's "Bytes" column exactly (896/1280/1408 B at 2^14/2^20/2^22
+ * entries).  Returns 0 if log_n is out of range. */
+size_t dpf_key_wire_size(uint32_t log_n);
+
+/* Serialize k into out[0..cap).  Wire format:
+ * magic u32 | version u8 | prf u8 | party u8 | log_n u8 | cw_out u32 |
+ * reserved u32 | root[16] | for d=1..n: cw[d-1][0][0], cw[d-1][0][1],
+ * cw[d-1][1][0], cw[d-1][1][1] (16 B each).  *written (optional) receives
+ * the byte count.  Errors: DPF_EINVAL (NULL, cap too small), DPF_EKEY. */
+int dpf_key_serialize(const dpf_key *k, uint8_t *out, size_t cap, size_t *written);
+
+/* Parse a wire key.  Errors: DPF_EINVAL (NULL), DPF_EKEY (bad magic/version/
+ * prf/party, log_n out of range, len != dpf_key_wire_size(log_n),
+ * lsb(root) != party, reserved != 0). */
+int dpf_key_deserialize(const uint8_t *in, size_t len, dpf_key *k);
+
+/* Client-side reconstruction: out[i] = share0[i] + share1[i] mod 2^32.
+ * Host pointers; out may alias either input.  Errors: DPF_EINVAL (NULL with
+ * count > 0). */
+int dpf_reconstruct(const uint32_t *share0, const uint32_t *share1, size_t count, uint32_t *out);
+
+/* ---------------------------------------------------------------- server */
+
+/* Device workspace bytes needed by dpf_eval_batch_shard for B keys of depth
+ * log_n over row_count rows of D words.  0 on invalid arguments. */
+size_t dpf_eval_workspace_bytes(uint32_t B, uint32_t log_n, uint64_t row_count, uint32_t D);
+
+/* Server answer for a batch ("batched together as a single
+ * matrix-matrix multiplication"):
+ *   shares[b][d] = sum_{j < N} Eval(keys[b], j) * table[j][d]  (mod 2^32)
+ * keys:   HOST array of B keys (same log_n, same prf); copied to the device
+ *         inside the call (they may be reused as soon as the call returns).
+ * table:  DEVICE, N x D uint32 (int32 bit patterns), row-major, 16-byte
+ *         aligned; N <= 2^log_n (rows >= N are absent = zero rows, R12).
+ * shares: DEVICE, B x D uint32, overwritten (not accumulated).
+ * workspace: DEVICE, >= dpf_eval_workspace_bytes(B, log_n, N, D) bytes,
+ *         256-byte aligned; must not be used concurrently by another call.
+ * Requirements: B >= 1, 1 <= D <= 1024 with D % 4 == 0, 1 <= N <= 2^log_n.
+ * Errors: DPF_EINVAL, DPF_EKEY (malformed key or keys disagree on log_n/prf),
+ * DPF_ENOMEM (workspace too small), DPF_EUNSUPPORTED (prf), DPF_ECUDA. */
+int dpf_eval_batch(const dpf_key *keys, uint32_t B, const uint32_t *table, uint64_t N, uint32_t D,
+                   uint32_t *shares, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Row-sharded answer (the multi-GPU split of P:536-540: "each of the N GPUs
+ * evaluate the DPF on a subset of the table indices, then summing"):
+ *   partial[b][d] = sum_{row_begin <= j < row_begin+row_count}
+ *                     Eval(keys[b], j) * table_shard[j - row_begin][d]
+ * table_shard points at row row_begin of the logical table.  Partials of any
+ * partition of [0, N) sum (mod 2^32) to dpf_eval_batch's shares.  Same
+ * arguments, ownership and errors as dpf_eval_batch, plus
+ * row_begin + row_count <= 2^log_n. */
+int dpf_eval_batch_shard(const dpf_key *keys, uint32_t B, const uint32_t *table_shard,
+                         uint64_t row_begin, uint64_t row_count, uint32_t D, uint32_t *partial_shares,
+                         void *workspace, size_t workspace_bytes, void *stream);
+
+/* Device-resident keys: as dpf_eval_batch_shard, but the B keys are already
+ * on the device as consecutive wire-format records (dpf_key_serialize
+ * output, stride dpf_key_wire_size(log_n) bytes, 16-byte aligned base),
+ * e.g. received by the server straight into HBM.  The keys are NOT
+ * re-validated (device memory is not read by the host): callers validate at
+ * dpf_key_deserialize time.  No host->device traffic; fully asynchronous. */
+int dpf_eval_batch_wire(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n, const uint32_t *table_shard,
+                        uint64_t row_begin, uint64_t row_count, uint32_t D, uint32_t *partial_shares,
+                        void *workspace, size_t workspace_bytes, void *stream);
+
+/* End-to-end serving call: as dpf_eval_batch_shard, but shares_host is a HOST
+ * buffer (pinned for best speed) that receives the B x D answers; the call
+ * synchronises `stream` before returning.  The table stays device-resident
+ * (server state).  workspace_bytes must cover
+ * dpf_eval_workspace_bytes(...) plus B*D*4 bytes rounded up to 256 (the
+ * device copy of the answer lives after the evaluation workspace). */
+int dpf_serve_batch(const dpf_key *keys, uint32_t B, const uint32_t *table_shard, uint64_t row_begin,
+                    uint64_t row_count, uint32_t D, uint32_t *shares_host, void *workspace,
+                    size_t workspace_bytes, void *stream);
+
+/* Test/debug only: leaf shares leaves[b][j] = Eval(keys[b], j) for all
+ * j < 2^log_n (sign applied), log_n <= 20.  DEVICE output (B x 2^log_n),
+ * workspace as for dpf_eval_batch with N = 2^log_n, D = 4. */
+int dpf_eval_leaves(const dpf_key *keys, uint32_t B, uint32_t *leaves, void *workspace,
+                    size_t workspace_bytes, void *stream);
+
+/* Counters of the last successful eval on this thread (host-side
+ * bookkeeping of the launch plan, no device reads): ChaCha20 blocks the
+ * kernels compute and kernels launched. */
+typedef struct dpf_eval_stats {
+  uint64_t prf_blocks;    /* total ChaCha20 blocks computed by the device */
+  uint32_t kernels;       /* kernel launches issued by the call */
+  uint32_t frontier_depth;/* f: BFS depth of the top kernel */
+  uint32_t keys_per_tile; /* Kt */
+  uint32_t nodes_per_tile;/* Ft */
+  uint32_t work_items;    /* fused-kernel work items */
+  uint32_t grid;          /* fused-kernel CTAs */
+} dpf_eval_stats;
+int dpf_last_eval_stats(dpf_eval_stats *out);
+
+/* Human-readable status text (static storage). */
+const char *dpf_strerror(int code);
+
+/* Library version string. */
+const char *dpf_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DPFPIR_H */

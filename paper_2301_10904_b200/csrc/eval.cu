@@ -1,0 +1,724 @@
+// eval.cu -- server half of libdpfpir: batched full-domain DPF evaluation
+// fused with the mod-2^32 table contraction, for sm_100a (B200).
+//
+// Path (P:n = PAPER.md line n):
+//   a1 key ingest    host dpf_key[] -> wire-format keys in the workspace (H2D)
+//   a2 top BFS       levels 1..f of every key's GGM tree (Eq. 3)
+//                    -> frontier[B][F] in HBM/L2 (P:428 level-by-level, only
+//                    for the small top of the tree)
+//   a3-a6 fused      persistent warp-specialised kernel, one CTA per SM:
+//                    * producer warps: per-thread depth-first expansion of a
+//                      depth-m subtree (the memory-bounded traversal of
+//                      P:437-443 with K = one node per thread and an SMEM
+//                      stack of m-1 pending right children), leaf conversion
+//                      into an SMEM y-tile ring (leaves never reach HBM)
+//                    * loader warp: cp.async.bulk of the matching table rows
+//                      into an SMEM T-tile ring (mbarrier complete_tx); each
+//                      T row is read by all keys of the tile (P:364 batched
+//                      matrix-matrix product)
+//                    * consumer warps: IMAD outer products acc[key][col] +=
+//                      y * T in registers ("dot product ...
+//                      accumulating the result in local memory"), flushed with
+//                      red.global.add.u32 (exact: Z_2^32 addition is
+//                      associative, P:483 tree-summation)
+//   a7 output        shares[B][D] on the device, party sign applied at flush.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "chacha_dev.cuh"
+#include "dpfpir.h"
+
+namespace dpfpir {
+bool host_key_valid(const dpf_key &k);
+
+namespace dev {
+
+// ----------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "DPF_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra DPF_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void red_add_u32(uint32_t *addr, uint32_t v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+}
+
+// Wire-format key accessors (include/dpfpir.h).
+__device__ __forceinline__ uint4 key_root(const uint8_t *k) { return __ldg(reinterpret_cast<const uint4 *>(k + 16)); }
+__device__ __forceinline__ uint32_t key_cw_out(const uint8_t *k) {
+  return __ldg(reinterpret_cast<const uint32_t *>(k + 8));
+}
+__device__ __forceinline__ uint32_t key_party(const uint8_t *k) {
+  return (__ldg(reinterpret_cast<const uint32_t *>(k + 4)) >> 16) & 0xFFu;
+}
+// 64-byte codeword column of depth d (1-based): [t][c] x uint4
+__device__ __forceinline__ const uint4 *key_cw(const uint8_t *k, uint32_t d) {
+  return reinterpret_cast<const uint4 *>(k + 32 + 64u * (d - 1u));
+}
+
+// ----------------------------------------------------------------- a2: top BFS
+// One launch per level k = 1..f.  Level k's nodes intersecting the row range
+// [r0, r1) are [lo_k, hi_k], lo_k = r0 >> (n-k); stored at [i - lo_k].
+// Thread per (key, parent): both children by one block (R9), kept if in range.
+__global__ void expand_level_kernel(const uint8_t *__restrict__ keys, uint32_t kstride, uint32_t B, uint32_t n,
+                                    uint32_t k, uint64_t r0, uint64_t r1, const uint4 *__restrict__ in,
+                                    uint4 *__restrict__ out, uint64_t cap) {
+  const uint64_t plo = r0 >> (n - (k - 1)), phi = (r1 - 1) >> (n - (k - 1));
+  const uint64_t lo = r0 >> (n - k), hi = (r1 - 1) >> (n - k);
+  const uint64_t np = phi - plo + 1;
+  const uint64_t total = np * B;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t b = uint32_t(i / np);
+    const uint64_t p = plo + (i % np);
+    const uint8_t *key = keys + uint64_t(b) * kstride;
+    const uint4 s = (k == 1) ? key_root(key) : in[uint64_t(b) * cap + (p - plo)];
+    uint4 c0, c1;
+    node_children(s, key_cw(key, k), c0, c1);
+    const uint64_t j0 = 2 * p, j1 = 2 * p + 1;
+    if (j0 >= lo && j0 <= hi) out[uint64_t(b) * cap + (j0 - lo)] = c0;
+    if (j1 >= lo && j1 <= hi) out[uint64_t(b) * cap + (j1 - lo)] = c1;
+  }
+}
+
+// f == 0: the frontier is the root itself.
+__global__ void copy_roots_kernel(const uint8_t *__restrict__ keys, uint32_t kstride, uint32_t B,
+                                  uint4 *__restrict__ out, uint64_t cap) {
+  const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b < B) out[uint64_t(b) * cap] = key_root(keys + uint64_t(b) * kstride);
+}
+
+// ----------------------------------------------------------------- a3..a6: fused
+struct FusedParams {
+  const uint8_t *keys;
+  const uint4 *frontier;  // [B][cap], node i at depth f (absolute lo_f + i)
+  const uint32_t *T;      // shard base: row r0
+  uint32_t *shares;       // [B][D]
+  uint64_t cap;           // frontier stride per key
+  uint64_t F;             // frontier nodes per key
+  uint64_t lo_f;          // absolute index of frontier node 0
+  uint64_t r0, r1;        // valid absolute rows
+  uint32_t kstride, B, n, m, D;
+  uint32_t Kt, Ft, tasks;  // tasks = Kt * Ft <= 32 * NP (lanes >= tasks idle)
+  uint32_t W;              // leaf pairs per producer thread per window
+  uint32_t n_ktiles, n_items, nwin;  // windows per item = 2^(m-1) / W
+  uint32_t CG, KG;         // consumer col groups / key groups
+  uint32_t y_stage_words, t_stage_words;
+};
+
+template <int NP, int NC>
+struct Smem {
+  static constexpr int kThreads = 32 * (NP + NC + 1);
+};
+
+// Consumer: warp-tile of KPW keys x (32 * CPL) columns; lane owns columns
+// lane + 32*(cg*CPL + c), c < CPL.  y read as broadcast (same word for all
+// lanes), T read coalesced.  No column guard in the loop: columns >= D read
+// padding/next-row words whose products are never flushed.
+template <int KPW, int CPL>
+__device__ __forceinline__ void consume_window(const uint32_t *__restrict__ yb, const uint32_t *__restrict__ tb,
+                                               uint32_t nslots, uint32_t Kt, uint32_t D, uint32_t key0,
+                                               uint32_t colbase, uint32_t (&acc)[KPW][CPL]) {
+  const uint32_t *yp = yb + key0;
+  const uint32_t *tp = tb + colbase;
+#pragma unroll 2
+  for (uint32_t s = 0; s < nslots; ++s) {
+    uint32_t tv[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) tv[c] = tp[32 * c];
+    uint32_t yv[KPW];
+    if constexpr (KPW % 4 == 0) {
+#pragma unroll
+      for (int k = 0; k < KPW; k += 4) {
+        const uint4 v = *reinterpret_cast<const uint4 *>(yp + k);
+        yv[k] = v.x; yv[k + 1] = v.y; yv[k + 2] = v.z; yv[k + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < KPW; ++k) yv[k] = yp[k];
+    }
+#pragma unroll
+    for (int k = 0; k < KPW; ++k)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) acc[k][c] += yv[k] * tv[c];
+    yp += Kt;
+    tp += D;
+  }
+}
+
+template <int NP, int NC, int KPW, int CPL>
+__global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const FusedParams p) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem);  // yfull[2], tfull[2], empty[2]
+  uint64_t *yfull = bars, *tfull = bars + 2, *empty = bars + 4;
+  uint32_t *ybuf = reinterpret_cast<uint32_t *>(smem + 128);
+  uint32_t *tbuf = ybuf + 2 * p.y_stage_words;
+  uint4 *stack = reinterpret_cast<uint4 *>(tbuf + 2 * p.t_stage_words);
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&yfull[s], NP);
+      mbar_init(&tfull[s], 1);
+      mbar_init(&empty[s], NC);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const uint32_t nslots = p.Ft * 2 * p.W;
+  const uint32_t nq = 1u << (p.m - 1);
+
+  if (warp < NP) {
+    // ------------------------------------------------------------ producers
+    const uint32_t tix = warp * 32 + lane;
+    const bool lane_on = tix < p.tasks;
+    const uint32_t kl = lane_on ? tix % p.Kt : 0, nl = lane_on ? tix / p.Kt : 0;
+    uint32_t wseq = 0;
+    for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      const uint32_t kt = item % p.n_ktiles, ng = item / p.n_ktiles;
+      const uint32_t b = kt * p.Kt + kl;
+      const uint64_t node = uint64_t(ng) * p.Ft + nl;
+      const bool valid = lane_on && b < p.B && node < p.F;
+      const uint8_t *key = p.keys + uint64_t(valid ? b : 0) * p.kstride;
+      const uint32_t cw_out = key_cw_out(key);
+      uint4 cur = valid ? p.frontier[uint64_t(b) * p.cap + node] : make_uint4(0, 0, 0, 0);
+      const uint64_t row_base = (p.lo_f + node) << p.m;
+      uint32_t dep = 0;
+      for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
+        const uint32_t stage = wseq & 1, use = wseq >> 1;
+        if (use > 0) mbar_wait(&empty[stage], (use - 1) & 1);
+        uint32_t *yb = ybuf + stage * p.y_stage_words;
+        for (uint32_t qi = 0; qi < p.W; ++qi) {
+          const uint32_t q = win * p.W + qi;
+          // descend (warp-uniform: every thread shares the schedule)
+          while (dep + 1 < p.m) {
+            uint4 c0, c1;
+            node_children(cur, key_cw(key, p.n - p.m + dep + 1), c0, c1);
+            stack[(dep + 1) * (32 * NP) + tix] = c1;
+            cur = c0;
+            ++dep;
+          }
+          uint4 l0, l1;
+          node_children(cur, key_cw(key, p.n), l0, l1);
+          const uint64_t row = row_base + 2 * q;
+          const uint32_t y0 = (valid && row >= p.r0 && row < p.r1) ? leaf_value(l0, cw_out) : 0u;
+          const uint32_t y1 = (valid && row + 1 >= p.r0 && row + 1 < p.r1) ? leaf_value(l1, cw_out) : 0u;
+          if (lane_on) {
+            const uint32_t slot = nl * 2 * p.W + 2 * qi;
+            yb[slot * p.Kt + kl] = y0;
+            yb[(slot + 1) * p.Kt + kl] = y1;
+          }
+          if (q + 1 < nq) {  // pop: the right sibling at depth m-1-ctz(q+1)
+            const uint32_t k = p.m - 1 - (__ffs(q + 1) - 1);
+            cur = stack[k * (32 * NP) + tix];
+            dep = k;
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&yfull[stage]);
+      }
+    }
+  } else if (warp < NP + NC) {
+    // ------------------------------------------------------------ consumers
+    const uint32_t cwarp = warp - NP;
+    const uint32_t kg = cwarp / p.CG, cg = cwarp % p.CG;
+    const bool active = kg < p.KG;
+    const uint32_t key0 = kg * KPW;
+    const uint32_t colbase = cg * CPL * 32 + lane;
+    uint32_t acc[KPW][CPL];
+#pragma unroll
+    for (int k = 0; k < KPW; ++k)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) acc[k][c] = 0;
+    uint32_t wseq = 0;
+    for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      const uint32_t kt = item % p.n_ktiles;
+      for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
+        const uint32_t stage = wseq & 1, use = wseq >> 1;
+        mbar_wait(&yfull[stage], use & 1);
+        mbar_wait(&tfull[stage], use & 1);
+        if (active)
+          consume_window<KPW, CPL>(ybuf + stage * p.y_stage_words, tbuf + stage * p.t_stage_words, nslots, p.Kt,
+                                   p.D, key0, colbase, acc);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[stage]);
+      }
+      // a6/a7: flush this item's partial answers, party sign applied once.
+      if (active) {
+#pragma unroll
+        for (int k = 0; k < KPW; ++k) {
+          const uint32_t b = kt * p.Kt + key0 + k;
+          if (key0 + k < p.Kt && b < p.B) {
+            const uint32_t neg = key_party(p.keys + uint64_t(b) * p.kstride);
+#pragma unroll
+            for (int c = 0; c < CPL; ++c) {
+              const uint32_t col = colbase + 32 * c;
+              if (col < p.D) red_add_u32(p.shares + uint64_t(b) * p.D + col, neg ? 0u - acc[k][c] : acc[k][c]);
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) acc[k][c] = 0;
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ T loader
+    uint32_t wseq = 0;
+    const uint64_t seg_rows = 2 * p.W;
+    const uint32_t row_bytes = p.D * 4;
+    for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      const uint32_t ng = item / p.n_ktiles;
+      for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
+        const uint32_t stage = wseq & 1, use = wseq >> 1;
+        if (use > 0) mbar_wait(&empty[stage], (use - 1) & 1);
+        uint32_t *tb = tbuf + stage * p.t_stage_words;
+        uint32_t my_bytes = 0;
+        for (uint32_t nl = lane; nl < p.Ft; nl += 32) {
+          const uint64_t node = uint64_t(ng) * p.Ft + nl;
+          if (node >= p.F) continue;
+          const uint64_t s0 = ((p.lo_f + node) << p.m) + seg_rows * win;
+          const uint64_t a = s0 > p.r0 ? s0 : p.r0, e = (s0 + seg_rows) < p.r1 ? (s0 + seg_rows) : p.r1;
+          if (a < e) my_bytes += uint32_t(e - a) * row_bytes;
+        }
+        const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, my_bytes);
+        if (lane == 0) mbar_arrive_expect_tx(&tfull[stage], total);
+        __syncwarp();
+        for (uint32_t nl = lane; nl < p.Ft; nl += 32) {
+          const uint64_t node = uint64_t(ng) * p.Ft + nl;
+          if (node >= p.F) continue;
+          const uint64_t s0 = ((p.lo_f + node) << p.m) + seg_rows * win;
+          const uint64_t a = s0 > p.r0 ? s0 : p.r0, e = (s0 + seg_rows) < p.r1 ? (s0 + seg_rows) : p.r1;
+          if (a < e)
+            bulk_g2s(tb + (uint64_t(nl) * seg_rows + (a - s0)) * p.D, p.T + (a - p.r0) * p.D,
+                     uint32_t(e - a) * row_bytes, &tfull[stage]);
+        }
+      }
+    }
+  }
+}
+
+// Test/debug leaf dump (branch-parallel: n blocks per leaf).
+__global__ void eval_leaves_kernel(const uint8_t *__restrict__ keys, uint32_t kstride, uint32_t B, uint32_t n,
+                                   uint32_t *__restrict__ leaves) {
+  const uint64_t N = 1ull << n;
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < N * B;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t b = uint32_t(i >> n);
+    const uint64_t j = i & (N - 1);
+    const uint8_t *key = keys + uint64_t(b) * kstride;
+    uint4 s = key_root(key);
+    for (uint32_t d = 1; d <= n; ++d) {
+      uint4 c0, c1;
+      node_children(s, key_cw(key, d), c0, c1);
+      s = ((j >> (n - d)) & 1) ? c1 : c0;
+    }
+    const uint32_t v = leaf_value(s, key_cw_out(key));
+    leaves[i] = key_party(key) ? 0u - v : v;
+  }
+}
+
+}  // namespace dev
+
+// =================================================================== host side
+namespace {
+
+constexpr int kNP = 8;  // producer warps
+constexpr int kNC = 4;  // consumer warps
+constexpr size_t kAlign = 256;
+constexpr uint32_t kMaxTStageBytes = 64 * 1024;
+constexpr uint32_t kMaxTStageBytesW1 = 96 * 1024;
+
+inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+inline uint32_t pow2ceil(uint32_t v) {
+  uint32_t r = 1;
+  while (r < v) r <<= 1;
+  return r;
+}
+
+struct KernelChoice {
+  int KPW, CPL;
+  void (*fn)(const dev::FusedParams);
+};
+
+template <int KPW, int CPL>
+KernelChoice choice() {
+  return {KPW, CPL, &dev::fused_eval_kernel<kNP, kNC, KPW, CPL>};
+}
+
+struct Plan {
+  uint32_t n, m, f, Kt, Ft, tasks, W, CG, KG, n_ktiles, n_items, nwin, grid;
+  uint64_t r0, r1, F, lo_f, cap;
+  uint32_t y_stage_words, t_stage_words;
+  size_t smem_bytes;
+  KernelChoice kc;
+  uint64_t prf_blocks;
+};
+
+int num_sms() {
+  static int sms = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                  cudaSuccess)
+      sms = 148;
+  });
+  return sms;
+}
+
+// Consumer warp tiling for (Kt keys, D cols) over kNC warps: KG key groups x
+// CG col groups, KPW = Kt / KG, CPL = ceil(D / (32 CG)).
+bool pick_kernel(uint32_t Kt, uint32_t D, Plan &pl) {
+  struct Cand {
+    uint32_t CG;
+    KernelChoice kc;
+  };
+  // Preference order: fewest loads per IMAD first.
+  static const Cand cands[] = {
+      {2, choice<16, 4>()}, {1, choice<8, 2>()},  {4, choice<8, 4>()},  {1, choice<8, 1>()},
+      {2, choice<16, 2>()}, {1, choice<4, 2>()},  {1, choice<4, 1>()},  {2, choice<4, 4>()},
+      {4, choice<4, 4>()},  {2, choice<2, 2>()},  {1, choice<2, 1>()},  {2, choice<2, 4>()},
+      {4, choice<2, 4>()},  {4, choice<1, 4>()},  {4, choice<1, 2>()},  {4, choice<1, 1>()},
+      {2, choice<1, 4>()},  {2, choice<1, 1>()},  {1, choice<1, 1>()},  {4, choice<16, 4>()},
+      {4, choice<8, 8>()},  {4, choice<4, 8>()},  {4, choice<2, 8>()},  {4, choice<1, 8>()},
+  };
+  for (const Cand &c : cands) {
+    const uint32_t KG = kNC / c.CG;
+    if (Kt % uint32_t(c.kc.KPW)) continue;
+    if (Kt / c.kc.KPW > KG) continue;                      // not enough warps for the keys
+    if (Kt / c.kc.KPW < KG && c.kc.KPW > 1) continue;      // would leave key groups idle; prefer smaller KPW
+    const uint32_t cols = 32u * c.kc.CPL * c.CG;
+    if (cols < D) continue;                                // not enough columns
+    if (c.kc.CPL > 1 && 32u * (c.kc.CPL - 1) * c.CG >= D) continue;  // wasteful CPL
+    pl.CG = c.CG;
+    pl.KG = Kt / c.kc.KPW;
+    pl.kc = c.kc;
+    return true;
+  }
+  return false;
+}
+
+int make_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl) {
+  std::memset(&pl, 0, sizeof pl);
+  pl.n = n;
+  pl.r0 = r0;
+  pl.r1 = r0 + rows;
+  // Key tile: lanes <-> keys (Kt <= 32), remaining lanes <-> frontier nodes.
+  pl.Kt = std::min<uint32_t>(32, pow2ceil(B));
+  while (pl.Kt * D > 8192 && pl.Kt > 1) pl.Kt >>= 1;  // accumulator budget: Kt*D <= 8192 words/CTA
+  if (!pick_kernel(pl.Kt, D, pl)) return DPF_EINVAL;
+  pl.Ft = 32 * kNP / pl.Kt;
+  // T stage must fit: Ft * 2 rows * D words at W = 1.
+  while (uint64_t(pl.Ft) * 2 * D * 4 > kMaxTStageBytesW1 && pl.Ft > 1) pl.Ft >>= 1;
+  pl.tasks = pl.Kt * pl.Ft;
+  pl.n_ktiles = (B + pl.Kt - 1) / pl.Kt;
+  // Subtree depth m (frontier depth f = n - m): the largest m that still
+  // gives >= 8 work items per SM; m <= 14 keeps the SMEM stack small.
+  const uint64_t target = 8ull * num_sms();
+  uint32_t best_m = 1;
+  for (uint32_t m = std::min<uint32_t>(n, 14); m >= 1; --m) {
+    const uint64_t F = ((pl.r1 - 1) >> m) - (r0 >> m) + 1;
+    const uint64_t items = uint64_t(pl.n_ktiles) * ((F + pl.Ft - 1) / pl.Ft);
+    best_m = m;
+    if (items >= target) break;
+  }
+  pl.m = best_m;
+  pl.f = n - pl.m;
+  pl.lo_f = r0 >> pl.m;
+  pl.F = ((pl.r1 - 1) >> pl.m) - pl.lo_f + 1;
+  pl.cap = pl.F;
+  const uint64_t items = uint64_t(pl.n_ktiles) * ((pl.F + pl.Ft - 1) / pl.Ft);
+  if (items > 0x7FFFFFFFull) return DPF_EINVAL;
+  pl.n_items = uint32_t(items);
+  // Window: W leaf pairs per thread; T stage = Ft*2W rows, y stage = Kt*Ft*2W.
+  const uint32_t nq = 1u << (pl.m - 1);
+  uint32_t W = std::min<uint32_t>(8, nq);
+  while (W > 1 && uint64_t(pl.Ft) * 2 * W * D * 4 > kMaxTStageBytes) W >>= 1;
+  pl.W = W;
+  pl.nwin = nq / W;
+  pl.y_stage_words = uint32_t(align_up(size_t(pl.Kt) * pl.Ft * 2 * W, 32));
+  // + padding: lanes whose columns exceed D read past the last row.
+  pl.t_stage_words = uint32_t(align_up(size_t(pl.Ft) * 2 * W * D + 32u * pl.kc.CPL * pl.CG, 32));
+  const size_t stack_bytes = size_t(pl.m) * 32 * kNP * 16;
+  pl.smem_bytes = 128 + 4 * (2 * size_t(pl.y_stage_words) + 2 * size_t(pl.t_stage_words)) + stack_bytes;
+  if (pl.smem_bytes > 227 * 1024) return DPF_EINVAL;
+  pl.grid = std::min<uint32_t>(pl.n_items, uint32_t(num_sms()));
+  // PRF blocks: top levels (nodes intersecting the range) + fused subtrees.
+  uint64_t top = 0;
+  for (uint32_t k = 0; k < pl.f; ++k) top += ((pl.r1 - 1) >> (n - k)) - (r0 >> (n - k)) + 1;
+  pl.prf_blocks = uint64_t(B) * top + uint64_t(pl.n_items) * pl.tasks * ((1ull << pl.m) - 1);
+  return DPF_OK;
+}
+
+struct Workspace {
+  uint4 *front[2];
+  uint8_t *keys;
+  size_t bytes;
+};
+
+size_t layout(const Plan &pl, uint32_t B, size_t kstride, Workspace *ws, void *base) {
+  size_t off = 0;
+  const size_t fbytes = align_up(size_t(B) * pl.cap * 16, kAlign);
+  const size_t kbytes = align_up(size_t(B) * kstride, kAlign);
+  if (ws) {
+    uint8_t *b = static_cast<uint8_t *>(base);
+    ws->front[0] = reinterpret_cast<uint4 *>(b + off);
+    ws->front[1] = reinterpret_cast<uint4 *>(b + off + fbytes);
+    ws->keys = b + off + 2 * fbytes;
+  }
+  off += 2 * fbytes + kbytes;
+  return off;
+}
+
+thread_local dpf_eval_stats g_stats{};
+
+// Per-thread pinned staging ring for host keys (2 slots, grown on demand).
+struct Staging {
+  uint8_t *buf[2] = {nullptr, nullptr};
+  size_t cap[2] = {0, 0};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  int next = 0;
+  ~Staging() {
+    for (int i = 0; i < 2; ++i) {
+      if (buf[i]) cudaFreeHost(buf[i]);
+      if (done[i]) cudaEventDestroy(done[i]);
+    }
+  }
+};
+thread_local Staging g_staging;
+
+int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint32_t B, const uint32_t *table,
+                uint32_t D, uint32_t *out, const Workspace &ws, cudaStream_t st, uint32_t *kernels) {
+  uint32_t nk = 0;
+  if (cudaMemsetAsync(out, 0, size_t(B) * D * 4, st) != cudaSuccess) return DPF_ECUDA;
+  // a2: levels 1..f; level k lands in front[(f-k)&1] so level f is front[0].
+  if (pl.f == 0) {
+    dev::copy_roots_kernel<<<(B + 127) / 128, 128, 0, st>>>(keys_dev, kstride, B, ws.front[0], pl.cap);
+    ++nk;
+  }
+  for (uint32_t k = 1; k <= pl.f; ++k) {
+    const uint64_t np = ((pl.r1 - 1) >> (pl.n - (k - 1))) - (pl.r0 >> (pl.n - (k - 1))) + 1;
+    const uint64_t total = np * B;
+    const uint32_t grid = uint32_t(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
+    dev::expand_level_kernel<<<grid, 256, 0, st>>>(keys_dev, kstride, B, pl.n, k, pl.r0, pl.r1,
+                                                   ws.front[(pl.f - k + 1) & 1], ws.front[(pl.f - k) & 1], pl.cap);
+    ++nk;
+  }
+  dev::FusedParams p;
+  p.keys = keys_dev;
+  p.frontier = ws.front[0];
+  p.T = table;
+  p.shares = out;
+  p.cap = pl.cap;
+  p.F = pl.F;
+  p.lo_f = pl.lo_f;
+  p.r0 = pl.r0;
+  p.r1 = pl.r1;
+  p.kstride = kstride;
+  p.B = B;
+  p.n = pl.n;
+  p.m = pl.m;
+  p.D = D;
+  p.Kt = pl.Kt;
+  p.Ft = pl.Ft;
+  p.tasks = pl.tasks;
+  p.W = pl.W;
+  p.n_ktiles = pl.n_ktiles;
+  p.n_items = pl.n_items;
+  p.nwin = pl.nwin;
+  p.CG = pl.CG;
+  p.KG = pl.KG;
+  p.y_stage_words = pl.y_stage_words;
+  p.t_stage_words = pl.t_stage_words;
+  if (cudaFuncSetAttribute(pl.kc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) !=
+      cudaSuccess)
+    return DPF_ECUDA;
+  pl.kc.fn<<<pl.grid, 32 * (kNP + kNC + 1), pl.smem_bytes, st>>>(p);
+  ++nk;
+  if (cudaGetLastError() != cudaSuccess) return DPF_ECUDA;
+  if (kernels) *kernels = nk;
+  return DPF_OK;
+}
+
+int check_common(uint32_t B, const uint32_t *table, uint64_t row_begin, uint64_t rows, uint32_t D,
+                 const uint32_t *out, void *ws, uint32_t n) {
+  if (B == 0 || !table || !out || !ws || D == 0 || D > 1024 || (D & 3)) return DPF_EINVAL;
+  if (n < 1 || n > DPF_MAX_LOG_N) return DPF_EKEY;
+  if (rows == 0) return DPF_EINVAL;
+  const uint64_t dom = n >= 64 ? ~0ull : (1ull << n);
+  if (row_begin >= dom || rows > dom - row_begin) return DPF_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(table) & 15) || (reinterpret_cast<uintptr_t>(ws) & (kAlign - 1)))
+    return DPF_EINVAL;
+  return DPF_OK;
+}
+
+int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uint32_t log_n,
+              const uint32_t *table, uint64_t row_begin, uint64_t rows, uint32_t D, uint32_t *out, void *workspace,
+              size_t ws_bytes, cudaStream_t st) {
+  uint32_t n = log_n;
+  if (keys) {
+    if (B == 0) return DPF_EINVAL;
+    n = keys[0].log_n;
+    for (uint32_t b = 0; b < B; ++b) {
+      if (!host_key_valid(keys[b])) return keys[b].prf == DPF_PRF_AES128 ? DPF_EUNSUPPORTED : DPF_EKEY;
+      if (keys[b].log_n != n || keys[b].prf != keys[0].prf) return DPF_EKEY;
+    }
+  }
+  int rc = check_common(B, table, row_begin, rows, D, out, workspace, n);
+  if (rc) return rc;
+  Plan pl;
+  rc = make_plan(B, n, row_begin, rows, D, pl);
+  if (rc) return rc;
+  const uint32_t kstride = uint32_t(dpf_key_wire_size(n));
+  Workspace ws;
+  const size_t need = layout(pl, B, kstride, &ws, workspace);
+  if (ws_bytes < need) return DPF_ENOMEM;
+  const uint8_t *kd = keys_wire_dev;
+  if (keys) {
+    // a1: serialize into pinned staging, then one H2D copy (async).
+    Staging &sg = g_staging;
+    const int slot = sg.next;
+    sg.next ^= 1;
+    const size_t kb = size_t(B) * kstride;
+    if (sg.done[slot]) cudaEventSynchronize(sg.done[slot]);  // previous use of this slot finished copying
+    if (sg.cap[slot] < kb) {
+      if (sg.buf[slot]) cudaFreeHost(sg.buf[slot]);
+      sg.buf[slot] = nullptr;
+      sg.cap[slot] = 0;
+      if (cudaHostAlloc(&sg.buf[slot], kb, cudaHostAllocDefault) != cudaSuccess) return DPF_ECUDA;
+      sg.cap[slot] = kb;
+    }
+    if (!sg.done[slot] && cudaEventCreateWithFlags(&sg.done[slot], cudaEventDisableTiming) != cudaSuccess)
+      return DPF_ECUDA;
+    for (uint32_t b = 0; b < B; ++b) {
+      size_t w = 0;
+      if (dpf_key_serialize(&keys[b], sg.buf[slot] + size_t(b) * kstride, kstride, &w) != DPF_OK) return DPF_EKEY;
+    }
+    if (cudaMemcpyAsync(ws.keys, sg.buf[slot], kb, cudaMemcpyHostToDevice, st) != cudaSuccess) return DPF_ECUDA;
+    if (cudaEventRecord(sg.done[slot], st) != cudaSuccess) return DPF_ECUDA;
+    kd = ws.keys;
+  }
+  uint32_t nk = 0;
+  rc = launch_eval(pl, kd, kstride, B, table, D, out, ws, st, &nk);
+  if (rc) return rc;
+  g_stats.prf_blocks = pl.prf_blocks;
+  g_stats.kernels = nk;
+  g_stats.frontier_depth = pl.f;
+  g_stats.keys_per_tile = pl.Kt;
+  g_stats.nodes_per_tile = pl.Ft;
+  g_stats.work_items = pl.n_items;
+  g_stats.grid = pl.grid;
+  return DPF_OK;
+}
+
+}  // namespace
+}  // namespace dpfpir
+
+using namespace dpfpir;
+
+extern "C" size_t dpf_eval_workspace_bytes(uint32_t B, uint32_t log_n, uint64_t row_count, uint32_t D) {
+  if (B == 0 || log_n < 1 || log_n > DPF_MAX_LOG_N || row_count == 0 || D == 0 || D > 1024 || (D & 3)) return 0;
+  Plan pl;
+  if (make_plan(B, log_n, 0, row_count, D, pl) != DPF_OK) return 0;
+  // The frontier size depends on the alignment of row_begin; size for the
+  // worst case (one extra node per key).
+  pl.cap += 1;
+  return layout(pl, B, dpf_key_wire_size(log_n), nullptr, nullptr);
+}
+
+extern "C" int dpf_eval_batch_shard(const dpf_key *keys, uint32_t B, const uint32_t *table_shard,
+                                    uint64_t row_begin, uint64_t row_count, uint32_t D, uint32_t *partial,
+                                    void *workspace, size_t workspace_bytes, void *stream) {
+  if (!keys) return DPF_EINVAL;
+  return eval_impl(keys, B, nullptr, 0, table_shard, row_begin, row_count, D, partial, workspace, workspace_bytes,
+                   static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int dpf_eval_batch(const dpf_key *keys, uint32_t B, const uint32_t *table, uint64_t N, uint32_t D,
+                              uint32_t *shares, void *workspace, size_t workspace_bytes, void *stream) {
+  return dpf_eval_batch_shard(keys, B, table, 0, N, D, shares, workspace, workspace_bytes, stream);
+}
+
+extern "C" int dpf_eval_batch_wire(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n,
+                                   const uint32_t *table_shard, uint64_t row_begin, uint64_t row_count, uint32_t D,
+                                   uint32_t *partial, void *workspace, size_t workspace_bytes, void *stream) {
+  if (!keys_wire_dev || (reinterpret_cast<uintptr_t>(keys_wire_dev) & 15)) return DPF_EINVAL;
+  return eval_impl(nullptr, B, keys_wire_dev, log_n, table_shard, row_begin, row_count, D, partial, workspace,
+                   workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int dpf_serve_batch(const dpf_key *keys, uint32_t B, const uint32_t *table_shard, uint64_t row_begin,
+                               uint64_t row_count, uint32_t D, uint32_t *shares_host, void *workspace,
+                               size_t workspace_bytes, void *stream) {
+  if (!shares_host) return DPF_EINVAL;
+  // The device answer lives at the end of the workspace.
+  const size_t need = dpf_eval_workspace_bytes(B, keys ? keys[0].log_n : 0, row_count, D);
+  const size_t out_bytes = align_up(size_t(B) * D * 4, kAlign);
+  if (!keys || need == 0) return DPF_EINVAL;
+  if (workspace_bytes < need + out_bytes) return DPF_ENOMEM;
+  uint32_t *dev_out = reinterpret_cast<uint32_t *>(static_cast<uint8_t *>(workspace) + need);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = eval_impl(keys, B, nullptr, 0, table_shard, row_begin, row_count, D, dev_out, workspace, need, st);
+  if (rc) return rc;
+  if (cudaMemcpyAsync(shares_host, dev_out, size_t(B) * D * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return DPF_ECUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return DPF_ECUDA;
+  return DPF_OK;
+}
+
+extern "C" int dpf_eval_leaves(const dpf_key *keys, uint32_t B, uint32_t *leaves, void *workspace,
+                               size_t workspace_bytes, void *stream) {
+  if (!keys || B == 0 || !leaves || !workspace) return DPF_EINVAL;
+  const uint32_t n = keys[0].log_n;
+  for (uint32_t b = 0; b < B; ++b)
+    if (!host_key_valid(keys[b]) || keys[b].log_n != n) return DPF_EKEY;
+  if (n > 20) return DPF_EINVAL;
+  const uint32_t kstride = uint32_t(dpf_key_wire_size(n));
+  if (workspace_bytes < size_t(B) * kstride) return DPF_ENOMEM;
+  std::vector<uint8_t> staged(size_t(B) * kstride);
+  for (uint32_t b = 0; b < B; ++b) dpf_key_serialize(&keys[b], staged.data() + size_t(b) * kstride, kstride, nullptr);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (cudaMemcpyAsync(workspace, staged.data(), staged.size(), cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return DPF_ECUDA;
+  const uint64_t total = (uint64_t(B) << n);
+  const uint32_t grid = uint32_t(std::min<uint64_t>((total + 255) / 256, 148ull * 8));
+  dev::eval_leaves_kernel<<<grid, 256, 0, st>>>(static_cast<uint8_t *>(workspace), kstride, B, n, leaves);
+  if (cudaGetLastError() != cudaSuccess) return DPF_ECUDA;
+  // staged is pageable: the H2D above completed its staging before return.
+  return DPF_OK;
+}
+
+extern "C" int dpf_last_eval_stats(dpf_eval_stats *out) {
+  if (!out) return DPF_EINVAL;
+  *out = g_stats;
+  return DPF_OK;
+}

@@ -1,0 +1,314 @@
+"""Thin Python binding of libdpfpir (include/dpfpir.h): argument marshalling only.
+
+Every step of the evaluation runs in the CUDA library; this module only turns
+numpy arrays / torch tensors into pointers and sizes.  PyTorch supplies device
+memory (tables, shares, workspace) and streams.  There is no CPU fallback: if
+libdpfpir.so is missing or no CUDA device is present, the device entry points
+raise.
+
+Names follow the C ABI: gen, key_serialize, key_deserialize, reconstruct,
+eval_workspace_bytes, eval_batch, eval_batch_shard, eval_batch_wire,
+serve_batch, eval_leaves, last_eval_stats.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Iterable, Optional, Sequence
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdpfpir.so")
+
+DPF_MAX_LOG_N = 32
+DPF_PRF_CHACHA20 = 1
+DPF_PRF_AES128 = 2
+DPF_OK, DPF_EINVAL, DPF_EKEY, DPF_ENOMEM, DPF_ECUDA, DPF_EUNSUPPORTED = 0, -1, -2, -3, -4, -6
+
+
+class DpfError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__("%s: %s (%d)" % (what, strerror(code), code))
+        self.code = code
+
+
+class DpfKey(ctypes.Structure):
+    """dpf_key (include/dpfpir.h), 2080 bytes, POD."""
+    _fields_ = [("magic", ctypes.c_uint32), ("version", ctypes.c_uint8), ("prf", ctypes.c_uint8),
+                ("party", ctypes.c_uint8), ("log_n", ctypes.c_uint8), ("cw_out", ctypes.c_uint32),
+                ("reserved", ctypes.c_uint32), ("root", ctypes.c_uint8 * 16),
+                ("cw", ctypes.c_uint8 * (DPF_MAX_LOG_N * 2 * 2 * 16))]
+
+
+class DpfEvalStats(ctypes.Structure):
+    _fields_ = [("prf_blocks", ctypes.c_uint64), ("kernels", ctypes.c_uint32), ("frontier_depth", ctypes.c_uint32),
+                ("keys_per_tile", ctypes.c_uint32), ("nodes_per_tile", ctypes.c_uint32),
+                ("work_items", ctypes.c_uint32), ("grid", ctypes.c_uint32)]
+
+
+KEY_BYTES = ctypes.sizeof(DpfKey)
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libdpfpir.so (built by __graft_entry__.build() / `python -m
+    paper_2301_10904_b200.build`).  Raises if it is missing: no fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError("libdpfpir.so not built (%s); run `python -m paper_2301_10904_b200.build`" % LIB_PATH)
+    L = ctypes.CDLL(LIB_PATH)
+    vp, sz, u32, u64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint32, ctypes.c_uint64
+    L.dpf_gen.argtypes = [u32, u64, u32, u32, vp, vp, vp]
+    L.dpf_key_wire_size.argtypes = [u32]
+    L.dpf_key_wire_size.restype = sz
+    L.dpf_key_serialize.argtypes = [vp, vp, sz, ctypes.POINTER(sz)]
+    L.dpf_key_deserialize.argtypes = [vp, sz, vp]
+    L.dpf_reconstruct.argtypes = [vp, vp, sz, vp]
+    L.dpf_eval_workspace_bytes.argtypes = [u32, u32, u64, u32]
+    L.dpf_eval_workspace_bytes.restype = sz
+    L.dpf_eval_batch.argtypes = [vp, u32, vp, u64, u32, vp, vp, sz, vp]
+    L.dpf_eval_batch_shard.argtypes = [vp, u32, vp, u64, u64, u32, vp, vp, sz, vp]
+    L.dpf_eval_batch_wire.argtypes = [vp, u32, u32, vp, u64, u64, u32, vp, vp, sz, vp]
+    L.dpf_serve_batch.argtypes = [vp, u32, vp, u64, u64, u32, vp, vp, sz, vp]
+    L.dpf_eval_leaves.argtypes = [vp, u32, vp, vp, sz, vp]
+    L.dpf_last_eval_stats.argtypes = [vp]
+    L.dpf_strerror.argtypes = [ctypes.c_int]
+    L.dpf_strerror.restype = ctypes.c_char_p
+    L.dpf_version.restype = ctypes.c_char_p
+    assert KEY_BYTES == 2080
+    _lib = L
+    return L
+
+
+EXPORTED_SYMBOLS = ("dpf_gen", "dpf_key_wire_size", "dpf_key_serialize", "dpf_key_deserialize", "dpf_reconstruct",
+                    "dpf_eval_workspace_bytes", "dpf_eval_batch", "dpf_eval_batch_shard", "dpf_eval_batch_wire",
+                    "dpf_serve_batch", "dpf_eval_leaves", "dpf_last_eval_stats", "dpf_strerror", "dpf_version")
+
+
+def strerror(code: int) -> str:
+    try:
+        return lib().dpf_strerror(code).decode()
+    except RuntimeError:
+        return "status %d" % code
+
+
+def _check(rc: int, what: str) -> None:
+    if rc != DPF_OK:
+        raise DpfError(rc, what)
+
+
+# ------------------------------------------------------------------ keys (host)
+
+class KeyBatch:
+    """B dpf_key records in one contiguous host buffer (numpy uint8 [B, 2080])."""
+
+    def __init__(self, raw: np.ndarray):
+        assert raw.dtype == np.uint8 and raw.ndim == 2 and raw.shape[1] == KEY_BYTES
+        self.raw = np.ascontiguousarray(raw)
+
+    @classmethod
+    def from_keys(cls, keys: Iterable[DpfKey]) -> "KeyBatch":
+        keys = list(keys)
+        raw = np.zeros((len(keys), KEY_BYTES), np.uint8)
+        for i, k in enumerate(keys):
+            ctypes.memmove(raw[i].ctypes.data, ctypes.addressof(k), KEY_BYTES)
+        return cls(raw)
+
+    def __len__(self) -> int:
+        return self.raw.shape[0]
+
+    def __getitem__(self, i: int) -> DpfKey:
+        return DpfKey.from_buffer_copy(self.raw[i].tobytes())
+
+    @property
+    def ptr(self) -> int:
+        return self.raw.ctypes.data
+
+    @property
+    def log_n(self) -> int:
+        return int(self.raw[0, 7])
+
+
+def _as_batch(keys) -> KeyBatch:
+    if isinstance(keys, KeyBatch):
+        return keys
+    if isinstance(keys, DpfKey):
+        return KeyBatch.from_keys([keys])
+    return KeyBatch.from_keys(keys)
+
+
+def gen(log_n: int, alpha: int, beta: int = 1, rng_seed: Optional[bytes] = None,
+        prf: int = DPF_PRF_CHACHA20) -> tuple[DpfKey, DpfKey]:
+    """dpf_gen: (k0, k1) with Eval(k0,j)+Eval(k1,j) = beta [j == alpha] mod 2^32."""
+    k0, k1 = DpfKey(), DpfKey()
+    seed = None
+    if rng_seed is not None:
+        assert len(rng_seed) == 32
+        seed = ctypes.create_string_buffer(bytes(rng_seed), 32)
+    _check(lib().dpf_gen(log_n, alpha, beta & 0xFFFFFFFF, prf, seed, ctypes.byref(k0), ctypes.byref(k1)), "dpf_gen")
+    return k0, k1
+
+
+def key_wire_size(log_n: int) -> int:
+    return lib().dpf_key_wire_size(log_n)
+
+
+def key_serialize(k: DpfKey) -> bytes:
+    n = key_wire_size(k.log_n)
+    buf = ctypes.create_string_buffer(max(n, 1))
+    written = ctypes.c_size_t(0)
+    _check(lib().dpf_key_serialize(ctypes.byref(k), buf, n, ctypes.byref(written)), "dpf_key_serialize")
+    return buf.raw[:written.value]
+
+
+def key_deserialize(b: bytes) -> DpfKey:
+    k = DpfKey()
+    buf = ctypes.create_string_buffer(bytes(b), max(len(b), 1))
+    _check(lib().dpf_key_deserialize(buf, len(b), ctypes.byref(k)), "dpf_key_deserialize")
+    return k
+
+
+def reconstruct(share0: np.ndarray, share1: np.ndarray) -> np.ndarray:
+    s0 = np.ascontiguousarray(share0, dtype=np.uint32)
+    s1 = np.ascontiguousarray(share1, dtype=np.uint32)
+    assert s0.shape == s1.shape
+    out = np.empty_like(s0)
+    _check(lib().dpf_reconstruct(s0.ctypes.data, s1.ctypes.data, s0.size, out.ctypes.data), "dpf_reconstruct")
+    return out
+
+
+# ------------------------------------------------------------------ device
+
+def eval_workspace_bytes(B: int, log_n: int, rows: int, D: int) -> int:
+    return lib().dpf_eval_workspace_bytes(B, log_n, rows, D)
+
+
+_ws_cache: dict = {}
+
+
+def _workspace(nbytes: int, device):
+    import torch
+    key = (str(device),)
+    ws = _ws_cache.get(key)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
+        _ws_cache[key] = ws
+    return ws
+
+
+def _stream_ptr(stream) -> int:
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream)
+
+
+def _check_table(table):
+    import torch
+    if not table.is_cuda:
+        raise ValueError("table must be a CUDA tensor (server state lives in HBM)")
+    if table.dtype not in (torch.int32, torch.uint32) or table.dim() != 2 or not table.is_contiguous():
+        raise ValueError("table must be a contiguous 2-D int32/uint32 CUDA tensor")
+
+
+def eval_batch_shard(keys, table_shard, row_begin: int = 0, out=None, workspace=None, stream=None):
+    """dpf_eval_batch_shard: partial[b][d] = sum_j Eval(k_b, row_begin+j) * table_shard[j][d] mod 2^32.
+    Returns an int32 CUDA tensor [B, D] (uint32 bit patterns)."""
+    import torch
+    kb = _as_batch(keys)
+    _check_table(table_shard)
+    rows, D = table_shard.shape
+    B = len(kb)
+    if out is None:
+        out = torch.empty((B, D), dtype=torch.int32, device=table_shard.device)
+    need = eval_workspace_bytes(B, kb.log_n, rows, D)
+    if need == 0:
+        raise DpfError(DPF_EINVAL, "dpf_eval_workspace_bytes")
+    ws = workspace if workspace is not None else _workspace(need, table_shard.device)
+    _check(lib().dpf_eval_batch_shard(kb.ptr, B, table_shard.data_ptr(), row_begin, rows, D, out.data_ptr(),
+                                      ws.data_ptr(), ws.numel() * ws.element_size(), _stream_ptr(stream)),
+           "dpf_eval_batch_shard")
+    return out
+
+
+def eval_batch(keys, table, out=None, workspace=None, stream=None):
+    """dpf_eval_batch: shares[b][d] = sum_{j<N} Eval(k_b, j) * table[j][d] mod 2^32."""
+    return eval_batch_shard(keys, table, 0, out, workspace, stream)
+
+
+def keys_to_wire(keys) -> np.ndarray:
+    """Serialize a key batch into consecutive wire records (uint8 [B, 32+64n])."""
+    kb = _as_batch(keys)
+    w = key_wire_size(kb.log_n)
+    out = np.zeros((len(kb), w), np.uint8)
+    written = ctypes.c_size_t(0)
+    for i in range(len(kb)):
+        _check(lib().dpf_key_serialize(kb.ptr + i * KEY_BYTES, out[i].ctypes.data, w, ctypes.byref(written)),
+               "dpf_key_serialize")
+    return out
+
+
+def eval_batch_wire(keys_wire_dev, log_n: int, table_shard, row_begin: int = 0, out=None, workspace=None,
+                    stream=None):
+    """dpf_eval_batch_wire: keys already in HBM as wire records (uint8 CUDA tensor [B, 32+64n])."""
+    import torch
+    _check_table(table_shard)
+    rows, D = table_shard.shape
+    B = keys_wire_dev.shape[0]
+    if out is None:
+        out = torch.empty((B, D), dtype=torch.int32, device=table_shard.device)
+    need = eval_workspace_bytes(B, log_n, rows, D)
+    ws = workspace if workspace is not None else _workspace(need, table_shard.device)
+    _check(lib().dpf_eval_batch_wire(keys_wire_dev.data_ptr(), B, log_n, table_shard.data_ptr(), row_begin, rows, D,
+                                     out.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(),
+                                     _stream_ptr(stream)), "dpf_eval_batch_wire")
+    return out
+
+
+def serve_workspace_bytes(B: int, log_n: int, rows: int, D: int) -> int:
+    return eval_workspace_bytes(B, log_n, rows, D) + (B * D * 4 + 255) // 256 * 256
+
+
+def serve_batch(keys, table_shard, shares_host, row_begin: int = 0, workspace=None, stream=None):
+    """dpf_serve_batch: host keys in, host answers out (synchronous)."""
+    kb = _as_batch(keys)
+    _check_table(table_shard)
+    rows, D = table_shard.shape
+    B = len(kb)
+    need = serve_workspace_bytes(B, kb.log_n, rows, D)
+    ws = workspace if workspace is not None else _workspace(need, table_shard.device)
+    if isinstance(shares_host, np.ndarray):
+        assert shares_host.dtype in (np.uint32, np.int32) and shares_host.size >= B * D
+        hptr = shares_host.ctypes.data
+    else:
+        assert not shares_host.is_cuda and shares_host.numel() >= B * D
+        hptr = shares_host.data_ptr()
+    _check(lib().dpf_serve_batch(kb.ptr, B, table_shard.data_ptr(), row_begin, rows, D, hptr, ws.data_ptr(),
+                                 ws.numel() * ws.element_size(), _stream_ptr(stream)), "dpf_serve_batch")
+    return shares_host
+
+
+def eval_leaves(keys, device="cuda", stream=None):
+    """dpf_eval_leaves (test/debug): leaves[b][j] = Eval(k_b, j), log_n <= 20."""
+    import torch
+    kb = _as_batch(keys)
+    B, n = len(kb), kb.log_n
+    out = torch.empty((B, 1 << n), dtype=torch.int32, device=device)
+    ws = _workspace(B * key_wire_size(n) + 256, out.device)
+    _check(lib().dpf_eval_leaves(kb.ptr, B, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
+           "dpf_eval_leaves")
+    return out
+
+
+def last_eval_stats() -> dict:
+    s = DpfEvalStats()
+    _check(lib().dpf_last_eval_stats(ctypes.byref(s)), "dpf_last_eval_stats")
+    return {f: getattr(s, f) for f, _ in DpfEvalStats._fields_}
+
+
+def as_u32(t) -> np.ndarray:
+    """CUDA/CPU int32 tensor -> numpy uint32 (bit patterns)."""
+    return t.detach().cpu().numpy().view(np.uint32)

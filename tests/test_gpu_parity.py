@@ -1,0 +1,160 @@
+"""GPU parity: the CUDA path (through the C ABI) equals the CPU oracle
+bit-exactly on the same seeded keys and tables (integer work: the bar is
+bit-exact).  Sizes span several work items, windows and
+ragged tails; full BASELINE sizes are checked on sampled keys."""
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def dp():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2301_10904_b200 import build as pbuild
+    from paper_2301_10904_b200 import dpfpir
+    pbuild.build()
+    dpfpir.lib()
+    return dpfpir
+
+
+def make_keys(dp, oracle, n, alphas, seed, parties=None, betas=None):
+    seeds = synth.gen_seeds(len(alphas), seed)
+    keys, okeys = [], []
+    for i, (a, s) in enumerate(zip(alphas, seeds)):
+        beta = 1 if betas is None else int(betas[i])
+        pair = dp.gen(n, int(a), beta, s)
+        p = (i % 2) if parties is None else parties[i]
+        keys.append(pair[p])
+        okeys.append(oracle.key_from_wire(dp.key_serialize(pair[p])))
+    return keys, okeys
+
+
+def to_dev(T):
+    return torch.from_numpy(T.view(np.int32)).cuda()
+
+
+def run_case(dp, oracle, n, N, D, B, seed, row_begin=0, rows=None, betas=None):
+    rows = N - row_begin if rows is None else rows
+    T = synth.table(N, D, seed)
+    al = synth.alphas(B, N, seed)
+    keys, okeys = make_keys(dp, oracle, n, al, seed, betas=betas)
+    Tsh = T[row_begin:row_begin + rows]
+    got = dp.as_u32(dp.eval_batch_shard(keys, to_dev(Tsh), row_begin))
+    torch.cuda.synchronize()
+    want = oracle.answer_batch(okeys, Tsh, row_begin=row_begin, threads=8)
+    np.testing.assert_array_equal(got, want)
+    return got
+
+
+def test_leaves_match_oracle_eval_full(dp, oracle):
+    for n, B in ((1, 1), (3, 2), (10, 3), (14, 2)):
+        keys, okeys = make_keys(dp, oracle, n, synth.alphas(B, 1 << n, n), n)
+        got = dp.as_u32(dp.eval_leaves(keys))
+        for b in range(B):
+            np.testing.assert_array_equal(got[b], oracle.eval_full(okeys[b]))
+
+
+def test_c1_exhaustive_two_servers(dp, oracle):
+    """Config c1 (BJ:7): 2^10 x 16, every alpha, both servers in-process."""
+    w = synth.CONFIGS["c1"]
+    T = synth.table(w.N, w.D, w.seed)
+    Td = to_dev(T)
+    seeds = synth.gen_seeds(w.N, w.seed)
+    pairs = [dp.gen(w.log_n, a, 1, seeds[a]) for a in range(w.N)]
+    sh = [dp.as_u32(dp.eval_batch([p[x] for p in pairs], Td)) for x in (0, 1)]
+    np.testing.assert_array_equal(dp.reconstruct(sh[0], sh[1]), T)          # row alpha for every alpha
+    for x in (0, 1):                                                          # bit-exact vs oracle
+        ok = [oracle.key_from_wire(dp.key_serialize(p[x])) for p in pairs[:64]]
+        np.testing.assert_array_equal(sh[x][:64], oracle.answer_batch(ok, T, threads=8))
+    for a in (0, 511, 1023):                                                  # batch 1 (the config's B)
+        s0 = dp.as_u32(dp.eval_batch([pairs[a][0]], Td))
+        s1 = dp.as_u32(dp.eval_batch([pairs[a][1]], Td))
+        np.testing.assert_array_equal(s0[0], sh[0][a])
+        np.testing.assert_array_equal(dp.reconstruct(s0, s1)[0], T[a])
+
+
+@pytest.mark.parametrize("n,N,D,B", [
+    (9, 512, 4, 1), (12, 4096, 64, 37), (13, 5000, 32, 64), (11, 2048, 256, 33), (10, 1000, 12, 3),
+    (14, 1 << 14, 16, 100), (15, 20000, 128, 40), (8, 256, 1024, 9), (12, 4096, 512, 16), (6, 64, 64, 70),
+    (1, 2, 8, 5), (2, 3, 4, 2),
+])
+def test_parity_shapes(dp, oracle, n, N, D, B):
+    run_case(dp, oracle, n, N, D, B, seed=1000 * n + D + B)
+
+
+def test_parity_c2_full(dp, oracle):
+    w = synth.CONFIGS["c2"]
+    run_case(dp, oracle, w.log_n, w.N, w.D, w.B, w.seed)
+    st = dp.last_eval_stats()
+    assert st["prf_blocks"] == w.B * (w.N - 1)  # N-1 blocks per key: optimal work
+
+
+def test_random_beta_and_wrap(dp, oracle):
+    n, N, D, B = 12, 4096, 32, 48
+    betas = synth.betas(B, 7, random=True)
+    run_case(dp, oracle, n, N, D, B, seed=7, betas=betas)
+    # adversarial wrap: all-ones table and beta = 2^32 - 1
+    T = np.full((N, D), 0xFFFFFFFF, np.uint32)
+    pair = dp.gen(n, 5, 0xFFFFFFFF, bytes(range(32)))
+    keys = [pair[0], pair[1], pair[0], pair[1]]
+    okeys = [oracle.key_from_wire(dp.key_serialize(k)) for k in keys]
+    got = dp.as_u32(dp.eval_batch(keys, to_dev(T)))
+    np.testing.assert_array_equal(got, oracle.answer_batch(okeys, T))
+    np.testing.assert_array_equal(dp.reconstruct(got[0], got[1]), np.ones(D, np.uint32))
+
+
+def test_shard_linearity(dp, oracle):
+    n, N, D, B = 14, 12345, 64, 40
+    T = synth.table(N, D, 9)
+    keys, okeys = make_keys(dp, oracle, n, synth.alphas(B, N, 9), 9)
+    whole = dp.as_u32(dp.eval_batch(keys, to_dev(T)))
+    np.testing.assert_array_equal(whole, oracle.answer_batch(okeys, T, threads=8))
+    for cuts in ([0, 4096, 8192, N], [0, 1, 777, 5000, 12000, N], [0, N // 2, N]):
+        acc = np.zeros_like(whole)
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            part = dp.as_u32(dp.eval_batch_shard(keys, to_dev(T[lo:hi]), lo))
+            np.testing.assert_array_equal(part, oracle.answer_batch(okeys, T[lo:hi], row_begin=lo, threads=8))
+            acc += part
+        np.testing.assert_array_equal(acc, whole)
+
+
+def test_wire_and_serve_paths(dp, oracle):
+    n, N, D, B = 12, 4096, 64, 32
+    T = synth.table(N, D, 11)
+    Td = to_dev(T)
+    keys, okeys = make_keys(dp, oracle, n, synth.alphas(B, N, 11), 11)
+    ref = dp.as_u32(dp.eval_batch(keys, Td))
+    wire = torch.from_numpy(dp.keys_to_wire(keys)).cuda()
+    np.testing.assert_array_equal(dp.as_u32(dp.eval_batch_wire(wire, n, Td)), ref)
+    host = torch.empty((B, D), dtype=torch.int32).pin_memory()
+    dp.serve_batch(keys, Td, host)
+    np.testing.assert_array_equal(host.numpy().view(np.uint32), ref)
+    np.testing.assert_array_equal(ref, oracle.answer_batch(okeys, T, threads=8))
+    again = dp.as_u32(dp.eval_batch(keys, Td))  # deterministic
+    np.testing.assert_array_equal(again, ref)
+
+
+def test_full_size_c3_sampled(dp, oracle):
+    """BASELINE config c3 (2^20 x 256, B = 256) in the bench's launch
+    configuration; the oracle recomputes sampled keys one by one."""
+    w = synth.CONFIGS["c3"]
+    T = synth.table(w.N, w.D, w.seed)
+    al = synth.alphas(w.B, w.N, w.seed)
+    seeds = synth.gen_seeds(w.B, w.seed)
+    pairs = [dp.gen(w.log_n, int(a), 1, s) for a, s in zip(al, seeds)]
+    Td = to_dev(T)
+    sh0 = dp.as_u32(dp.eval_batch([p[0] for p in pairs], Td))
+    sh1 = dp.as_u32(dp.eval_batch([p[1] for p in pairs], Td))
+    st = dp.last_eval_stats()
+    assert st["prf_blocks"] == w.B * (w.N - 1)
+    np.testing.assert_array_equal(dp.reconstruct(sh0, sh1), T[al.astype(np.int64)])  # every query
+    sample = [0, 129, 255]
+    ok = [oracle.key_from_wire(dp.key_serialize(pairs[b][b % 2])) for b in sample]
+    want = oracle.answer_batch(ok, T, threads=3)
+    for i, b in enumerate(sample):
+        np.testing.assert_array_equal((sh0, sh1)[b % 2][b], want[i])
