@@ -179,6 +179,14 @@ typedef struct dpf_eval_stats {
 } dpf_eval_stats;
 int dpf_last_eval_stats(dpf_eval_stats *out);
 
+/* Optional instrumentation (used by bench.py): after dpf_kernel_timer_begin(C)
+ * each of the next C evaluations on this thread records a CUDA event pair on
+ * its stream around the fused evaluation kernel.  dpf_kernel_timer_read waits
+ * for them, writes up to `capacity` per-launch durations (ms) and disables
+ * the timer; *count receives the number written. */
+int dpf_kernel_timer_begin(uint32_t capacity);
+int dpf_kernel_timer_read(float *ms, uint32_t capacity, uint32_t *count);
+
 /* Human-readable status text (static storage). */
 const char *dpf_strerror(int code);
 

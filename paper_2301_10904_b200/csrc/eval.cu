@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -59,6 +60,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "@!p bra DPF_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+// Same, with a suspend-time hint: the waiting warp sleeps in hardware until
+// the phase completes (or the hint elapses) instead of re-polling, so idle
+// consumer/loader warps stop stealing issue slots from the PRF producers.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "DPF_WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra DPF_WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(0x100000u)
+      : "memory");
+}
+// Named hardware barriers for the y-tile ring: a warp blocked in bar.sync is
+// descheduled (no issue slots), unlike an mbarrier try_wait poll loop.
+// IDs: 1 + stage = FULL (producers arrive, consumers sync),
+//      3 + stage = EMPTY (consumers arrive, producers + loader sync).
+__device__ __forceinline__ void named_sync(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes, uint64_t *bar) {
   asm volatile(
@@ -107,6 +130,35 @@ __global__ void expand_level_kernel(const uint8_t *__restrict__ keys, uint32_t k
     if (j0 >= lo && j0 <= hi) out[uint64_t(b) * cap + (j0 - lo)] = c0;
     if (j1 >= lo && j1 <= hi) out[uint64_t(b) * cap + (j1 - lo)] = c1;
   }
+}
+
+// Levels 1..a (a <= kTopSmemLevels) of every key in one launch: one CTA per
+// key expands level by level in shared memory (ping-pong), then writes level a
+// to `out`.  Removes a-1 kernel boundaries from the top of the tree.
+constexpr uint32_t kTopSmemLevels = 10;
+__global__ void __launch_bounds__(256) expand_top_smem_kernel(const uint8_t *__restrict__ keys, uint32_t kstride,
+                                                              uint32_t n, uint32_t a, uint64_t r0, uint64_t r1,
+                                                              uint4 *__restrict__ out, uint64_t cap) {
+  __shared__ uint4 buf[2][1u << kTopSmemLevels];
+  const uint32_t b = blockIdx.x;
+  const uint8_t *key = keys + uint64_t(b) * kstride;
+  if (threadIdx.x == 0) buf[0][0] = key_root(key);
+  __syncthreads();
+  for (uint32_t k = 1; k <= a; ++k) {
+    const uint64_t plo = r0 >> (n - (k - 1)), phi = (r1 - 1) >> (n - (k - 1));
+    const uint64_t lo = r0 >> (n - k), hi = (r1 - 1) >> (n - k);
+    const uint4 *in = buf[(k - 1) & 1];
+    uint4 *o = buf[k & 1];
+    for (uint64_t p = plo + threadIdx.x; p <= phi; p += blockDim.x) {
+      uint4 c0, c1;
+      node_children(in[p - plo], key_cw(key, k), c0, c1);
+      if (2 * p >= lo) o[2 * p - lo] = c0;
+      if (2 * p + 1 <= hi) o[2 * p + 1 - lo] = c1;
+    }
+    __syncthreads();
+  }
+  const uint64_t cnt = ((r1 - 1) >> (n - a)) - (r0 >> (n - a)) + 1;
+  for (uint64_t i = threadIdx.x; i < cnt; i += blockDim.x) out[uint64_t(b) * cap + i] = buf[a & 1][i];
 }
 
 // f == 0: the frontier is the root itself.
@@ -177,8 +229,12 @@ __device__ __forceinline__ void consume_window(const uint32_t *__restrict__ yb, 
 template <int NP, int NC, int KPW, int CPL>
 __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const FusedParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem);  // yfull[2], tfull[2], empty[2]
-  uint64_t *yfull = bars, *tfull = bars + 2, *empty = bars + 4;
+  uint64_t *tfull = reinterpret_cast<uint64_t *>(smem);  // T-tile ring: bulk-copy completion
+  constexpr uint32_t kFullThreads = 32 * (NP + NC), kEmptyThreads = 32 * (NP + NC + 1);
+  // windows this CTA will run (consumers skip the EMPTY arrive for the last
+  // two, which no producer will ever wait for)
+  const uint32_t my_items = blockIdx.x < p.n_items ? (p.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const uint32_t total_w = my_items * p.nwin;
   uint32_t *ybuf = reinterpret_cast<uint32_t *>(smem + 128);
   uint32_t *tbuf = ybuf + 2 * p.y_stage_words;
   uint4 *stack = reinterpret_cast<uint4 *>(tbuf + 2 * p.t_stage_words);
@@ -186,9 +242,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&yfull[s], NP);
       mbar_init(&tfull[s], 1);
-      mbar_init(&empty[s], NC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -215,7 +269,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
       uint32_t dep = 0;
       for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
         const uint32_t stage = wseq & 1, use = wseq >> 1;
-        if (use > 0) mbar_wait(&empty[stage], (use - 1) & 1);
+        if (use > 0) named_sync(3 + stage, kEmptyThreads);
         uint32_t *yb = ybuf + stage * p.y_stage_words;
         for (uint32_t qi = 0; qi < p.W; ++qi) {
           const uint32_t q = win * p.W + qi;
@@ -243,8 +297,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
             dep = k;
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&yfull[stage]);
+        named_arrive(1 + stage, kFullThreads);
       }
     }
   } else if (warp < NP + NC) {
@@ -264,13 +317,12 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
       const uint32_t kt = item % p.n_ktiles;
       for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
         const uint32_t stage = wseq & 1, use = wseq >> 1;
-        mbar_wait(&yfull[stage], use & 1);
+        named_sync(1 + stage, kFullThreads);
         mbar_wait(&tfull[stage], use & 1);
         if (active)
           consume_window<KPW, CPL>(ybuf + stage * p.y_stage_words, tbuf + stage * p.t_stage_words, nslots, p.Kt,
                                    p.D, key0, colbase, acc);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[stage]);
+        if (wseq + 2 < total_w) named_arrive(3 + stage, kEmptyThreads);
       }
       // a6/a7: flush this item's partial answers, party sign applied once.
       if (active) {
@@ -299,7 +351,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
       const uint32_t ng = item / p.n_ktiles;
       for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
         const uint32_t stage = wseq & 1, use = wseq >> 1;
-        if (use > 0) mbar_wait(&empty[stage], (use - 1) & 1);
+        if (use > 0) named_sync(3 + stage, kEmptyThreads);
         uint32_t *tb = tbuf + stage * p.t_stage_words;
         uint32_t my_bytes = 0;
         for (uint32_t nl = lane; nl < p.Ft; nl += 32) {
@@ -351,7 +403,6 @@ __global__ void eval_leaves_kernel(const uint8_t *__restrict__ keys, uint32_t ks
 // =================================================================== host side
 namespace {
 
-constexpr int kNP = 8;  // producer warps
 constexpr int kNC = 4;  // consumer warps
 constexpr size_t kAlign = 256;
 constexpr uint32_t kMaxTStageBytes = 64 * 1024;
@@ -365,13 +416,13 @@ inline uint32_t pow2ceil(uint32_t v) {
 }
 
 struct KernelChoice {
-  int KPW, CPL;
+  int NP, KPW, CPL;
   void (*fn)(const dev::FusedParams);
 };
 
-template <int KPW, int CPL>
+template <int NP, int KPW, int CPL>
 KernelChoice choice() {
-  return {KPW, CPL, &dev::fused_eval_kernel<kNP, kNC, KPW, CPL>};
+  return {NP, KPW, CPL, &dev::fused_eval_kernel<NP, kNC, KPW, CPL>};
 }
 
 struct Plan {
@@ -397,21 +448,38 @@ int num_sms() {
 
 // Consumer warp tiling for (Kt keys, D cols) over kNC warps: KG key groups x
 // CG col groups, KPW = Kt / KG, CPL = ceil(D / (32 CG)).
+struct Cand {
+  uint32_t CG;
+  KernelChoice kc;
+};
+
+// Preference order: fewest loads per IMAD first.
+template <int NP>
+const std::vector<Cand> &cands() {
+  static const std::vector<Cand> v = {
+      {2, choice<NP, 16, 4>()}, {1, choice<NP, 8, 2>()}, {4, choice<NP, 8, 4>()}, {1, choice<NP, 8, 1>()},
+      {2, choice<NP, 16, 2>()}, {1, choice<NP, 4, 2>()}, {1, choice<NP, 4, 1>()}, {2, choice<NP, 4, 4>()},
+      {4, choice<NP, 4, 4>()},  {2, choice<NP, 2, 2>()}, {1, choice<NP, 2, 1>()}, {2, choice<NP, 2, 4>()},
+      {4, choice<NP, 2, 4>()},  {4, choice<NP, 1, 4>()}, {4, choice<NP, 1, 2>()}, {4, choice<NP, 1, 1>()},
+      {2, choice<NP, 1, 4>()},  {2, choice<NP, 1, 1>()}, {1, choice<NP, 1, 1>()}, {4, choice<NP, 16, 4>()},
+      {4, choice<NP, 8, 8>()},  {4, choice<NP, 4, 8>()}, {4, choice<NP, 2, 8>()}, {4, choice<NP, 1, 8>()},
+  };
+  return v;
+}
+
+int producer_warps() {
+  static int np = [] {
+    const char *e = getenv("DPF_NP");  // tuning override: 8, 12 or 16
+    int v = e ? atoi(e) : 8;
+    return (v == 12 || v == 16) ? v : 8;
+  }();
+  return np;
+}
+
 bool pick_kernel(uint32_t Kt, uint32_t D, Plan &pl) {
-  struct Cand {
-    uint32_t CG;
-    KernelChoice kc;
-  };
-  // Preference order: fewest loads per IMAD first.
-  static const Cand cands[] = {
-      {2, choice<16, 4>()}, {1, choice<8, 2>()},  {4, choice<8, 4>()},  {1, choice<8, 1>()},
-      {2, choice<16, 2>()}, {1, choice<4, 2>()},  {1, choice<4, 1>()},  {2, choice<4, 4>()},
-      {4, choice<4, 4>()},  {2, choice<2, 2>()},  {1, choice<2, 1>()},  {2, choice<2, 4>()},
-      {4, choice<2, 4>()},  {4, choice<1, 4>()},  {4, choice<1, 2>()},  {4, choice<1, 1>()},
-      {2, choice<1, 4>()},  {2, choice<1, 1>()},  {1, choice<1, 1>()},  {4, choice<16, 4>()},
-      {4, choice<8, 8>()},  {4, choice<4, 8>()},  {4, choice<2, 8>()},  {4, choice<1, 8>()},
-  };
-  for (const Cand &c : cands) {
+  const int NP = producer_warps();
+  const std::vector<Cand> &cs = NP == 16 ? cands<16>() : NP == 12 ? cands<12>() : cands<8>();
+  for (const Cand &c : cs) {
     const uint32_t KG = kNC / c.CG;
     if (Kt % uint32_t(c.kc.KPW)) continue;
     if (Kt / c.kc.KPW > KG) continue;                      // not enough warps for the keys
@@ -436,16 +504,19 @@ int make_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Pl
   pl.Kt = std::min<uint32_t>(32, pow2ceil(B));
   while (pl.Kt * D > 8192 && pl.Kt > 1) pl.Kt >>= 1;  // accumulator budget: Kt*D <= 8192 words/CTA
   if (!pick_kernel(pl.Kt, D, pl)) return DPF_EINVAL;
-  pl.Ft = 32 * kNP / pl.Kt;
+  const uint32_t NP = uint32_t(pl.kc.NP);
+  pl.Ft = 32 * NP / pl.Kt;
   // T stage must fit: Ft * 2 rows * D words at W = 1.
   while (uint64_t(pl.Ft) * 2 * D * 4 > kMaxTStageBytesW1 && pl.Ft > 1) pl.Ft >>= 1;
   pl.tasks = pl.Kt * pl.Ft;
   pl.n_ktiles = (B + pl.Kt - 1) / pl.Kt;
   // Subtree depth m (frontier depth f = n - m): the largest m that still
-  // gives >= 8 work items per SM; m <= 14 keeps the SMEM stack small.
+  // gives >= 8 work items per SM; the SMEM DFS stack (m x 16 B per producer
+  // thread) is capped at 64 KB.
   const uint64_t target = 8ull * num_sms();
+  const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((64 * 1024) / (32 * NP * 16)));
   uint32_t best_m = 1;
-  for (uint32_t m = std::min<uint32_t>(n, 14); m >= 1; --m) {
+  for (uint32_t m = std::min<uint32_t>(n, m_cap); m >= 1; --m) {
     const uint64_t F = ((pl.r1 - 1) >> m) - (r0 >> m) + 1;
     const uint64_t items = uint64_t(pl.n_ktiles) * ((F + pl.Ft - 1) / pl.Ft);
     best_m = m;
@@ -463,14 +534,17 @@ int make_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Pl
   const uint32_t nq = 1u << (pl.m - 1);
   uint32_t W = std::min<uint32_t>(8, nq);
   while (W > 1 && uint64_t(pl.Ft) * 2 * W * D * 4 > kMaxTStageBytes) W >>= 1;
-  pl.W = W;
-  pl.nwin = nq / W;
-  pl.y_stage_words = uint32_t(align_up(size_t(pl.Kt) * pl.Ft * 2 * W, 32));
-  // + padding: lanes whose columns exceed D read past the last row.
-  pl.t_stage_words = uint32_t(align_up(size_t(pl.Ft) * 2 * W * D + 32u * pl.kc.CPL * pl.CG, 32));
-  const size_t stack_bytes = size_t(pl.m) * 32 * kNP * 16;
-  pl.smem_bytes = 128 + 4 * (2 * size_t(pl.y_stage_words) + 2 * size_t(pl.t_stage_words)) + stack_bytes;
-  if (pl.smem_bytes > 227 * 1024) return DPF_EINVAL;
+  const size_t stack_bytes = size_t(pl.m) * 32 * NP * 16;
+  for (;; W >>= 1) {
+    pl.W = W;
+    pl.nwin = nq / W;
+    pl.y_stage_words = uint32_t(align_up(size_t(pl.Kt) * pl.Ft * 2 * W, 32));
+    // + padding: lanes whose columns exceed D read past the last row.
+    pl.t_stage_words = uint32_t(align_up(size_t(pl.Ft) * 2 * W * D + 32u * pl.kc.CPL * pl.CG, 32));
+    pl.smem_bytes = 128 + 4 * (2 * size_t(pl.y_stage_words) + 2 * size_t(pl.t_stage_words)) + stack_bytes;
+    if (pl.smem_bytes <= 227 * 1024) break;
+    if (W == 1) return DPF_EINVAL;
+  }
   pl.grid = std::min<uint32_t>(pl.n_items, uint32_t(num_sms()));
   // PRF blocks: top levels (nodes intersecting the range) + fused subtrees.
   uint64_t top = 0;
@@ -501,6 +575,17 @@ size_t layout(const Plan &pl, uint32_t B, size_t kstride, Workspace *ws, void *b
 
 thread_local dpf_eval_stats g_stats{};
 
+// Optional per-launch timing of the fused kernel (bench instrumentation).
+struct KernelTimer {
+  std::vector<cudaEvent_t> ev;
+  uint32_t used = 0;
+  bool on = false;
+  ~KernelTimer() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
+};
+thread_local KernelTimer g_timer;
+
 // Per-thread pinned staging ring for host keys (2 slots, grown on demand).
 struct Staging {
   uint8_t *buf[2] = {nullptr, nullptr};
@@ -525,7 +610,13 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
     dev::copy_roots_kernel<<<(B + 127) / 128, 128, 0, st>>>(keys_dev, kstride, B, ws.front[0], pl.cap);
     ++nk;
   }
-  for (uint32_t k = 1; k <= pl.f; ++k) {
+  const uint32_t a = std::min(pl.f, dev::kTopSmemLevels);
+  if (a >= 1) {
+    dev::expand_top_smem_kernel<<<B, 256, 0, st>>>(keys_dev, kstride, pl.n, a, pl.r0, pl.r1, ws.front[(pl.f - a) & 1],
+                                                   pl.cap);
+    ++nk;
+  }
+  for (uint32_t k = a + 1; k <= pl.f; ++k) {
     const uint64_t np = ((pl.r1 - 1) >> (pl.n - (k - 1))) - (pl.r0 >> (pl.n - (k - 1))) + 1;
     const uint64_t total = np * B;
     const uint32_t grid = uint32_t(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
@@ -562,7 +653,10 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
   if (cudaFuncSetAttribute(pl.kc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) !=
       cudaSuccess)
     return DPF_ECUDA;
-  pl.kc.fn<<<pl.grid, 32 * (kNP + kNC + 1), pl.smem_bytes, st>>>(p);
+  const bool timed = g_timer.on && 2 * g_timer.used + 1 < g_timer.ev.size();
+  if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
+  pl.kc.fn<<<pl.grid, 32 * (pl.kc.NP + kNC + 1), pl.smem_bytes, st>>>(p);
+  if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used++ + 1], st);
   ++nk;
   if (cudaGetLastError() != cudaSuccess) return DPF_ECUDA;
   if (kernels) *kernels = nk;
@@ -714,6 +808,31 @@ extern "C" int dpf_eval_leaves(const dpf_key *keys, uint32_t B, uint32_t *leaves
   dev::eval_leaves_kernel<<<grid, 256, 0, st>>>(static_cast<uint8_t *>(workspace), kstride, B, n, leaves);
   if (cudaGetLastError() != cudaSuccess) return DPF_ECUDA;
   // staged is pageable: the H2D above completed its staging before return.
+  return DPF_OK;
+}
+
+extern "C" int dpf_kernel_timer_begin(uint32_t capacity) {
+  KernelTimer &t = g_timer;
+  while (t.ev.size() < 2 * size_t(capacity)) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return DPF_ECUDA;
+    t.ev.push_back(e);
+  }
+  t.used = 0;
+  t.on = capacity > 0;
+  return DPF_OK;
+}
+
+extern "C" int dpf_kernel_timer_read(float *ms, uint32_t capacity, uint32_t *count) {
+  KernelTimer &t = g_timer;
+  t.on = false;
+  const uint32_t n = std::min(t.used, capacity);
+  for (uint32_t i = 0; i < n; ++i) {
+    if (cudaEventSynchronize(t.ev[2 * i + 1]) != cudaSuccess) return DPF_ECUDA;
+    if (ms && cudaEventElapsedTime(&ms[i], t.ev[2 * i], t.ev[2 * i + 1]) != cudaSuccess) return DPF_ECUDA;
+  }
+  if (count) *count = n;
+  t.used = 0;
   return DPF_OK;
 }
 

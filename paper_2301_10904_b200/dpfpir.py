@@ -75,6 +75,8 @@ def lib() -> ctypes.CDLL:
     L.dpf_serve_batch.argtypes = [vp, u32, vp, u64, u64, u32, vp, vp, sz, vp]
     L.dpf_eval_leaves.argtypes = [vp, u32, vp, vp, sz, vp]
     L.dpf_last_eval_stats.argtypes = [vp]
+    L.dpf_kernel_timer_begin.argtypes = [u32]
+    L.dpf_kernel_timer_read.argtypes = [vp, u32, vp]
     L.dpf_strerror.argtypes = [ctypes.c_int]
     L.dpf_strerror.restype = ctypes.c_char_p
     L.dpf_version.restype = ctypes.c_char_p
@@ -85,7 +87,8 @@ def lib() -> ctypes.CDLL:
 
 EXPORTED_SYMBOLS = ("dpf_gen", "dpf_key_wire_size", "dpf_key_serialize", "dpf_key_deserialize", "dpf_reconstruct",
                     "dpf_eval_workspace_bytes", "dpf_eval_batch", "dpf_eval_batch_shard", "dpf_eval_batch_wire",
-                    "dpf_serve_batch", "dpf_eval_leaves", "dpf_last_eval_stats", "dpf_strerror", "dpf_version")
+                    "dpf_serve_batch", "dpf_eval_leaves", "dpf_last_eval_stats", "dpf_kernel_timer_begin",
+                    "dpf_kernel_timer_read", "dpf_strerror", "dpf_version")
 
 
 def strerror(code: int) -> str:
@@ -307,6 +310,17 @@ def last_eval_stats() -> dict:
     s = DpfEvalStats()
     _check(lib().dpf_last_eval_stats(ctypes.byref(s)), "dpf_last_eval_stats")
     return {f: getattr(s, f) for f, _ in DpfEvalStats._fields_}
+
+
+def kernel_timer_begin(capacity: int) -> None:
+    _check(lib().dpf_kernel_timer_begin(capacity), "dpf_kernel_timer_begin")
+
+
+def kernel_timer_read(capacity: int) -> list:
+    ms = (ctypes.c_float * max(capacity, 1))()
+    cnt = ctypes.c_uint32(0)
+    _check(lib().dpf_kernel_timer_read(ms, capacity, ctypes.byref(cnt)), "dpf_kernel_timer_read")
+    return [ms[i] for i in range(cnt.value)]
 
 
 def as_u32(t) -> np.ndarray:

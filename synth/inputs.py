@@ -14,7 +14,7 @@ import dataclasses
 
 import numpy as np
 
-__all__ = ["Workload", "CONFIGS", "table", "alphas", "betas", "gen_seeds", "rng"]
+__all__ = ["Workload", "CONFIGS", "table", "table_rows", "alphas", "betas", "gen_seeds", "rng"]
 
 _STREAM_TABLE, _STREAM_ALPHA, _STREAM_BETA, _STREAM_GEN = 1, 2, 3, 4
 
@@ -23,9 +23,30 @@ def rng(seed: int, stream: int) -> np.random.Generator:
     return np.random.Generator(np.random.PCG64([seed & 0xFFFFFFFF, stream]))
 
 
+TABLE_BLOCK_ROWS = 1 << 16
+
+
+def table_rows(N: int, D: int, seed: int, r0: int, r1: int) -> np.ndarray:
+    """Rows [r0, r1) of the int32 embedding table T[N][D] (uint32 bit patterns,
+    uniform).  Generated in blocks of 2^16 rows, each from its own PCG64
+    stream, so a rank can build just its row shard."""
+    assert 0 <= r0 <= r1 <= N
+    out = np.empty((r1 - r0, D), np.uint32)
+    blk = r0 // TABLE_BLOCK_ROWS
+    while blk * TABLE_BLOCK_ROWS < r1:
+        b0 = blk * TABLE_BLOCK_ROWS
+        b1 = min(b0 + TABLE_BLOCK_ROWS, N)
+        g = np.random.Generator(np.random.PCG64([seed & 0xFFFFFFFF, _STREAM_TABLE, blk]))
+        rows = g.integers(0, 1 << 32, size=(b1 - b0, D), dtype=np.uint32)
+        lo, hi = max(b0, r0), min(b1, r1)
+        out[lo - r0:hi - r0] = rows[lo - b0:hi - b0]
+        blk += 1
+    return out
+
+
 def table(N: int, D: int, seed: int) -> np.ndarray:
-    """int32 embedding table T[N][D] as uint32 bit patterns, uniform."""
-    return rng(seed, _STREAM_TABLE).integers(0, 1 << 32, size=(N, D), dtype=np.uint32)
+    """The whole int32 embedding table T[N][D] (see table_rows)."""
+    return table_rows(N, D, seed, 0, N)
 
 
 def alphas(B: int, N: int, seed: int) -> np.ndarray:
