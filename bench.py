@@ -182,6 +182,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--table", default="auto", choices=["auto", "packed", "rowmajor"],
+                    help="packed = limb-packed table + tcgen05 contraction (D in {128,256}); rowmajor = IMAD path")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -208,6 +210,10 @@ def main():
 
     T_host = synth.table_rows(w.N, w.D, w.seed, r0, r0 + rows)
     T = torch.from_numpy(T_host.view(np.int32)).to(dev)
+    use_packed = args.table == "packed" or (args.table == "auto" and w.D in (128, 256) and w.B >= 32)
+    # server state: the table is re-laid-out once into u8 limb planes (outside every timed region)
+    Tp = dpfpir.table_pack(T, r0) if use_packed else None
+    torch.cuda.synchronize()
     al, pairs = make_keys(w, dpfpir)
     keys0 = dpfpir.KeyBatch.from_keys([p[0] for p in pairs])
     wire_host = dpfpir.keys_to_wire(keys0)
@@ -217,7 +223,10 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step():
-        dpfpir.eval_batch_wire(wire, w.log_n, T, r0, out=out, workspace=ws, stream=stream)
+        if use_packed:
+            dpfpir.eval_batch_wire_packed(wire, w.log_n, Tp, out=out, workspace=ws, stream=stream)
+        else:
+            dpfpir.eval_batch_wire(wire, w.log_n, T, r0, out=out, workspace=ws, stream=stream)
         if G > 1:
             shard.reduce_partial_shares(out, dst=0)
 
@@ -230,7 +239,8 @@ def main():
     step()
     share0 = dpfpir.as_u32(out) if rank == 0 else None
     keys1 = dpfpir.KeyBatch.from_keys([p[1] for p in pairs])
-    out1 = dpfpir.eval_batch_shard(keys1, T, r0, workspace=ws)
+    out1 = (dpfpir.eval_batch_packed(keys1, Tp, workspace=ws) if use_packed else
+            dpfpir.eval_batch_shard(keys1, T, r0, workspace=ws))
     if G > 1:
         shard.reduce_partial_shares(out1, dst=0)
     parity = {}
@@ -268,14 +278,18 @@ def main():
     host_out = torch.empty((w.B, w.D), dtype=torch.int32).pin_memory()
 
     def e2e_step():
-        if G == 1:
+        if G == 1 and not use_packed:
             dpfpir.serve_batch(keys0, T, host_out, r0, workspace=ws, stream=stream)
+            return
+        if use_packed:
+            dpfpir.eval_batch_packed(keys0, Tp, out=out, workspace=ws, stream=stream)
         else:
             dpfpir.eval_batch_shard(keys0, T, r0, out=out, workspace=ws, stream=stream)
+        if G > 1:
             shard.reduce_partial_shares(out, dst=0)
-            if rank == 0:
-                host_out.copy_(out, non_blocking=True)
-            torch.cuda.current_stream().synchronize()
+        if rank == 0:
+            host_out.copy_(out, non_blocking=True)
+        stream.synchronize()
 
     for _ in range(2):
         e2e_step()
@@ -307,7 +321,7 @@ def main():
     roofline = {
         "bound": "alu", "achieved": achieved * 1e-12, "peak": alu_peak * 1e-12, "unit": "Tops/s",
         "frac": achieved / alu_peak, "traffic": traffic,
-        "kernel": "fused_eval_kernel", "kernel_ms": kern_avg_ms,
+        "kernel": "fused_eval_tc_kernel" if use_packed else "fused_eval_kernel", "kernel_ms": kern_avg_ms,
         "kernel_share_of_step": kern_avg_ms / ms_per_step,
         "ops": "640 ALU-pipe int32 ops (LOP3 xor + SHF rotate) per ChaCha20 block x %d blocks per launch" % fused_blocks,
         "peak_basis": "148 SMs x 64 ALU lanes/clk x %.0f MHz (%s)" % (pk["sm_max_mhz"], pk["source"]),
@@ -334,12 +348,15 @@ def main():
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": w.name + ": " + w.note, "log_n": w.log_n, "N": w.N, "D": w.D, "B": w.B,
                        "parallelism": "row-shard x%d + NCCL reduce" % G if G > 1 else "1 GPU",
-                       "keys": "device-resident wire keys (dpf_eval_batch_wire)",
+                       "keys": "device-resident wire keys (dpf_eval_batch_wire%s)" % ("_packed" if use_packed else ""),
+                       "table": "limb-packed (dpf_table_pack, tcgen05 kind::i8 contraction)" if use_packed
+                       else "row-major int32 (IMAD contraction)",
                        "l2": "no flush: table shard (%d MiB) >= L2 and the path is ALU-bound" %
                              (rows * w.D * 4 >> 20)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(wire_host.nbytes),
-                    "d2h_bytes_per_step": w.B * w.D * 4, "api": "dpf_serve_batch" if G == 1 else
-                    "dpf_eval_batch_shard + NCCL reduce + D2H"},
+                    "d2h_bytes_per_step": w.B * w.D * 4, "api": ("dpf_serve_batch" if G == 1 and not use_packed else
+                            "dpf_eval_batch%s + %sD2H" % ("_packed" if use_packed else "_shard",
+                                                          "NCCL reduce + " if G > 1 else ""))},
             "gpu_launches": int(stats["kernels"]) * args.steps,
             "roofline": roofline,
             "cpu_baseline": cpu,

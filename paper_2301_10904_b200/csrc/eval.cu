@@ -378,6 +378,12 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
   }
 }
 
+}  // namespace dev
+}  // namespace dpfpir
+#include "fused_tc.cuh"
+namespace dpfpir {
+namespace dev {
+
 // Test/debug leaf dump (branch-parallel: n blocks per leaf).
 __global__ void eval_leaves_kernel(const uint8_t *__restrict__ keys, uint32_t kstride, uint32_t B, uint32_t n,
                                    uint32_t *__restrict__ leaves) {
@@ -426,6 +432,9 @@ KernelChoice choice() {
 }
 
 struct Plan {
+  bool tc;  // tcgen05 contraction on a limb-packed table
+  uint32_t tmem_cols, y_stage_bytes, t_stage_bytes;
+  uint64_t r0a, packed_rows;
   uint32_t n, m, f, Kt, Ft, tasks, W, CG, KG, n_ktiles, n_items, nwin, grid;
   uint64_t r0, r1, F, lo_f, cap;
   uint32_t y_stage_words, t_stage_words;
@@ -448,21 +457,18 @@ int num_sms() {
 
 // Consumer warp tiling for (Kt keys, D cols) over kNC warps: KG key groups x
 // CG col groups, KPW = Kt / KG, CPL = ceil(D / (32 CG)).
-struct Cand {
-  uint32_t CG;
-  KernelChoice kc;
-};
-
-// Preference order: fewest loads per IMAD first.
+// Consumer warp tiling for (Kt keys, D cols) over kNC warps: CG column groups
+// x KG = kNC/CG key groups; a warp owns KPW keys x 32*CPL columns.  Among the
+// compiled (KPW, CPL) tiles, pick the one with the fewest instructions per
+// slot on the busiest consumer warp (CPL T loads + KPW/4 y loads + KPW*CPL
+// IMADs), then the fewest in total.
 template <int NP>
-const std::vector<Cand> &cands() {
-  static const std::vector<Cand> v = {
-      {2, choice<NP, 16, 4>()}, {1, choice<NP, 8, 2>()}, {4, choice<NP, 8, 4>()}, {1, choice<NP, 8, 1>()},
-      {2, choice<NP, 16, 2>()}, {1, choice<NP, 4, 2>()}, {1, choice<NP, 4, 1>()}, {2, choice<NP, 4, 4>()},
-      {4, choice<NP, 4, 4>()},  {2, choice<NP, 2, 2>()}, {1, choice<NP, 2, 1>()}, {2, choice<NP, 2, 4>()},
-      {4, choice<NP, 2, 4>()},  {4, choice<NP, 1, 4>()}, {4, choice<NP, 1, 2>()}, {4, choice<NP, 1, 1>()},
-      {2, choice<NP, 1, 4>()},  {2, choice<NP, 1, 1>()}, {1, choice<NP, 1, 1>()}, {4, choice<NP, 16, 4>()},
-      {4, choice<NP, 8, 8>()},  {4, choice<NP, 4, 8>()}, {4, choice<NP, 2, 8>()}, {4, choice<NP, 1, 8>()},
+const std::vector<KernelChoice> &tiles() {
+  static const std::vector<KernelChoice> v = {
+      choice<NP, 16, 4>(), choice<NP, 16, 2>(), choice<NP, 16, 1>(), choice<NP, 8, 8>(), choice<NP, 8, 4>(),
+      choice<NP, 8, 2>(),  choice<NP, 8, 1>(),  choice<NP, 4, 8>(),  choice<NP, 4, 4>(), choice<NP, 4, 2>(),
+      choice<NP, 4, 1>(),  choice<NP, 2, 8>(),  choice<NP, 2, 4>(),  choice<NP, 2, 2>(), choice<NP, 2, 1>(),
+      choice<NP, 1, 8>(),  choice<NP, 1, 4>(),  choice<NP, 1, 2>(),  choice<NP, 1, 1>(),
   };
   return v;
 }
@@ -478,21 +484,25 @@ int producer_warps() {
 
 bool pick_kernel(uint32_t Kt, uint32_t D, Plan &pl) {
   const int NP = producer_warps();
-  const std::vector<Cand> &cs = NP == 16 ? cands<16>() : NP == 12 ? cands<12>() : cands<8>();
-  for (const Cand &c : cs) {
-    const uint32_t KG = kNC / c.CG;
-    if (Kt % uint32_t(c.kc.KPW)) continue;
-    if (Kt / c.kc.KPW > KG) continue;                      // not enough warps for the keys
-    if (Kt / c.kc.KPW < KG && c.kc.KPW > 1) continue;      // would leave key groups idle; prefer smaller KPW
-    const uint32_t cols = 32u * c.kc.CPL * c.CG;
-    if (cols < D) continue;                                // not enough columns
-    if (c.kc.CPL > 1 && 32u * (c.kc.CPL - 1) * c.CG >= D) continue;  // wasteful CPL
-    pl.CG = c.CG;
-    pl.KG = Kt / c.kc.KPW;
-    pl.kc = c.kc;
-    return true;
+  const std::vector<KernelChoice> &ts = NP == 16 ? tiles<16>() : NP == 12 ? tiles<12>() : tiles<8>();
+  uint64_t best = ~0ull;
+  for (const KernelChoice &kc : ts) {
+    for (uint32_t CG : {1u, 2u, 4u}) {
+      const uint32_t KG = kNC / CG;
+      if (Kt % uint32_t(kc.KPW) || Kt / kc.KPW > KG) continue;
+      if (32u * kc.CPL * CG < D) continue;
+      const uint32_t per_warp = kc.CPL + (kc.KPW + 3) / 4 + kc.KPW * kc.CPL;
+      const uint32_t total = per_warp * CG * (Kt / kc.KPW);
+      const uint64_t score = (uint64_t(per_warp) << 32) | total;
+      if (score < best) {
+        best = score;
+        pl.CG = CG;
+        pl.KG = Kt / kc.KPW;
+        pl.kc = kc;
+      }
+    }
   }
-  return false;
+  return best != ~0ull;
 }
 
 int make_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl) {
@@ -547,6 +557,74 @@ int make_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Pl
   }
   pl.grid = std::min<uint32_t>(pl.n_items, uint32_t(num_sms()));
   // PRF blocks: top levels (nodes intersecting the range) + fused subtrees.
+  uint64_t top = 0;
+  for (uint32_t k = 0; k < pl.f; ++k) top += ((pl.r1 - 1) >> (n - k)) - (r0 >> (n - k)) + 1;
+  pl.prf_blocks = uint64_t(B) * top + uint64_t(pl.n_items) * pl.tasks * ((1ull << pl.m) - 1);
+  return DPF_OK;
+}
+
+// Subtree depth m for a plan: the largest m <= m_cap that still gives >= 8
+// work items per SM (and >= m_min).
+uint32_t choose_m(const Plan &pl, uint32_t n, uint64_t r0, uint32_t m_min, uint32_t m_cap) {
+  const uint64_t target = 8ull * num_sms();
+  uint32_t best = m_min;
+  for (uint32_t m = std::min<uint32_t>(n, m_cap); m >= m_min; --m) {
+    const uint64_t F = ((pl.r1 - 1) >> m) - (r0 >> m) + 1;
+    const uint64_t items = uint64_t(pl.n_ktiles) * ((F + pl.Ft - 1) / pl.Ft);
+    best = m;
+    if (items >= target) break;
+  }
+  return best;
+}
+
+uint32_t tc_producer_warps() {
+  static uint32_t np = [] {
+    const char *e = getenv("DPF_TC_NP");  // tuning override: 8 or 16
+    return (e && atoi(e) == 16) ? 16u : 8u;
+  }();
+  return np;
+}
+
+// tcgen05 plan (limb-packed table): Kt = 32 keys (N of the MMA), Ft = 8
+// nodes, 2W = 8 or 16 leaves per node per window (whole 8-row packed blocks),
+// D in {128, 256} (M = 128 tiles; 4 limb accumulators x D/128 tiles x 32
+// keys <= 256 TMEM columns).
+int make_tc_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl) {
+  std::memset(&pl, 0, sizeof pl);
+  if (D % 128 || D > 256 || n < 3) return DPF_EINVAL;
+  pl.tc = true;
+  pl.n = n;
+  pl.r0 = r0;
+  pl.r1 = r0 + rows;
+  pl.r0a = r0 & ~7ull;
+  pl.packed_rows = ((pl.r1 + 7) & ~7ull) - pl.r0a;
+  const uint32_t NP = tc_producer_warps();
+  pl.Kt = 4 * NP;  // 32 or 64 keys = MMA N
+  pl.Ft = 32 * NP / pl.Kt;
+  pl.tasks = pl.Kt * pl.Ft;
+  pl.n_ktiles = (B + pl.Kt - 1) / pl.Kt;
+  const uint32_t W = D <= 128 ? 8 : 4;
+  const uint32_t m_min = W == 8 ? 4 : 3;
+  if (n < m_min) return DPF_EINVAL;
+  pl.m = choose_m(pl, n, r0, m_min, std::min<uint32_t>(14, uint32_t((56 * 1024) / (32 * NP * 16))));
+  pl.f = n - pl.m;
+  pl.lo_f = r0 >> pl.m;
+  pl.F = ((pl.r1 - 1) >> pl.m) - pl.lo_f + 1;
+  pl.cap = pl.F;
+  const uint64_t items = uint64_t(pl.n_ktiles) * ((pl.F + pl.Ft - 1) / pl.Ft);
+  if (items > 0x7FFFFFFFull) return DPF_EINVAL;
+  pl.n_items = uint32_t(items);
+  pl.W = W;
+  pl.nwin = (1u << (pl.m - 1)) / W;
+  const uint32_t Kw = pl.Ft * 2 * W;
+  pl.y_stage_bytes = 4 * pl.Kt * Kw;
+  pl.t_stage_bytes = Kw * 4 * D;
+  const uint32_t cols = (D / 128) * 4 * pl.Kt;
+  pl.tmem_cols = 32;
+  while (pl.tmem_cols < cols) pl.tmem_cols <<= 1;
+  pl.smem_bytes = 1024 + 2 * size_t(pl.y_stage_bytes) + 2 * size_t(pl.t_stage_bytes) + size_t(pl.m) * 32 * NP * 16;
+  if (pl.smem_bytes > 227 * 1024) return DPF_EINVAL;
+  pl.grid = std::min<uint32_t>(pl.n_items, uint32_t(num_sms()));
   uint64_t top = 0;
   for (uint32_t k = 0; k < pl.f; ++k) top += ((pl.r1 - 1) >> (n - k)) - (r0 >> (n - k)) + 1;
   pl.prf_blocks = uint64_t(B) * top + uint64_t(pl.n_items) * pl.tasks * ((1ull << pl.m) - 1);
@@ -624,6 +702,7 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
                                                    ws.front[(pl.f - k + 1) & 1], ws.front[(pl.f - k) & 1], pl.cap);
     ++nk;
   }
+  const bool timed = g_timer.on && 2 * g_timer.used + 1 < g_timer.ev.size();
   dev::FusedParams p;
   p.keys = keys_dev;
   p.frontier = ws.front[0];
@@ -650,10 +729,30 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
   p.KG = pl.KG;
   p.y_stage_words = pl.y_stage_words;
   p.t_stage_words = pl.t_stage_words;
+  if (pl.tc) {
+    dev::TcParams tp;
+    tp.f = p;
+    tp.packed = reinterpret_cast<const uint8_t *>(table);
+    tp.r0a = pl.r0a;
+    tp.packed_rows = pl.packed_rows;
+    tp.y_stage_bytes = pl.y_stage_bytes;
+    tp.t_stage_bytes = pl.t_stage_bytes;
+    tp.tmem_cols = pl.tmem_cols;
+    const uint32_t NP = pl.Kt / 4;
+    auto fn = NP == 16 ? &dev::fused_eval_tc_kernel<16> : &dev::fused_eval_tc_kernel<8>;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
+      return DPF_ECUDA;
+    if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
+    fn<<<pl.grid, 32 * (NP + 4 + 1), pl.smem_bytes, st>>>(tp);
+    if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used++ + 1], st);
+    ++nk;
+    if (cudaGetLastError() != cudaSuccess) return DPF_ECUDA;
+    if (kernels) *kernels = nk;
+    return DPF_OK;
+  }
   if (cudaFuncSetAttribute(pl.kc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) !=
       cudaSuccess)
     return DPF_ECUDA;
-  const bool timed = g_timer.on && 2 * g_timer.used + 1 < g_timer.ev.size();
   if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
   pl.kc.fn<<<pl.grid, 32 * (pl.kc.NP + kNC + 1), pl.smem_bytes, st>>>(p);
   if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used++ + 1], st);
@@ -677,7 +776,7 @@ int check_common(uint32_t B, const uint32_t *table, uint64_t row_begin, uint64_t
 
 int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uint32_t log_n,
               const uint32_t *table, uint64_t row_begin, uint64_t rows, uint32_t D, uint32_t *out, void *workspace,
-              size_t ws_bytes, cudaStream_t st) {
+              size_t ws_bytes, cudaStream_t st, bool packed = false) {
   uint32_t n = log_n;
   if (keys) {
     if (B == 0) return DPF_EINVAL;
@@ -690,7 +789,7 @@ int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uin
   int rc = check_common(B, table, row_begin, rows, D, out, workspace, n);
   if (rc) return rc;
   Plan pl;
-  rc = make_plan(B, n, row_begin, rows, D, pl);
+  rc = packed ? make_tc_plan(B, n, row_begin, rows, D, pl) : make_plan(B, n, row_begin, rows, D, pl);
   if (rc) return rc;
   const uint32_t kstride = uint32_t(dpf_key_wire_size(n));
   Workspace ws;
@@ -746,7 +845,49 @@ extern "C" size_t dpf_eval_workspace_bytes(uint32_t B, uint32_t log_n, uint64_t 
   // The frontier size depends on the alignment of row_begin; size for the
   // worst case (one extra node per key).
   pl.cap += 1;
-  return layout(pl, B, dpf_key_wire_size(log_n), nullptr, nullptr);
+  size_t bytes = layout(pl, B, dpf_key_wire_size(log_n), nullptr, nullptr);
+  Plan tc;
+  if (make_tc_plan(B, log_n, 0, row_count, D, tc) == DPF_OK) {
+    tc.cap += 1;
+    bytes = std::max(bytes, layout(tc, B, dpf_key_wire_size(log_n), nullptr, nullptr));
+  }
+  return bytes;
+}
+
+extern "C" size_t dpf_table_packed_bytes(uint64_t row_begin, uint64_t row_count, uint32_t D) {
+  if (row_count == 0 || D == 0 || D % 16) return 0;
+  const uint64_t r0a = row_begin & ~7ull, r1a = (row_begin + row_count + 7) & ~7ull;
+  return size_t((r1a - r0a) * 4ull * D);
+}
+
+extern "C" int dpf_table_pack(const uint32_t *table_shard, uint64_t row_begin, uint64_t row_count, uint32_t D,
+                              void *packed, void *stream) {
+  if (!table_shard || !packed || row_count == 0 || D == 0 || D % 16) return DPF_EINVAL;
+  if ((reinterpret_cast<uintptr_t>(table_shard) & 15) || (reinterpret_cast<uintptr_t>(packed) & 15))
+    return DPF_EINVAL;
+  const uint64_t r0a = row_begin & ~7ull, r1a = (row_begin + row_count + 7) & ~7ull;
+  const uint64_t nblocks = (r1a - r0a) / 8;
+  const uint64_t total = nblocks * 8 * (D / 16);
+  const uint32_t grid = uint32_t(std::min<uint64_t>((total + 255) / 256, 148ull * 32));
+  dev::table_pack_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      table_shard, row_begin, row_begin + row_count, r0a, nblocks, D, static_cast<uint8_t *>(packed));
+  return cudaGetLastError() == cudaSuccess ? DPF_OK : DPF_ECUDA;
+}
+
+extern "C" int dpf_eval_batch_packed(const dpf_key *keys, uint32_t B, const void *packed, uint64_t row_begin,
+                                     uint64_t row_count, uint32_t D, uint32_t *partial, void *workspace,
+                                     size_t workspace_bytes, void *stream) {
+  if (!keys) return DPF_EINVAL;
+  return eval_impl(keys, B, nullptr, 0, static_cast<const uint32_t *>(packed), row_begin, row_count, D, partial,
+                   workspace, workspace_bytes, static_cast<cudaStream_t>(stream), true);
+}
+
+extern "C" int dpf_eval_batch_wire_packed(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n,
+                                          const void *packed, uint64_t row_begin, uint64_t row_count, uint32_t D,
+                                          uint32_t *partial, void *workspace, size_t workspace_bytes, void *stream) {
+  if (!keys_wire_dev || (reinterpret_cast<uintptr_t>(keys_wire_dev) & 15)) return DPF_EINVAL;
+  return eval_impl(nullptr, B, keys_wire_dev, log_n, static_cast<const uint32_t *>(packed), row_begin, row_count, D,
+                   partial, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), true);
 }
 
 extern "C" int dpf_eval_batch_shard(const dpf_key *keys, uint32_t B, const uint32_t *table_shard,

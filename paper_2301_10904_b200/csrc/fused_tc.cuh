@@ -1,0 +1,332 @@
+// fused_tc.cuh -- tcgen05 variant of the fused kernel: the leaf-share x table
+// contraction runs on the 5th-generation tensor cores (kind::i8) instead of
+// IMAD, so the SM's issue slots are left to the ChaCha20 producers.
+//
+// Limb decomposition: write y = sum_i y_i 2^(8i)
+// and t = sum_k t_k 2^(8k) with u8 limbs.  Then
+//     y * t mod 2^32 = sum_{s=0..3} 2^(8s) * A_s  mod 2^32,
+//     A_s = sum_{i+k=s} y_i t_k          (10 limb products, 4 accumulators)
+// and for a sum over leaves j the same holds with A_s = sum_j sum_{i+k=s}
+// y_i(j) t_k(j), accumulated in s32 TMEM with saturation OFF (wrapping, so A_s
+// is exact mod 2^32, which is all 2^(8s) A_s mod 2^32 needs).
+//
+// Operands per window (one per ring stage):
+//   A = table limb plane k, MN-major (M = 128 table columns d, K = leaves),
+//       from the limb-packed table (dpf_table_pack): blocks of 8 rows laid out
+//       [limb][d/16][row(8)][16 d] -- the no-swizzle MN-major core-matrix
+//       layout, so a node's 2W-row segment is ONE contiguous bulk copy;
+//       LBO = 32 D bytes (next 8 rows), SBO = 128 bytes (next 16 columns).
+//   B = leaf-share limb plane i, K-major (N = Kt keys, K = leaves), written
+//       by the producers as core matrices [K/16][Kt/8][8 keys][16 leaves];
+//       LBO = (Kt/8) 128 bytes (next 16 leaves), SBO = 128 bytes (next 8 keys).
+//   D = TMEM, accumulator (dt, s) at columns (dt*4 + s)*Kt, lane = column d.
+#pragma once
+
+namespace dpfpir {
+namespace dev {
+
+struct TcParams {
+  FusedParams f;
+  const uint8_t *packed;  // limb-packed rows [r0a, r0a + packed_rows)
+  uint64_t r0a, packed_rows;
+  uint32_t y_stage_bytes, t_stage_bytes, tmem_cols;
+};
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory matrix descriptor, SWIZZLE_NONE, version 1 (sm_100).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t((lbo >> 4) & 0x3FFFu) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
+}
+
+// Instruction descriptor, kind::i8: D = s32 (no saturate), A = u8 MN-major,
+// B = u8 K-major, M = 128, N = n.
+__host__ __device__ constexpr uint32_t umma_idesc_u8(uint32_t n) {
+  return (2u << 4)            // c_format = S32
+         | (0u << 7)          // a_format = unsigned 8-bit
+         | (0u << 10)         // b_format = unsigned 8-bit
+         | (1u << 15)         // a_major = MN
+         | (0u << 16)         // b_major = K
+         | ((n >> 3) << 17)   // N >> 3
+         | ((128u >> 4) << 24);  // M >> 4
+}
+
+__device__ __forceinline__ void umma_u8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                        uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+template <int NP>
+__global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(const TcParams tp) {
+  constexpr int NC = 4;
+  const FusedParams &p = tp.f;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t *yfull = reinterpret_cast<uint64_t *>(smem);  // [2], count NP (producer warps)
+  uint64_t *tfull = yfull + 2;                           // [2], count 1 + tx bytes
+  uint64_t *empty = yfull + 4;                           // [2], count 1 (tcgen05.commit)
+  uint64_t *accfull = yfull + 6;                         // count 1 (tcgen05.commit)
+  uint64_t *accempty = yfull + 7;                        // count NC (epilogue warps)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + 64);
+  uint8_t *ybuf = smem + 1024;
+  uint8_t *tbuf = ybuf + 2 * tp.y_stage_bytes;
+  uint4 *stack = reinterpret_cast<uint4 *>(tbuf + 2 * tp.t_stage_bytes);
+
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&yfull[s], NP);
+      mbar_init(&tfull[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accfull, 1);
+    mbar_init(accempty, NC);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == NP) {  // consumer warp 0 owns the TMEM allocation
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(tp.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const uint32_t nq = 1u << (p.m - 1);
+  const uint32_t W2 = 2 * p.W;               // leaves per node per window (multiple of 8)
+  const uint32_t Kw = p.Ft * W2;             // leaves per window (multiple of 32)
+  const uint32_t ybplane = p.Kt * Kw;        // bytes per y limb plane
+  const uint32_t D = p.D;
+
+  if (warp < NP) {
+    // ------------------------------------------------------------ producers
+    const uint32_t tix = warp * 32 + lane;
+    const uint32_t kl = tix % p.Kt, nl = tix / p.Kt;
+    uint32_t wseq = 0;
+    for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      const uint32_t kt = item % p.n_ktiles, ng = item / p.n_ktiles;
+      const uint32_t b = kt * p.Kt + kl;
+      const uint64_t node = uint64_t(ng) * p.Ft + nl;
+      const bool valid = b < p.B && node < p.F;
+      const uint8_t *key = p.keys + uint64_t(valid ? b : 0) * p.kstride;
+      const uint32_t cw_out = key_cw_out(key);
+      uint4 cur = valid ? p.frontier[uint64_t(b) * p.cap + node] : make_uint4(0, 0, 0, 0);
+      const uint64_t row_base = (p.lo_f + node) << p.m;
+      uint32_t dep = 0;
+      for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
+        const uint32_t stage = wseq & 1, use = wseq >> 1;
+        if (use > 0) mbar_wait(&empty[stage], (use - 1) & 1);
+        uint8_t *yb = ybuf + stage * tp.y_stage_bytes;
+        for (uint32_t qi = 0; qi < p.W; ++qi) {
+          const uint32_t q = win * p.W + qi;
+          while (dep + 1 < p.m) {
+            uint4 c0, c1;
+            node_children(cur, key_cw(key, p.n - p.m + dep + 1), c0, c1);
+            stack[(dep + 1) * (32 * NP) + tix] = c1;
+            cur = c0;
+            ++dep;
+          }
+          uint4 l0, l1;
+          node_children(cur, key_cw(key, p.n), l0, l1);
+          const uint64_t row = row_base + 2 * q;
+          const uint32_t y0 = (valid && row >= p.r0 && row < p.r1) ? leaf_value(l0, cw_out) : 0u;
+          const uint32_t y1 = (valid && row + 1 >= p.r0 && row + 1 < p.r1) ? leaf_value(l1, cw_out) : 0u;
+          // limb planes, K-major core matrices: (k/16, key/8) -> 128 B, row key%8, byte k%16
+          const uint32_t kk = nl * W2 + 2 * qi;
+          const uint32_t off = ((kk >> 4) * (p.Kt >> 3) + (kl >> 3)) * 128u + (kl & 7u) * 16u + (kk & 15u);
+          const uint32_t p01 = __byte_perm(y0, y1, 0x5140), p23 = __byte_perm(y0, y1, 0x7362);
+          *reinterpret_cast<uint16_t *>(yb + off) = uint16_t(p01);
+          *reinterpret_cast<uint16_t *>(yb + ybplane + off) = uint16_t(p01 >> 16);
+          *reinterpret_cast<uint16_t *>(yb + 2 * ybplane + off) = uint16_t(p23);
+          *reinterpret_cast<uint16_t *>(yb + 3 * ybplane + off) = uint16_t(p23 >> 16);
+          if (q + 1 < nq) {
+            const uint32_t k = p.m - 1 - (__ffs(q + 1) - 1);
+            cur = stack[k * (32 * NP) + tix];
+            dep = k;
+          }
+        }
+        fence_proxy_async_smem();  // generic-proxy STS -> visible to the tensor core (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&yfull[stage]);
+      }
+    }
+  } else if (warp < NP + NC) {
+    // ------------------------------------------------ MMA issuer + epilogue
+    const uint32_t q = warp - NP;  // TMEM lane quarter
+    const uint32_t n_dt = D / 128;
+    const uint32_t idesc = umma_idesc_u8(p.Kt);
+    const uint32_t a_lbo = 32u * D, b_lbo = (p.Kt >> 3) * 128u;
+    const uint32_t ybase = smem_u32(ybuf), tbase = smem_u32(tbuf);
+    uint32_t wseq = 0, it = 0;
+    for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+      const uint32_t kt = item % p.n_ktiles;
+      if (q == 0) {
+        if (it > 0) mbar_wait(accempty, (it - 1) & 1);  // epilogue drained the accumulators
+        for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
+          const uint32_t stage = wseq & 1, use = wseq >> 1;
+          mbar_wait(&yfull[stage], use & 1);
+          mbar_wait(&tfull[stage], use & 1);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t yb = ybase + stage * tp.y_stage_bytes, tb = tbase + stage * tp.t_stage_bytes;
+            for (uint32_t cc = 0; cc < Kw / 32; ++cc) {
+              for (uint32_t dt = 0; dt < n_dt; ++dt) {
+#pragma unroll
+                for (uint32_t s = 0; s < 4; ++s) {
+#pragma unroll
+                  for (uint32_t i = 0; i <= s; ++i) {
+                    const uint32_t k = s - i;
+                    const uint64_t ad = umma_desc(tb + k * 8u * D + dt * 1024u + cc * 4u * a_lbo, a_lbo, 128u);
+                    const uint64_t bd = umma_desc(yb + i * ybplane + cc * 2u * b_lbo, b_lbo, 128u);
+                    const uint32_t acc = (win == 0 && cc == 0 && i == 0) ? 0u : 1u;
+                    umma_u8(tmem_base + (dt * 4 + s) * p.Kt, ad, bd, idesc, acc);
+                  }
+                }
+              }
+            }
+            umma_commit(&empty[stage]);               // stage reusable once these MMAs finish
+            if (win + 1 == p.nwin) umma_commit(accfull);  // item's accumulators complete
+          }
+          __syncwarp();
+        }
+      }
+      // epilogue: all NC warps, TMEM lanes 32q..32q+31 = columns d
+      mbar_wait(accfull, it & 1);
+      tc_fence_after();
+      for (uint32_t dt = 0; dt < n_dt; ++dt) {
+        const uint32_t d = dt * 128 + q * 32 + lane;
+        for (uint32_t h = 0; h < p.Kt / 16; ++h) {
+          uint32_t a0[16], a1[16], a2[16], a3[16];
+          const uint32_t taddr = tmem_base + ((q * 32u) << 16) + dt * 4 * p.Kt + h * 16;
+          tmem_ld16(taddr, a0);
+          tmem_ld16(taddr + p.Kt, a1);
+          tmem_ld16(taddr + 2 * p.Kt, a2);
+          tmem_ld16(taddr + 3 * p.Kt, a3);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const uint32_t bkey = kt * p.Kt + h * 16 + j;
+            if (bkey < p.B && d < D) {
+              const uint32_t v = a0[j] + (a1[j] << 8) + (a2[j] << 16) + (a3[j] << 24);
+              const uint32_t neg = key_party(p.keys + uint64_t(bkey) * p.kstride);
+              red_add_u32(p.shares + uint64_t(bkey) * D + d, neg ? 0u - v : v);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(accempty);
+    }
+  } else {
+    // ------------------------------------------------------------ T loader
+    uint32_t wseq = 0;
+    const uint64_t row_bytes = 4ull * D;
+    const uint64_t pend = tp.r0a + tp.packed_rows;
+    for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      const uint32_t ng = item / p.n_ktiles;
+      for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
+        const uint32_t stage = wseq & 1, use = wseq >> 1;
+        if (use > 0) mbar_wait(&empty[stage], (use - 1) & 1);
+        uint8_t *tb = tbuf + stage * tp.t_stage_bytes;
+        uint32_t my_bytes = 0;
+        for (uint32_t nl = lane; nl < p.Ft; nl += 32) {
+          const uint64_t node = uint64_t(ng) * p.Ft + nl;
+          if (node >= p.F) continue;
+          const uint64_t s0 = ((p.lo_f + node) << p.m) + uint64_t(W2) * win;
+          const uint64_t a = s0 > tp.r0a ? s0 : tp.r0a, e = (s0 + W2) < pend ? (s0 + W2) : pend;
+          if (a < e) my_bytes += uint32_t((e - a) * row_bytes);
+        }
+        const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, my_bytes);
+        if (lane == 0) mbar_arrive_expect_tx(&tfull[stage], total);
+        __syncwarp();
+        for (uint32_t nl = lane; nl < p.Ft; nl += 32) {
+          const uint64_t node = uint64_t(ng) * p.Ft + nl;
+          if (node >= p.F) continue;
+          const uint64_t s0 = ((p.lo_f + node) << p.m) + uint64_t(W2) * win;
+          const uint64_t a = s0 > tp.r0a ? s0 : tp.r0a, e = (s0 + W2) < pend ? (s0 + W2) : pend;
+          if (a < e)
+            bulk_g2s(tb + (uint64_t(nl) * W2 + (a - s0)) * row_bytes, tp.packed + (a - tp.r0a) * row_bytes,
+                     uint32_t((e - a) * row_bytes), &tfull[stage]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == NP) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tp.tmem_cols)
+                 : "memory");
+  }
+}
+
+// Limb-pack rows [r0a, r1a) of a shard (8-row aligned; rows outside
+// [r0, r1) are zero): block b = rows r0a+8b..+8, laid out
+// [limb k][d/16][row rr][16 bytes: byte k of T[row][16c .. 16c+15]].
+__global__ void table_pack_kernel(const uint32_t *__restrict__ T, uint64_t r0, uint64_t r1, uint64_t r0a,
+                                  uint64_t nblocks, uint32_t D, uint8_t *__restrict__ out) {
+  const uint32_t nchunk = D / 16;
+  const uint64_t total = nblocks * 8 * nchunk;  // one thread per (block, row, chunk): 16 words in, 4 x 16 B out
+  for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
+       t += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t c = uint32_t(t % nchunk);
+    const uint32_t rr = uint32_t((t / nchunk) % 8);
+    const uint64_t blk = t / (8ull * nchunk);
+    const uint64_t row = r0a + blk * 8 + rr;
+    uint32_t w[16];
+    if (row >= r0 && row < r1) {
+      const uint4 *src = reinterpret_cast<const uint4 *>(T + (row - r0) * D + 16ull * c);
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const uint4 x = __ldg(src + v);
+        w[4 * v] = x.x; w[4 * v + 1] = x.y; w[4 * v + 2] = x.z; w[4 * v + 3] = x.w;
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < 16; ++v) w[v] = 0;
+    }
+    uint8_t *blk_out = out + blk * 32ull * D;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t o[4];
+#pragma unroll
+      for (int g = 0; g < 4; ++g) {
+        const uint32_t sh = 8 * k;
+        o[g] = ((w[4 * g] >> sh) & 0xFF) | (((w[4 * g + 1] >> sh) & 0xFF) << 8) |
+               (((w[4 * g + 2] >> sh) & 0xFF) << 16) | (((w[4 * g + 3] >> sh) & 0xFF) << 24);
+      }
+      *reinterpret_cast<uint4 *>(blk_out + (uint64_t(k) * nchunk + c) * 128 + rr * 16) =
+          make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+}
+
+}  // namespace dev
+}  // namespace dpfpir

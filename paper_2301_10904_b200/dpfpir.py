@@ -74,6 +74,11 @@ def lib() -> ctypes.CDLL:
     L.dpf_eval_batch_wire.argtypes = [vp, u32, u32, vp, u64, u64, u32, vp, vp, sz, vp]
     L.dpf_serve_batch.argtypes = [vp, u32, vp, u64, u64, u32, vp, vp, sz, vp]
     L.dpf_eval_leaves.argtypes = [vp, u32, vp, vp, sz, vp]
+    L.dpf_table_packed_bytes.argtypes = [u64, u64, u32]
+    L.dpf_table_packed_bytes.restype = sz
+    L.dpf_table_pack.argtypes = [vp, u64, u64, u32, vp, vp]
+    L.dpf_eval_batch_packed.argtypes = [vp, u32, vp, u64, u64, u32, vp, vp, sz, vp]
+    L.dpf_eval_batch_wire_packed.argtypes = [vp, u32, u32, vp, u64, u64, u32, vp, vp, sz, vp]
     L.dpf_last_eval_stats.argtypes = [vp]
     L.dpf_kernel_timer_begin.argtypes = [u32]
     L.dpf_kernel_timer_read.argtypes = [vp, u32, vp]
@@ -88,6 +93,7 @@ def lib() -> ctypes.CDLL:
 EXPORTED_SYMBOLS = ("dpf_gen", "dpf_key_wire_size", "dpf_key_serialize", "dpf_key_deserialize", "dpf_reconstruct",
                     "dpf_eval_workspace_bytes", "dpf_eval_batch", "dpf_eval_batch_shard", "dpf_eval_batch_wire",
                     "dpf_serve_batch", "dpf_eval_leaves", "dpf_last_eval_stats", "dpf_kernel_timer_begin",
+                    "dpf_table_packed_bytes", "dpf_table_pack", "dpf_eval_batch_packed", "dpf_eval_batch_wire_packed",
                     "dpf_kernel_timer_read", "dpf_strerror", "dpf_version")
 
 
@@ -268,6 +274,65 @@ def eval_batch_wire(keys_wire_dev, log_n: int, table_shard, row_begin: int = 0, 
     _check(lib().dpf_eval_batch_wire(keys_wire_dev.data_ptr(), B, log_n, table_shard.data_ptr(), row_begin, rows, D,
                                      out.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(),
                                      _stream_ptr(stream)), "dpf_eval_batch_wire")
+    return out
+
+
+class PackedTable:
+    """A device table shard re-laid-out by dpf_table_pack for the tcgen05 path."""
+
+    def __init__(self, data, row_begin: int, row_count: int, D: int):
+        self.data, self.row_begin, self.row_count, self.D = data, row_begin, row_count, D
+
+    @property
+    def shape(self):
+        return (self.row_count, self.D)
+
+
+def table_packed_bytes(row_begin: int, row_count: int, D: int) -> int:
+    return lib().dpf_table_packed_bytes(row_begin, row_count, D)
+
+
+def table_pack(table_shard, row_begin: int = 0, stream=None) -> PackedTable:
+    """dpf_table_pack: limb-packed copy of a row-major CUDA table shard."""
+    import torch
+    _check_table(table_shard)
+    rows, D = table_shard.shape
+    nbytes = table_packed_bytes(row_begin, rows, D)
+    if nbytes == 0:
+        raise DpfError(DPF_EINVAL, "dpf_table_packed_bytes")
+    buf = torch.empty(nbytes, dtype=torch.uint8, device=table_shard.device)
+    _check(lib().dpf_table_pack(table_shard.data_ptr(), row_begin, rows, D, buf.data_ptr(), _stream_ptr(stream)),
+           "dpf_table_pack")
+    return PackedTable(buf, row_begin, rows, D)
+
+
+def eval_batch_packed(keys, packed: PackedTable, out=None, workspace=None, stream=None):
+    """dpf_eval_batch_packed: the tcgen05 contraction path on a packed table shard."""
+    import torch
+    kb = _as_batch(keys)
+    B, D = len(kb), packed.D
+    if out is None:
+        out = torch.empty((B, D), dtype=torch.int32, device=packed.data.device)
+    need = eval_workspace_bytes(B, kb.log_n, packed.row_count, D)
+    ws = workspace if workspace is not None else _workspace(need, packed.data.device)
+    _check(lib().dpf_eval_batch_packed(kb.ptr, B, packed.data.data_ptr(), packed.row_begin, packed.row_count, D,
+                                       out.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(),
+                                       _stream_ptr(stream)), "dpf_eval_batch_packed")
+    return out
+
+
+def eval_batch_wire_packed(keys_wire_dev, log_n: int, packed: PackedTable, out=None, workspace=None, stream=None):
+    """dpf_eval_batch_wire_packed: device-resident wire keys, packed table."""
+    import torch
+    B, D = keys_wire_dev.shape[0], packed.D
+    if out is None:
+        out = torch.empty((B, D), dtype=torch.int32, device=packed.data.device)
+    need = eval_workspace_bytes(B, log_n, packed.row_count, D)
+    ws = workspace if workspace is not None else _workspace(need, packed.data.device)
+    _check(lib().dpf_eval_batch_wire_packed(keys_wire_dev.data_ptr(), B, log_n, packed.data.data_ptr(),
+                                            packed.row_begin, packed.row_count, D, out.data_ptr(), ws.data_ptr(),
+                                            ws.numel() * ws.element_size(), _stream_ptr(stream)),
+           "dpf_eval_batch_wire_packed")
     return out
 
 

@@ -158,3 +158,62 @@ def test_full_size_c3_sampled(dp, oracle):
     want = oracle.answer_batch(ok, T, threads=3)
     for i, b in enumerate(sample):
         np.testing.assert_array_equal((sh0, sh1)[b % 2][b], want[i])
+
+
+# ---------------------------------------------------------------- tcgen05 path
+
+def run_packed_case(dp, oracle, n, N, D, B, seed, row_begin=0, rows=None, T=None):
+    rows = N - row_begin if rows is None else rows
+    T = synth.table(N, D, seed) if T is None else T
+    al = synth.alphas(B, N, seed)
+    keys, okeys = make_keys(dp, oracle, n, al, seed)
+    Tsh = T[row_begin:row_begin + rows]
+    pk = dp.table_pack(to_dev(Tsh), row_begin)
+    got = dp.as_u32(dp.eval_batch_packed(keys, pk))
+    want = oracle.answer_batch(okeys, Tsh, row_begin=row_begin, threads=8)
+    np.testing.assert_array_equal(got, want)
+    # the IMAD path on the row-major table agrees too
+    np.testing.assert_array_equal(dp.as_u32(dp.eval_batch_shard(keys, to_dev(Tsh), row_begin)), want)
+    return got
+
+
+@pytest.mark.parametrize("n,N,D,B", [
+    (12, 4096, 256, 32), (13, 8000, 128, 40), (14, 1 << 14, 256, 64), (10, 1000, 128, 5), (3, 8, 256, 1),
+    (11, 2047, 256, 100), (16, 1 << 16, 128, 33),
+])
+def test_packed_tc_parity(dp, oracle, n, N, D, B):
+    run_packed_case(dp, oracle, n, N, D, B, seed=3000 + n + D + B)
+
+
+def test_packed_tc_shards_unaligned(dp, oracle):
+    n, N, D, B = 13, 6000, 256, 48
+    T = synth.table(N, D, 21)
+    for lo, hi in ((0, 1001), (1001, 4093), (4093, 6000), (5, 13)):
+        run_packed_case(dp, oracle, n, N, D, B, 21, row_begin=lo, rows=hi - lo, T=T)
+
+
+def test_packed_tc_wraps_mod_2_32(dp, oracle):
+    """All-ones limbs over 2^16 leaves overflow every s32 limb accumulator
+    many times: exact results prove the accumulation wraps (no saturation)."""
+    n, N, D, B = 16, 1 << 16, 128, 32
+    T = np.full((N, D), 0xFFFFFFFF, np.uint32)
+    run_packed_case(dp, oracle, n, N, D, B, 31, T=T)
+    T2 = synth.table(N, D, 5) | np.uint32(0xFF00FF00)
+    run_packed_case(dp, oracle, n, N, D, B, 32, T=T2)
+
+
+def test_packed_tc_c3_sampled(dp, oracle):
+    w = synth.CONFIGS["c3"]
+    T = synth.table(w.N, w.D, w.seed)
+    al = synth.alphas(w.B, w.N, w.seed)
+    seeds = synth.gen_seeds(w.B, w.seed)
+    pairs = [dp.gen(w.log_n, int(a), 1, s) for a, s in zip(al, seeds)]
+    pk = dp.table_pack(to_dev(T))
+    sh0 = dp.as_u32(dp.eval_batch_packed([p[0] for p in pairs], pk))
+    sh1 = dp.as_u32(dp.eval_batch_packed([p[1] for p in pairs], pk))
+    np.testing.assert_array_equal(dp.reconstruct(sh0, sh1), T[al.astype(np.int64)])
+    sample = [3, 200]
+    ok = [oracle.key_from_wire(dp.key_serialize(pairs[b][0])) for b in sample]
+    want = oracle.answer_batch(ok, T, threads=2)
+    for i, b in enumerate(sample):
+        np.testing.assert_array_equal(sh0[b], want[i])
