@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
       const uint32_t cw_out = key_cw_out(key);
       uint4 cur = valid ? p.frontier[uint64_t(b) * p.cap + node] : make_uint4(0, 0, 0, 0);
       const uint64_t row_base = (p.lo_f + node) << p.m;
+      const bool inside = valid && row_base >= p.r0 && row_base + (1ull << p.m) <= p.r1;
       uint32_t dep = 0;
       for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
         const uint32_t stage = wseq & 1, use = wseq >> 1;
@@ -283,9 +284,12 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
           }
           uint4 l0, l1;
           node_children(cur, key_cw(key, p.n), l0, l1);
-          const uint64_t row = row_base + 2 * q;
-          const uint32_t y0 = (valid && row >= p.r0 && row < p.r1) ? leaf_value(l0, cw_out) : 0u;
-          const uint32_t y1 = (valid && row + 1 >= p.r0 && row + 1 < p.r1) ? leaf_value(l1, cw_out) : 0u;
+          uint32_t y0 = leaf_value(l0, cw_out), y1 = leaf_value(l1, cw_out);
+          if (!inside) {
+            const uint64_t row = row_base + 2 * q;
+            y0 = (valid && row >= p.r0 && row < p.r1) ? y0 : 0u;
+            y1 = (valid && row + 1 >= p.r0 && row + 1 < p.r1) ? y1 : 0u;
+          }
           if (lane_on) {
             const uint32_t slot = nl * 2 * p.W + 2 * qi;
             yb[slot * p.Kt + kl] = y0;
@@ -433,6 +437,7 @@ KernelChoice choice() {
 
 struct Plan {
   bool tc;  // tcgen05 contraction on a limb-packed table
+  uint32_t nsy;  // y-ring depth (tc)
   uint32_t tmem_cols, y_stage_bytes, t_stage_bytes;
   uint64_t r0a, packed_rows;
   uint32_t n, m, f, Kt, Ft, tasks, W, CG, KG, n_ktiles, n_items, nwin, grid;
@@ -473,17 +478,21 @@ const std::vector<KernelChoice> &tiles() {
   return v;
 }
 
-int producer_warps() {
-  static int np = [] {
-    const char *e = getenv("DPF_NP");  // tuning override: 8, 12 or 16
-    int v = e ? atoi(e) : 8;
-    return (v == 12 || v == 16) ? v : 8;
+// Producer warps of the IMAD kernel: 16 (4 per SMSP, measured best) when the
+// consumer accumulators are small enough to share the register file
+// (Kt*D <= 4096 words per CTA), else 8.  DPF_NP overrides (tuning).
+int producer_warps(uint32_t Kt, uint32_t D) {
+  static int forced = [] {
+    const char *e = getenv("DPF_NP");
+    const int v = e ? atoi(e) : 0;
+    return (v == 8 || v == 12 || v == 16) ? v : 0;
   }();
-  return np;
+  if (forced) return forced;
+  return Kt * D <= 4096 ? 16 : 8;
 }
 
 bool pick_kernel(uint32_t Kt, uint32_t D, Plan &pl) {
-  const int NP = producer_warps();
+  const int NP = producer_warps(Kt, D);
   const std::vector<KernelChoice> &ts = NP == 16 ? tiles<16>() : NP == 12 ? tiles<12>() : tiles<8>();
   uint64_t best = ~0ull;
   for (const KernelChoice &kc : ts) {
@@ -579,10 +588,20 @@ uint32_t choose_m(const Plan &pl, uint32_t n, uint64_t r0, uint32_t m_min, uint3
 
 uint32_t tc_producer_warps() {
   static uint32_t np = [] {
-    const char *e = getenv("DPF_TC_NP");  // tuning override: 8 or 16
-    return (e && atoi(e) == 16) ? 16u : 8u;
+    const char *e = getenv("DPF_TC_NP");  // tuning override: 8, 12 or 16 (default 16)
+    const int v = e ? atoi(e) : 16;
+    return (v == 8 || v == 12) ? uint32_t(v) : 16u;
   }();
   return np;
+}
+
+uint32_t tc_y_stages() {
+  static uint32_t ns = [] {
+    const char *e = getenv("DPF_TC_NSY");  // tuning override: y-ring depth 2..4
+    const int v = e ? atoi(e) : 2;
+    return uint32_t(v < 2 ? 2 : v > 4 ? 4 : v);
+  }();
+  return ns;
 }
 
 // tcgen05 plan (limb-packed table): Kt = 32 keys (N of the MMA), Ft = 8
@@ -599,14 +618,19 @@ int make_tc_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D,
   pl.r0a = r0 & ~7ull;
   pl.packed_rows = ((pl.r1 + 7) & ~7ull) - pl.r0a;
   const uint32_t NP = tc_producer_warps();
-  pl.Kt = 4 * NP;  // 32 or 64 keys = MMA N
+  pl.Kt = 4 * NP;  // 32, 48 or 64 keys = MMA N
+  pl.nsy = tc_y_stages();
   pl.Ft = 32 * NP / pl.Kt;
   pl.tasks = pl.Kt * pl.Ft;
   pl.n_ktiles = (B + pl.Kt - 1) / pl.Kt;
   const uint32_t W = D <= 128 ? 8 : 4;
-  const uint32_t m_min = W == 8 ? 4 : 3;
+  const uint32_t m_min = W == 8 ? 4 : 3;  // 2^(m-1) >= W leaf pairs
   if (n < m_min) return DPF_EINVAL;
-  pl.m = choose_m(pl, n, r0, m_min, std::min<uint32_t>(14, uint32_t((56 * 1024) / (32 * NP * 16))));
+  // SMEM: NSY y stages + 2 T stages + the DFS stack (levels 1..m-2, 16 B per producer thread)
+  const size_t fixed = 1024 + size_t(pl.nsy) * 4 * pl.Kt * pl.Ft * 2 * W + 2ull * pl.Ft * 2 * W * 4 * D;
+  if (fixed + 32ull * NP * 16 > 227 * 1024) return DPF_EINVAL;
+  const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / (32 * NP * 16)));
+  pl.m = choose_m(pl, n, r0, m_min, m_cap);
   pl.f = n - pl.m;
   pl.lo_f = r0 >> pl.m;
   pl.F = ((pl.r1 - 1) >> pl.m) - pl.lo_f + 1;
@@ -622,7 +646,8 @@ int make_tc_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D,
   const uint32_t cols = (D / 128) * 4 * pl.Kt;
   pl.tmem_cols = 32;
   while (pl.tmem_cols < cols) pl.tmem_cols <<= 1;
-  pl.smem_bytes = 1024 + 2 * size_t(pl.y_stage_bytes) + 2 * size_t(pl.t_stage_bytes) + size_t(pl.m) * 32 * NP * 16;
+  pl.smem_bytes = 1024 + size_t(pl.nsy) * pl.y_stage_bytes + 2 * size_t(pl.t_stage_bytes) +
+                  size_t(pl.m) * 32 * NP * 16;  // stack slots 1..m-1 (slot 0 unused)
   if (pl.smem_bytes > 227 * 1024) return DPF_EINVAL;
   pl.grid = std::min<uint32_t>(pl.n_items, uint32_t(num_sms()));
   uint64_t top = 0;
@@ -739,7 +764,13 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
     tp.t_stage_bytes = pl.t_stage_bytes;
     tp.tmem_cols = pl.tmem_cols;
     const uint32_t NP = pl.Kt / 4;
-    auto fn = NP == 16 ? &dev::fused_eval_tc_kernel<16> : &dev::fused_eval_tc_kernel<8>;
+    void (*fn)(const dev::TcParams) = nullptr;
+#define DPF_TC_CASE(np, ns) \
+  if (NP == np && pl.nsy == ns) fn = &dev::fused_eval_tc_kernel<np, ns>;
+    DPF_TC_CASE(8, 2) DPF_TC_CASE(8, 3) DPF_TC_CASE(8, 4) DPF_TC_CASE(12, 2) DPF_TC_CASE(12, 3)
+    DPF_TC_CASE(12, 4) DPF_TC_CASE(16, 2) DPF_TC_CASE(16, 3) DPF_TC_CASE(16, 4)
+#undef DPF_TC_CASE
+    if (!fn) return DPF_EINVAL;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
       return DPF_ECUDA;
     if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);

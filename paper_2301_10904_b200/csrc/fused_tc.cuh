@@ -81,28 +81,42 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
-template <int NP>
+// y limb-plane write for leaves (kk, kk+1) of key kl: K-major core matrices
+// (k/16, key/8) -> 128 B, row key%8, byte k%16; one u16 per limb plane.
+__device__ __forceinline__ void put_leaf_pair(uint8_t *yb, uint32_t ybplane, uint32_t Kt, uint32_t kl, uint32_t kk,
+                                              uint32_t y0, uint32_t y1) {
+  const uint32_t off = ((kk >> 4) * (Kt >> 3) + (kl >> 3)) * 128u + (kl & 7u) * 16u + (kk & 15u);
+  const uint32_t p01 = __byte_perm(y0, y1, 0x5140), p23 = __byte_perm(y0, y1, 0x7362);
+  *reinterpret_cast<uint16_t *>(yb + off) = uint16_t(p01);
+  *reinterpret_cast<uint16_t *>(yb + ybplane + off) = uint16_t(p01 >> 16);
+  *reinterpret_cast<uint16_t *>(yb + 2 * ybplane + off) = uint16_t(p23);
+  *reinterpret_cast<uint16_t *>(yb + 3 * ybplane + off) = uint16_t(p23 >> 16);
+}
+
+// NP producer warps, NSY-deep y ring (T ring: 2 stages).  Named barriers:
+// 1..NSY = y stage FULL (producers arrive, MMA warp syncs); NSY+1 = epilogue.
+template <int NP, int NSY>
 __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(const TcParams tp) {
   constexpr int NC = 4;
   const FusedParams &p = tp.f;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t *yfull = reinterpret_cast<uint64_t *>(smem);  // [2], count NP (producer warps)
-  uint64_t *tfull = yfull + 2;                           // [2], count 1 + tx bytes
-  uint64_t *empty = yfull + 4;                           // [2], count 1 (tcgen05.commit)
-  uint64_t *accfull = yfull + 6;                         // count 1 (tcgen05.commit)
-  uint64_t *accempty = yfull + 7;                        // count NC (epilogue warps)
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + 64);
+  uint64_t *tfull = reinterpret_cast<uint64_t *>(smem);  // [2], count 1 + tx bytes
+  uint64_t *tempty = tfull + 2;                          // [2], count 1 (tcgen05.commit)
+  uint64_t *accfull = tfull + 4;                         // count 1 (tcgen05.commit)
+  uint64_t *accempty = tfull + 5;                        // count NC (epilogue warps)
+  uint64_t *yempty = tfull + 6;                          // [NSY], count 1 (tcgen05.commit)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + 6 * 8 + NSY * 8);
   uint8_t *ybuf = smem + 1024;
-  uint8_t *tbuf = ybuf + 2 * tp.y_stage_bytes;
+  uint8_t *tbuf = ybuf + NSY * tp.y_stage_bytes;
   uint4 *stack = reinterpret_cast<uint4 *>(tbuf + 2 * tp.t_stage_bytes);
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < 2; ++s) {
-      mbar_init(&yfull[s], NP);
       mbar_init(&tfull[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&tempty[s], 1);
     }
+    for (int s = 0; s < NSY; ++s) mbar_init(&yempty[s], 1);
     mbar_init(accfull, 1);
     mbar_init(accempty, NC);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -118,16 +132,21 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const uint32_t nq = 1u << (p.m - 1);
-  const uint32_t W2 = 2 * p.W;               // leaves per node per window (multiple of 8)
-  const uint32_t Kw = p.Ft * W2;             // leaves per window (multiple of 32)
-  const uint32_t ybplane = p.Kt * Kw;        // bytes per y limb plane
+  const uint32_t W2 = 2 * p.W;         // leaves per node per window (multiple of 8)
+  const uint32_t Kw = p.Ft * W2;       // leaves per window (multiple of 32)
+  const uint32_t ybplane = p.Kt * Kw;  // bytes per y limb plane
   const uint32_t D = p.D;
 
   if (warp < NP) {
     // ------------------------------------------------------------ producers
+    // Depth-first over the depth-m subtree: descend to the leaf-parent level
+    // pushing right children on the SMEM stack, expand the leaf-parent (two
+    // leaves), pop the next pending right child.  Warp-uniform schedule;
+    // 2^m - 1 blocks per subtree.  (Measured: this two-site form beats a
+    // single-site "one block per iteration" loop and a 4-leaf "quad" form.)
     const uint32_t tix = warp * 32 + lane;
     const uint32_t kl = tix % p.Kt, nl = tix / p.Kt;
+    const uint32_t nq = 1u << (p.m - 1);
     uint32_t wseq = 0;
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       const uint32_t kt = item % p.n_ktiles, ng = item / p.n_ktiles;
@@ -138,11 +157,12 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
       const uint32_t cw_out = key_cw_out(key);
       uint4 cur = valid ? p.frontier[uint64_t(b) * p.cap + node] : make_uint4(0, 0, 0, 0);
       const uint64_t row_base = (p.lo_f + node) << p.m;
+      const bool inside = valid && row_base >= p.r0 && row_base + (1ull << p.m) <= p.r1;
       uint32_t dep = 0;
       for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
-        const uint32_t stage = wseq & 1, use = wseq >> 1;
-        if (use > 0) mbar_wait(&empty[stage], (use - 1) & 1);
-        uint8_t *yb = ybuf + stage * tp.y_stage_bytes;
+        const uint32_t ys = wseq % NSY, yuse = wseq / NSY;
+        if (yuse > 0) mbar_wait(&yempty[ys], (yuse - 1) & 1);
+        uint8_t *yb = ybuf + ys * tp.y_stage_bytes;
         for (uint32_t qi = 0; qi < p.W; ++qi) {
           const uint32_t q = win * p.W + qi;
           while (dep + 1 < p.m) {
@@ -154,26 +174,21 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
           }
           uint4 l0, l1;
           node_children(cur, key_cw(key, p.n), l0, l1);
-          const uint64_t row = row_base + 2 * q;
-          const uint32_t y0 = (valid && row >= p.r0 && row < p.r1) ? leaf_value(l0, cw_out) : 0u;
-          const uint32_t y1 = (valid && row + 1 >= p.r0 && row + 1 < p.r1) ? leaf_value(l1, cw_out) : 0u;
-          // limb planes, K-major core matrices: (k/16, key/8) -> 128 B, row key%8, byte k%16
-          const uint32_t kk = nl * W2 + 2 * qi;
-          const uint32_t off = ((kk >> 4) * (p.Kt >> 3) + (kl >> 3)) * 128u + (kl & 7u) * 16u + (kk & 15u);
-          const uint32_t p01 = __byte_perm(y0, y1, 0x5140), p23 = __byte_perm(y0, y1, 0x7362);
-          *reinterpret_cast<uint16_t *>(yb + off) = uint16_t(p01);
-          *reinterpret_cast<uint16_t *>(yb + ybplane + off) = uint16_t(p01 >> 16);
-          *reinterpret_cast<uint16_t *>(yb + 2 * ybplane + off) = uint16_t(p23);
-          *reinterpret_cast<uint16_t *>(yb + 3 * ybplane + off) = uint16_t(p23 >> 16);
-          if (q + 1 < nq) {
+          uint32_t y0 = leaf_value(l0, cw_out), y1 = leaf_value(l1, cw_out);
+          if (!inside) {
+            const uint64_t row = row_base + 2 * q;
+            y0 = (valid && row >= p.r0 && row < p.r1) ? y0 : 0u;
+            y1 = (valid && row + 1 >= p.r0 && row + 1 < p.r1) ? y1 : 0u;
+          }
+          put_leaf_pair(yb, ybplane, p.Kt, kl, nl * W2 + 2 * qi, y0, y1);
+          if (q + 1 < nq) {  // pop the right sibling at depth m-1-ctz(q+1)
             const uint32_t k = p.m - 1 - (__ffs(q + 1) - 1);
             cur = stack[k * (32 * NP) + tix];
             dep = k;
           }
         }
         fence_proxy_async_smem();  // generic-proxy STS -> visible to the tensor core (async proxy)
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&yfull[stage]);
+        named_arrive(1 + ys, 32 * (NP + 1));  // the MMA warp sleeps in bar.sync until all producers arrive
       }
     }
   } else if (warp < NP + NC) {
@@ -189,12 +204,12 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
       if (q == 0) {
         if (it > 0) mbar_wait(accempty, (it - 1) & 1);  // epilogue drained the accumulators
         for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
-          const uint32_t stage = wseq & 1, use = wseq >> 1;
-          mbar_wait(&yfull[stage], use & 1);
-          mbar_wait(&tfull[stage], use & 1);
+          const uint32_t ys = wseq % NSY, ts = wseq & 1, tuse = wseq >> 1;
+          named_sync(1 + ys, 32 * (NP + 1));
+          mbar_wait(&tfull[ts], tuse & 1);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t yb = ybase + stage * tp.y_stage_bytes, tb = tbase + stage * tp.t_stage_bytes;
+            const uint32_t yb = ybase + ys * tp.y_stage_bytes, tb = tbase + ts * tp.t_stage_bytes;
             for (uint32_t cc = 0; cc < Kw / 32; ++cc) {
               for (uint32_t dt = 0; dt < n_dt; ++dt) {
 #pragma unroll
@@ -210,32 +225,38 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
                 }
               }
             }
-            umma_commit(&empty[stage]);               // stage reusable once these MMAs finish
+            umma_commit(&yempty[ys]);                     // y stage reusable once these MMAs finish
+            umma_commit(&tempty[ts]);                     // T stage likewise
             if (win + 1 == p.nwin) umma_commit(accfull);  // item's accumulators complete
           }
           __syncwarp();
         }
       }
-      // epilogue: all NC warps, TMEM lanes 32q..32q+31 = columns d
-      mbar_wait(accfull, it & 1);
+      // epilogue: all NC warps, TMEM lanes 32q..32q+31 = columns d.  Only the
+      // MMA warp polls the commit barrier; the others sleep in bar.sync.
+      if (q == 0) mbar_wait(accfull, it & 1);
+      named_sync(NSY + 1, 32 * NC);
       tc_fence_after();
       for (uint32_t dt = 0; dt < n_dt; ++dt) {
         const uint32_t d = dt * 128 + q * 32 + lane;
         for (uint32_t h = 0; h < p.Kt / 16; ++h) {
-          uint32_t a0[16], a1[16], a2[16], a3[16];
+          uint32_t v[16], x[16], z[16];
           const uint32_t taddr = tmem_base + ((q * 32u) << 16) + dt * 4 * p.Kt + h * 16;
-          tmem_ld16(taddr, a0);
-          tmem_ld16(taddr + p.Kt, a1);
-          tmem_ld16(taddr + 2 * p.Kt, a2);
-          tmem_ld16(taddr + 3 * p.Kt, a3);
+          tmem_ld16(taddr, v);
+          tmem_ld16(taddr + p.Kt, x);
+          tmem_wait_ld();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += x[j] << 8;
+          tmem_ld16(taddr + 2 * p.Kt, x);
+          tmem_ld16(taddr + 3 * p.Kt, z);
           tmem_wait_ld();
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const uint32_t bkey = kt * p.Kt + h * 16 + j;
             if (bkey < p.B && d < D) {
-              const uint32_t v = a0[j] + (a1[j] << 8) + (a2[j] << 16) + (a3[j] << 24);
+              const uint32_t val = v[j] + (x[j] << 16) + (z[j] << 24);  // A0 + 2^8 A1 + 2^16 A2 + 2^24 A3
               const uint32_t neg = key_party(p.keys + uint64_t(bkey) * p.kstride);
-              red_add_u32(p.shares + uint64_t(bkey) * D + d, neg ? 0u - v : v);
+              red_add_u32(p.shares + uint64_t(bkey) * D + d, neg ? 0u - val : val);
             }
           }
         }
@@ -252,9 +273,9 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       const uint32_t ng = item / p.n_ktiles;
       for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
-        const uint32_t stage = wseq & 1, use = wseq >> 1;
-        if (use > 0) mbar_wait(&empty[stage], (use - 1) & 1);
-        uint8_t *tb = tbuf + stage * tp.t_stage_bytes;
+        const uint32_t ts = wseq & 1, tuse = wseq >> 1;
+        if (tuse > 0) mbar_wait_sleep(&tempty[ts], (tuse - 1) & 1);
+        uint8_t *tb = tbuf + ts * tp.t_stage_bytes;
         uint32_t my_bytes = 0;
         for (uint32_t nl = lane; nl < p.Ft; nl += 32) {
           const uint64_t node = uint64_t(ng) * p.Ft + nl;
@@ -264,7 +285,7 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
           if (a < e) my_bytes += uint32_t((e - a) * row_bytes);
         }
         const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, my_bytes);
-        if (lane == 0) mbar_arrive_expect_tx(&tfull[stage], total);
+        if (lane == 0) mbar_arrive_expect_tx(&tfull[ts], total);
         __syncwarp();
         for (uint32_t nl = lane; nl < p.Ft; nl += 32) {
           const uint64_t node = uint64_t(ng) * p.Ft + nl;
@@ -273,7 +294,7 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
           const uint64_t a = s0 > tp.r0a ? s0 : tp.r0a, e = (s0 + W2) < pend ? (s0 + W2) : pend;
           if (a < e)
             bulk_g2s(tb + (uint64_t(nl) * W2 + (a - s0)) * row_bytes, tp.packed + (a - tp.r0a) * row_bytes,
-                     uint32_t((e - a) * row_bytes), &tfull[stage]);
+                     uint32_t((e - a) * row_bytes), &tfull[ts]);
         }
       }
     }

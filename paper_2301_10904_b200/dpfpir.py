@@ -19,7 +19,8 @@ from typing import Iterable, Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libdpfpir.so")
+# DPFPIR_LIB overrides the in-tree library (A/B builds during tuning)
+LIB_PATH = os.environ.get("DPFPIR_LIB") or os.path.join(_PKG, "libdpfpir.so")
 
 DPF_MAX_LOG_N = 32
 DPF_PRF_CHACHA20 = 1
