@@ -183,7 +183,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--table", default="auto", choices=["auto", "packed", "rowmajor"],
-                    help="packed = limb-packed table + tcgen05 contraction (D in {128,256}); rowmajor = IMAD path")
+                    help="packed = limb-packed table + tcgen05 contraction (D % 128 == 0); rowmajor = IMAD path")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -210,7 +210,7 @@ def main():
 
     T_host = synth.table_rows(w.N, w.D, w.seed, r0, r0 + rows)
     T = torch.from_numpy(T_host.view(np.int32)).to(dev)
-    use_packed = args.table == "packed" or (args.table == "auto" and w.D in (128, 256) and w.B >= 32)
+    use_packed = args.table == "packed" or (args.table == "auto" and w.D % 128 == 0 and w.D <= 1024 and w.B >= 32)
     # server state: the table is re-laid-out once into u8 limb planes (outside every timed region)
     Tp = dpfpir.table_pack(T, r0) if use_packed else None
     torch.cuda.synchronize()

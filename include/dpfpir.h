@@ -156,14 +156,15 @@ int dpf_eval_batch_wire(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n
  * "tcgen05 contraction").  The table must first be re-laid-out once (server
  * state) by dpf_table_pack into blocks of 8 rows:
  *   block b (rows 8b'..8b'+7 with b' = row_begin/8 + b), 32*D bytes,
- *   [limb k < 4][column chunk c < D/16][row r < 8][16 bytes: byte k of
- *   T[row][16c .. 16c+15]]
+ *   [d-tile t < D/128][limb k < 4][chunk c < 8][row r < 8][16 bytes: byte k
+ *   of T[row][128t + 16c .. 128t + 16c + 15]]
  * Rows of the 8-row blocks outside [row_begin, row_begin+row_count) are
- * zero.  Requirements of the packed eval: D in {128, 256}, log_n >= 3.  The
- * kernel tiles 32 keys per work item, so batches of >= 32 keys use it fully. */
+ * zero.  Requirements: D a multiple of 128, D <= 1024, log_n >= 3.  The
+ * kernel tiles 64 keys per work item (32 for D <= 512, 16 above), so
+ * batches of that many keys use it fully. */
 
 /* Bytes of the packed copy of rows [row_begin, row_begin+row_count) (8-row
- * aligned), 0 if D % 16 != 0 or row_count == 0. */
+ * aligned), 0 if D % 128 != 0 or row_count == 0. */
 size_t dpf_table_packed_bytes(uint64_t row_begin, uint64_t row_count, uint32_t D);
 
 /* Pack a row-major DEVICE table shard (row_count x D uint32, pointing at row
@@ -174,7 +175,7 @@ int dpf_table_pack(const uint32_t *table_shard, uint64_t row_begin, uint64_t row
 
 /* As dpf_eval_batch_shard / dpf_eval_batch_wire, reading the packed table
  * (`packed` from dpf_table_pack with the same row_begin, row_count, D).
- * Same ownership and errors; DPF_EINVAL if D is not 128 or 256. */
+ * Same ownership and errors; DPF_EINVAL if D % 128 != 0 or D > 1024. */
 int dpf_eval_batch_packed(const dpf_key *keys, uint32_t B, const void *packed, uint64_t row_begin,
                           uint64_t row_count, uint32_t D, uint32_t *partial_shares, void *workspace,
                           size_t workspace_bytes, void *stream);

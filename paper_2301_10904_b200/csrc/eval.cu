@@ -416,7 +416,7 @@ namespace {
 constexpr int kNC = 4;  // consumer warps
 constexpr size_t kAlign = 256;
 constexpr uint32_t kMaxTStageBytes = 64 * 1024;
-constexpr uint32_t kMaxTStageBytesW1 = 96 * 1024;
+constexpr uint32_t kMaxTStageBytesW1 = 80 * 1024;  // leaves room for a 64 KB DFS stack
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 inline uint32_t pow2ceil(uint32_t v) {
@@ -437,7 +437,7 @@ KernelChoice choice() {
 
 struct Plan {
   bool tc;  // tcgen05 contraction on a limb-packed table
-  uint32_t nsy;  // y-ring depth (tc)
+  uint32_t nsy, nst;  // y-ring / T-ring depth (tc)
   uint32_t tmem_cols, y_stage_bytes, t_stage_bytes;
   uint64_t r0a, packed_rows;
   uint32_t n, m, f, Kt, Ft, tasks, W, CG, KG, n_ktiles, n_items, nwin, grid;
@@ -525,8 +525,8 @@ int make_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Pl
   if (!pick_kernel(pl.Kt, D, pl)) return DPF_EINVAL;
   const uint32_t NP = uint32_t(pl.kc.NP);
   pl.Ft = 32 * NP / pl.Kt;
-  // T stage must fit: Ft * 2 rows * D words at W = 1.
-  while (uint64_t(pl.Ft) * 2 * D * 4 > kMaxTStageBytesW1 && pl.Ft > 1) pl.Ft >>= 1;
+  // T stage must fit: Ft * 2 rows * D words at W = 1, plus the column padding.
+  while ((uint64_t(pl.Ft) * 2 * D + 32u * pl.kc.CPL * pl.CG) * 4 > kMaxTStageBytesW1 && pl.Ft > 1) pl.Ft >>= 1;
   pl.tasks = pl.Kt * pl.Ft;
   pl.n_ktiles = (B + pl.Kt - 1) / pl.Kt;
   // Subtree depth m (frontier depth f = n - m): the largest m that still
@@ -586,51 +586,39 @@ uint32_t choose_m(const Plan &pl, uint32_t n, uint64_t r0, uint32_t m_min, uint3
   return best;
 }
 
-uint32_t tc_producer_warps() {
-  static uint32_t np = [] {
-    const char *e = getenv("DPF_TC_NP");  // tuning override: 8, 12 or 16 (default 16)
-    const int v = e ? atoi(e) : 16;
-    return (v == 8 || v == 12) ? uint32_t(v) : 16u;
-  }();
-  return np;
-}
+constexpr uint32_t kTcNP = 16;   // producer warps (4 per SMSP)
+constexpr uint32_t kTcNSY = 2;   // y-ring depth
+// T-ring depth (16 KB entries).  8 entries measured no faster than 4 at
+// D = 512/1024, so the SMEM goes to the DFS stack instead.
+inline uint32_t tc_t_stages(uint32_t) { return 4u; }
 
-uint32_t tc_y_stages() {
-  static uint32_t ns = [] {
-    const char *e = getenv("DPF_TC_NSY");  // tuning override: y-ring depth 2..4
-    const int v = e ? atoi(e) : 2;
-    return uint32_t(v < 2 ? 2 : v > 4 ? 4 : v);
-  }();
-  return ns;
-}
-
-// tcgen05 plan (limb-packed table): Kt = 32 keys (N of the MMA), Ft = 8
-// nodes, 2W = 8 or 16 leaves per node per window (whole 8-row packed blocks),
-// D in {128, 256} (M = 128 tiles; 4 limb accumulators x D/128 tiles x 32
-// keys <= 256 TMEM columns).
+// tcgen05 plan (limb-packed table), D a multiple of 128 up to 1024:
+// Kt = MMA N = 64/32/16 keys so that 4 limb accumulators x D/128 tiles x Kt
+// columns fit the 512 TMEM columns; Ft = 512/Kt frontier nodes per item;
+// W = 4 leaf pairs per node per window (one 8-row packed block).
 int make_tc_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl) {
   std::memset(&pl, 0, sizeof pl);
-  if (D % 128 || D > 256 || n < 3) return DPF_EINVAL;
+  if (D % 128 || D > 1024 || n < 3) return DPF_EINVAL;
   pl.tc = true;
   pl.n = n;
   pl.r0 = r0;
   pl.r1 = r0 + rows;
   pl.r0a = r0 & ~7ull;
   pl.packed_rows = ((pl.r1 + 7) & ~7ull) - pl.r0a;
-  const uint32_t NP = tc_producer_warps();
-  pl.Kt = 4 * NP;  // 32, 48 or 64 keys = MMA N
-  pl.nsy = tc_y_stages();
-  pl.Ft = 32 * NP / pl.Kt;
+  pl.Kt = D <= 256 ? 64 : D <= 512 ? 32 : 16;
+  pl.nsy = kTcNSY;
+  pl.Ft = 32 * kTcNP / pl.Kt;
   pl.tasks = pl.Kt * pl.Ft;
   pl.n_ktiles = (B + pl.Kt - 1) / pl.Kt;
-  const uint32_t W = D <= 128 ? 8 : 4;
-  const uint32_t m_min = W == 8 ? 4 : 3;  // 2^(m-1) >= W leaf pairs
-  if (n < m_min) return DPF_EINVAL;
-  // SMEM: NSY y stages + 2 T stages + the DFS stack (levels 1..m-2, 16 B per producer thread)
-  const size_t fixed = 1024 + size_t(pl.nsy) * 4 * pl.Kt * pl.Ft * 2 * W + 2ull * pl.Ft * 2 * W * 4 * D;
-  if (fixed + 32ull * NP * 16 > 227 * 1024) return DPF_EINVAL;
-  const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / (32 * NP * 16)));
-  pl.m = choose_m(pl, n, r0, m_min, m_cap);
+  const uint32_t W = 4;
+  const uint32_t Kw = pl.Ft * 2 * W;
+  pl.y_stage_bytes = 4 * pl.Kt * Kw;
+  // SMEM: T ring + y ring + the DFS stack (16 B per producer thread per level)
+  pl.nst = tc_t_stages(D);
+  const size_t fixed = 1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(kTcNSY) * pl.y_stage_bytes;
+  const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / (32 * kTcNP * 16)));
+  if (m_cap < 3) return DPF_EINVAL;
+  pl.m = choose_m(pl, n, r0, 3, m_cap);
   pl.f = n - pl.m;
   pl.lo_f = r0 >> pl.m;
   pl.F = ((pl.r1 - 1) >> pl.m) - pl.lo_f + 1;
@@ -640,14 +628,10 @@ int make_tc_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D,
   pl.n_items = uint32_t(items);
   pl.W = W;
   pl.nwin = (1u << (pl.m - 1)) / W;
-  const uint32_t Kw = pl.Ft * 2 * W;
-  pl.y_stage_bytes = 4 * pl.Kt * Kw;
-  pl.t_stage_bytes = Kw * 4 * D;
   const uint32_t cols = (D / 128) * 4 * pl.Kt;
   pl.tmem_cols = 32;
   while (pl.tmem_cols < cols) pl.tmem_cols <<= 1;
-  pl.smem_bytes = 1024 + size_t(pl.nsy) * pl.y_stage_bytes + 2 * size_t(pl.t_stage_bytes) +
-                  size_t(pl.m) * 32 * NP * 16;  // stack slots 1..m-1 (slot 0 unused)
+  pl.smem_bytes = fixed + size_t(pl.m) * 32 * kTcNP * 16;  // stack slots 1..m-1 (slot 0 unused)
   if (pl.smem_bytes > 227 * 1024) return DPF_EINVAL;
   pl.grid = std::min<uint32_t>(pl.n_items, uint32_t(num_sms()));
   uint64_t top = 0;
@@ -761,20 +745,12 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
     tp.r0a = pl.r0a;
     tp.packed_rows = pl.packed_rows;
     tp.y_stage_bytes = pl.y_stage_bytes;
-    tp.t_stage_bytes = pl.t_stage_bytes;
     tp.tmem_cols = pl.tmem_cols;
-    const uint32_t NP = pl.Kt / 4;
-    void (*fn)(const dev::TcParams) = nullptr;
-#define DPF_TC_CASE(np, ns) \
-  if (NP == np && pl.nsy == ns) fn = &dev::fused_eval_tc_kernel<np, ns>;
-    DPF_TC_CASE(8, 2) DPF_TC_CASE(8, 3) DPF_TC_CASE(8, 4) DPF_TC_CASE(12, 2) DPF_TC_CASE(12, 3)
-    DPF_TC_CASE(12, 4) DPF_TC_CASE(16, 2) DPF_TC_CASE(16, 3) DPF_TC_CASE(16, 4)
-#undef DPF_TC_CASE
-    if (!fn) return DPF_EINVAL;
+    auto fn = pl.nst == 8 ? &dev::fused_eval_tc_kernel<kTcNP, kTcNSY, 8> : &dev::fused_eval_tc_kernel<kTcNP, kTcNSY, 4>;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
       return DPF_ECUDA;
     if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
-    fn<<<pl.grid, 32 * (NP + 4 + 1), pl.smem_bytes, st>>>(tp);
+    fn<<<pl.grid, 32 * (kTcNP + 4 + 1), pl.smem_bytes, st>>>(tp);
     if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used++ + 1], st);
     ++nk;
     if (cudaGetLastError() != cudaSuccess) return DPF_ECUDA;
@@ -886,14 +862,14 @@ extern "C" size_t dpf_eval_workspace_bytes(uint32_t B, uint32_t log_n, uint64_t 
 }
 
 extern "C" size_t dpf_table_packed_bytes(uint64_t row_begin, uint64_t row_count, uint32_t D) {
-  if (row_count == 0 || D == 0 || D % 16) return 0;
+  if (row_count == 0 || D == 0 || D % 128) return 0;
   const uint64_t r0a = row_begin & ~7ull, r1a = (row_begin + row_count + 7) & ~7ull;
   return size_t((r1a - r0a) * 4ull * D);
 }
 
 extern "C" int dpf_table_pack(const uint32_t *table_shard, uint64_t row_begin, uint64_t row_count, uint32_t D,
                               void *packed, void *stream) {
-  if (!table_shard || !packed || row_count == 0 || D == 0 || D % 16) return DPF_EINVAL;
+  if (!table_shard || !packed || row_count == 0 || D == 0 || D % 128) return DPF_EINVAL;
   if ((reinterpret_cast<uintptr_t>(table_shard) & 15) || (reinterpret_cast<uintptr_t>(packed) & 15))
     return DPF_EINVAL;
   const uint64_t r0a = row_begin & ~7ull, r1a = (row_begin + row_count + 7) & ~7ull;

@@ -10,12 +10,14 @@
 // y_i(j) t_k(j), accumulated in s32 TMEM with saturation OFF (wrapping, so A_s
 // is exact mod 2^32, which is all 2^(8s) A_s mod 2^32 needs).
 //
-// Operands per window (one per ring stage):
+// Operands:
 //   A = table limb plane k, MN-major (M = 128 table columns d, K = leaves),
 //       from the limb-packed table (dpf_table_pack): blocks of 8 rows laid out
-//       [limb][d/16][row(8)][16 d] -- the no-swizzle MN-major core-matrix
-//       layout, so a node's 2W-row segment is ONE contiguous bulk copy;
-//       LBO = 32 D bytes (next 8 rows), SBO = 128 bytes (next 16 columns).
+//       [d-tile (128 cols)][limb][16-col chunk (8)][row (8)][16 bytes] -- the
+//       no-swizzle MN-major core-matrix layout, so one node's 8-row window
+//       segment of one d-tile is ONE contiguous 4 KB bulk copy.  The T ring
+//       holds (32-leaf K-chunk, d-tile) entries of 4 such blocks = 16 KB:
+//       LBO = 4096 bytes (next 8 rows), SBO = 128 bytes (next 16 columns).
 //   B = leaf-share limb plane i, K-major (N = Kt keys, K = leaves), written
 //       by the producers as core matrices [K/16][Kt/8][8 keys][16 leaves];
 //       LBO = (Kt/8) 128 bytes (next 16 leaves), SBO = 128 bytes (next 8 keys).
@@ -29,8 +31,10 @@ struct TcParams {
   FusedParams f;
   const uint8_t *packed;  // limb-packed rows [r0a, r0a + packed_rows)
   uint64_t r0a, packed_rows;
-  uint32_t y_stage_bytes, t_stage_bytes, tmem_cols;
+  uint32_t y_stage_bytes, tmem_cols;
 };
+
+constexpr uint32_t kTcTStageBytes = 16384;  // 32 leaves x 128 columns x 4 limbs
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -93,26 +97,27 @@ __device__ __forceinline__ void put_leaf_pair(uint8_t *yb, uint32_t ybplane, uin
   *reinterpret_cast<uint16_t *>(yb + 3 * ybplane + off) = uint16_t(p23 >> 16);
 }
 
-// NP producer warps, NSY-deep y ring (T ring: 2 stages).  Named barriers:
-// 1..NSY = y stage FULL (producers arrive, MMA warp syncs); NSY+1 = epilogue.
-template <int NP, int NSY>
+// NP producer warps, NSY-deep y ring, NST-deep T ring of (K-chunk, d-tile)
+// entries.  Named barriers: 1..NSY = y stage FULL (producers arrive, the MMA
+// warp syncs); NSY+1 = epilogue.
+template <int NP, int NSY, int NST>
 __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(const TcParams tp) {
   constexpr int NC = 4;
   const FusedParams &p = tp.f;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t *tfull = reinterpret_cast<uint64_t *>(smem);  // [2], count 1 + tx bytes
-  uint64_t *tempty = tfull + 2;                          // [2], count 1 (tcgen05.commit)
-  uint64_t *accfull = tfull + 4;                         // count 1 (tcgen05.commit)
-  uint64_t *accempty = tfull + 5;                        // count NC (epilogue warps)
-  uint64_t *yempty = tfull + 6;                          // [NSY], count 1 (tcgen05.commit)
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + 6 * 8 + NSY * 8);
-  uint8_t *ybuf = smem + 1024;
-  uint8_t *tbuf = ybuf + NSY * tp.y_stage_bytes;
-  uint4 *stack = reinterpret_cast<uint4 *>(tbuf + 2 * tp.t_stage_bytes);
+  uint64_t *tfull = reinterpret_cast<uint64_t *>(smem);  // [NST], count 1 + tx bytes
+  uint64_t *tempty = tfull + NST;                        // [NST], count 1 (tcgen05.commit)
+  uint64_t *yempty = tempty + NST;                       // [NSY], count 1 (tcgen05.commit)
+  uint64_t *accfull = yempty + NSY;                      // count 1 (tcgen05.commit)
+  uint64_t *accempty = accfull + 1;                      // count NC (epilogue warps)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accempty + 1);
+  uint8_t *tbuf = smem + 1024;
+  uint8_t *ybuf = tbuf + NST * kTcTStageBytes;
+  uint4 *stack = reinterpret_cast<uint4 *>(ybuf + NSY * tp.y_stage_bytes);
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < NST; ++s) {
       mbar_init(&tfull[s], 1);
       mbar_init(&tempty[s], 1);
     }
@@ -194,39 +199,45 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
   } else if (warp < NP + NC) {
     // ------------------------------------------------ MMA issuer + epilogue
     const uint32_t q = warp - NP;  // TMEM lane quarter
-    const uint32_t n_dt = D / 128;
+    const uint32_t n_dt = D / 128, n_cc = Kw / 32;
     const uint32_t idesc = umma_idesc_u8(p.Kt);
-    const uint32_t a_lbo = 32u * D, b_lbo = (p.Kt >> 3) * 128u;
+    const uint32_t b_lbo = (p.Kt >> 3) * 128u;
     const uint32_t ybase = smem_u32(ybuf), tbase = smem_u32(tbuf);
-    uint32_t wseq = 0, it = 0;
+    uint32_t wseq = 0, tseq = 0, it = 0;
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
       const uint32_t kt = item % p.n_ktiles;
       if (q == 0) {
         if (it > 0) mbar_wait(accempty, (it - 1) & 1);  // epilogue drained the accumulators
         for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
-          const uint32_t ys = wseq % NSY, ts = wseq & 1, tuse = wseq >> 1;
+          const uint32_t ys = wseq % NSY;
           named_sync(1 + ys, 32 * (NP + 1));
-          mbar_wait(&tfull[ts], tuse & 1);
           tc_fence_after();
-          if (lane == 0) {
-            const uint32_t yb = ybase + ys * tp.y_stage_bytes, tb = tbase + ts * tp.t_stage_bytes;
-            for (uint32_t cc = 0; cc < Kw / 32; ++cc) {
-              for (uint32_t dt = 0; dt < n_dt; ++dt) {
+          const uint32_t yb = ybase + ys * tp.y_stage_bytes;
+          for (uint32_t cc = 0; cc < n_cc; ++cc) {
+            for (uint32_t dt = 0; dt < n_dt; ++dt, ++tseq) {
+              const uint32_t ts = tseq % NST, tuse = tseq / NST;
+              mbar_wait(&tfull[ts], tuse & 1);
+              tc_fence_after();
+              if (lane == 0) {
+                const uint32_t tb = tbase + ts * kTcTStageBytes;
 #pragma unroll
                 for (uint32_t s = 0; s < 4; ++s) {
 #pragma unroll
                   for (uint32_t i = 0; i <= s; ++i) {
                     const uint32_t k = s - i;
-                    const uint64_t ad = umma_desc(tb + k * 8u * D + dt * 1024u + cc * 4u * a_lbo, a_lbo, 128u);
+                    const uint64_t ad = umma_desc(tb + k * 1024u, 4096u, 128u);
                     const uint64_t bd = umma_desc(yb + i * ybplane + cc * 2u * b_lbo, b_lbo, 128u);
                     const uint32_t acc = (win == 0 && cc == 0 && i == 0) ? 0u : 1u;
                     umma_u8(tmem_base + (dt * 4 + s) * p.Kt, ad, bd, idesc, acc);
                   }
                 }
+                umma_commit(&tempty[ts]);  // T entry reusable once these MMAs finish
               }
+              __syncwarp();
             }
-            umma_commit(&yempty[ys]);                     // y stage reusable once these MMAs finish
-            umma_commit(&tempty[ts]);                     // T stage likewise
+          }
+          if (lane == 0) {
+            umma_commit(&yempty[ys]);                     // y stage reusable
             if (win + 1 == p.nwin) umma_commit(accfull);  // item's accumulators complete
           }
           __syncwarp();
@@ -267,34 +278,28 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
     }
   } else {
     // ------------------------------------------------------------ T loader
-    uint32_t wseq = 0;
-    const uint64_t row_bytes = 4ull * D;
+    // Per (window, 32-leaf chunk, d-tile): 4 nodes x one 4 KB packed block.
+    uint32_t tseq = 0;
     const uint64_t pend = tp.r0a + tp.packed_rows;
+    const uint32_t n_dt = D / 128, n_cc = Kw / 32;
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       const uint32_t ng = item / p.n_ktiles;
-      for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
-        const uint32_t ts = wseq & 1, tuse = wseq >> 1;
-        if (tuse > 0) mbar_wait_sleep(&tempty[ts], (tuse - 1) & 1);
-        uint8_t *tb = tbuf + ts * tp.t_stage_bytes;
-        uint32_t my_bytes = 0;
-        for (uint32_t nl = lane; nl < p.Ft; nl += 32) {
-          const uint64_t node = uint64_t(ng) * p.Ft + nl;
-          if (node >= p.F) continue;
+      for (uint32_t win = 0; win < p.nwin; ++win) {
+        for (uint32_t cc = 0; cc < n_cc; ++cc) {
+          // lane j < 4: node 4cc + j, rows [s0, s0 + 8) (one packed block)
+          const uint64_t node = uint64_t(ng) * p.Ft + 4 * cc + (lane & 3);
           const uint64_t s0 = ((p.lo_f + node) << p.m) + uint64_t(W2) * win;
-          const uint64_t a = s0 > tp.r0a ? s0 : tp.r0a, e = (s0 + W2) < pend ? (s0 + W2) : pend;
-          if (a < e) my_bytes += uint32_t((e - a) * row_bytes);
-        }
-        const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, my_bytes);
-        if (lane == 0) mbar_arrive_expect_tx(&tfull[ts], total);
-        __syncwarp();
-        for (uint32_t nl = lane; nl < p.Ft; nl += 32) {
-          const uint64_t node = uint64_t(ng) * p.Ft + nl;
-          if (node >= p.F) continue;
-          const uint64_t s0 = ((p.lo_f + node) << p.m) + uint64_t(W2) * win;
-          const uint64_t a = s0 > tp.r0a ? s0 : tp.r0a, e = (s0 + W2) < pend ? (s0 + W2) : pend;
-          if (a < e)
-            bulk_g2s(tb + (uint64_t(nl) * W2 + (a - s0)) * row_bytes, tp.packed + (a - tp.r0a) * row_bytes,
-                     uint32_t((e - a) * row_bytes), &tfull[ts]);
+          const bool ok = lane < 4 && node < p.F && s0 >= tp.r0a && s0 < pend;
+          const uint32_t total = __popc(__ballot_sync(0xFFFFFFFFu, ok)) * 4096u;
+          for (uint32_t dt = 0; dt < n_dt; ++dt, ++tseq) {
+            const uint32_t ts = tseq % NST, tuse = tseq / NST;
+            if (tuse > 0) mbar_wait(&tempty[ts], (tuse - 1) & 1);
+            if (lane == 0) mbar_arrive_expect_tx(&tfull[ts], total);
+            __syncwarp();
+            if (ok)
+              bulk_g2s(tbuf + ts * kTcTStageBytes + lane * 4096u,
+                       tp.packed + ((s0 - tp.r0a) >> 3) * (32ull * D) + dt * 4096ull, 4096u, &tfull[ts]);
+          }
         }
       }
     }
@@ -309,8 +314,9 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
 }
 
 // Limb-pack rows [r0a, r1a) of a shard (8-row aligned; rows outside
-// [r0, r1) are zero): block b = rows r0a+8b..+8, laid out
-// [limb k][d/16][row rr][16 bytes: byte k of T[row][16c .. 16c+15]].
+// [r0, r1) are zero): block b = rows r0a+8b..+8 (32 D bytes), laid out
+// [d-tile dt][limb k][chunk cl][row rr][16 bytes: byte k of
+// T[row][128 dt + 16 cl .. + 15]].
 __global__ void table_pack_kernel(const uint32_t *__restrict__ T, uint64_t r0, uint64_t r1, uint64_t r0a,
                                   uint64_t nblocks, uint32_t D, uint8_t *__restrict__ out) {
   const uint32_t nchunk = D / 16;
@@ -343,7 +349,8 @@ __global__ void table_pack_kernel(const uint32_t *__restrict__ T, uint64_t r0, u
         o[g] = ((w[4 * g] >> sh) & 0xFF) | (((w[4 * g + 1] >> sh) & 0xFF) << 8) |
                (((w[4 * g + 2] >> sh) & 0xFF) << 16) | (((w[4 * g + 3] >> sh) & 0xFF) << 24);
       }
-      *reinterpret_cast<uint4 *>(blk_out + (uint64_t(k) * nchunk + c) * 128 + rr * 16) =
+      const uint32_t dt = c >> 3, cl = c & 7;  // d-tile (128 columns), 16-column chunk within it
+      *reinterpret_cast<uint4 *>(blk_out + ((uint64_t(dt) * 4 + k) * 8 + cl) * 128 + rr * 16) =
           make_uint4(o[0], o[1], o[2], o[3]);
     }
   }

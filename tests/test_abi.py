@@ -133,3 +133,15 @@ def test_eval_rejects_bad_args_without_gpu(lib):
     k_other, _ = dpfpir.gen(9, 1, 1, bytes(32))
     mixed = dpfpir.KeyBatch.from_keys([k0, k_other])
     assert L.dpf_eval_batch(mixed.ptr, 2, tp, 16, 4, out, wsp, 60000, None) == dpfpir.DPF_EKEY
+
+
+def test_planner_accepts_every_valid_shape(lib):
+    """The host planner (tile choice, subtree depth, SMEM budget) must find a
+    launch plan for every argument combination the header allows."""
+    bad = []
+    for D in range(4, 1025, 4):
+        for B in (1, 3, 17, 64, 100, 1000):
+            for n, rows in ((1, 2), (3, 5), (10, 1000), (20, 1 << 20), (24, 1 << 24)):
+                if dpfpir.eval_workspace_bytes(B, n, rows, D) == 0:
+                    bad.append((D, B, n, rows))
+    assert not bad, bad[:10]

@@ -179,7 +179,8 @@ def run_packed_case(dp, oracle, n, N, D, B, seed, row_begin=0, rows=None, T=None
 
 @pytest.mark.parametrize("n,N,D,B", [
     (12, 4096, 256, 32), (13, 8000, 128, 40), (14, 1 << 14, 256, 64), (10, 1000, 128, 5), (3, 8, 256, 1),
-    (11, 2047, 256, 100), (16, 1 << 16, 128, 33),
+    (11, 2047, 256, 100), (16, 1 << 16, 128, 33), (12, 3000, 384, 40), (11, 2048, 512, 70), (10, 1024, 1024, 20),
+    (13, 5000, 640, 17),
 ])
 def test_packed_tc_parity(dp, oracle, n, N, D, B):
     run_packed_case(dp, oracle, n, N, D, B, seed=3000 + n + D + B)

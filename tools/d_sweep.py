@@ -1,0 +1,57 @@
+"""Entry-size sweep (the paper's Fig. embedding_entry_size_throughput):
+queries/s vs D (int32 words per row) at 2^20 rows, B keys, both contraction
+paths where valid (IMAD on the row-major table; tcgen05 on the packed table).
+    python tools/d_sweep.py [--B 256] [--log-n 20]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_2301_10904_b200 import dpfpir  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--B", type=int, default=256)
+ap.add_argument("--log-n", type=int, default=20)
+ap.add_argument("--D", type=int, nargs="+", default=[16, 32, 64, 128, 256, 512, 1024])
+ap.add_argument("--steps", type=int, default=5)
+args = ap.parse_args()
+n, B = args.log_n, args.B
+N = 1 << n
+al = synth.alphas(B, N, 99)
+keys = [dpfpir.gen(n, int(a), 1, s)[0] for a, s in zip(al, synth.gen_seeds(B, 99))]
+wire = torch.from_numpy(dpfpir.keys_to_wire(keys)).cuda()
+peak = 148 * 64 * 1965e6
+for D in args.D:
+    T = torch.from_numpy(synth.table(N, D, 7).view(np.int32)).cuda()
+    ws = torch.empty(dpfpir.eval_workspace_bytes(B, n, N, D), dtype=torch.uint8, device="cuda")
+    out = torch.empty((B, D), dtype=torch.int32, device="cuda")
+    paths = [("imad", None)]
+    if D % 128 == 0:
+        paths.append(("tcgen05", dpfpir.table_pack(T)))
+    for name, pk in paths:
+        def step():
+            if pk is None:
+                dpfpir.eval_batch_wire(wire, n, T, 0, out=out, workspace=ws)
+            else:
+                dpfpir.eval_batch_wire_packed(wire, n, pk, out=out, workspace=ws)
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / args.steps
+        st = dpfpir.last_eval_stats()
+        print(json.dumps({"D": D, "entry_bytes": 4 * D, "path": name, "B": B, "log_n": n, "ms": round(ms, 3),
+                          "qps": round(B / (ms * 1e-3)), "step_frac_alu": round(640 * B * (N - 1) / (ms * 1e-3) / peak, 3),
+                          "keys_per_tile": st["keys_per_tile"], "frontier_depth": st["frontier_depth"]}), flush=True)
+    del T, ws
