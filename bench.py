@@ -107,12 +107,12 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_keys(w, dpfpir):
+def make_keys(w, dpfpir, prf=1):
     """B client queries of config w: party-0 keys go to this server (the
     second server is an identical, independent machine)."""
     al = synth.alphas(w.B, w.N, w.seed)
     seeds = synth.gen_seeds(w.B, w.seed)
-    pairs = [dpfpir.gen(w.log_n, int(a), 1, s) for a, s in zip(al, seeds)]
+    pairs = [dpfpir.gen(w.log_n, int(a), 1, s, prf=prf) for a, s in zip(al, seeds)]
     return al, pairs
 
 
@@ -144,7 +144,8 @@ def run_reference(args, rank, world):
     from paper_2301_10904_b200 import build as pbuild
     from paper_2301_10904_b200 import dpfpir
     pbuild.build()  # host-side Gen only (client work, outside the timed region)
-    _, pairs = make_keys(w, dpfpir)
+    prf = dpfpir.DPF_PRF_AES128 if args.prf == "aes128" else dpfpir.DPF_PRF_CHACHA20
+    _, pairs = make_keys(w, dpfpir, prf)
     wire = dpfpir.keys_to_wire([p[0] for p in pairs])
     T = synth.table(w.N, w.D, w.seed)
     threads = cpu_threads()
@@ -182,6 +183,8 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--prf", default="chacha20", choices=["chacha20", "aes128"],
+                    help="tree PRF (chacha20 = the paper's fastest standard PRF, Table 5; aes128 = its baseline)")
     ap.add_argument("--table", default="auto", choices=["auto", "packed", "rowmajor"],
                     help="packed = limb-packed table + tcgen05 contraction (D % 128 == 0); rowmajor = IMAD path")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -214,7 +217,8 @@ def main():
     # server state: the table is re-laid-out once into u8 limb planes (outside every timed region)
     Tp = dpfpir.table_pack(T, r0) if use_packed else None
     torch.cuda.synchronize()
-    al, pairs = make_keys(w, dpfpir)
+    prf = dpfpir.DPF_PRF_AES128 if args.prf == "aes128" else dpfpir.DPF_PRF_CHACHA20
+    al, pairs = make_keys(w, dpfpir, prf)
     keys0 = dpfpir.KeyBatch.from_keys([p[0] for p in pairs])
     wire_host = dpfpir.keys_to_wire(keys0)
     wire = torch.from_numpy(wire_host).to(dev)
@@ -224,9 +228,9 @@ def main():
 
     def step():
         if use_packed:
-            dpfpir.eval_batch_wire_packed(wire, w.log_n, Tp, out=out, workspace=ws, stream=stream)
+            dpfpir.eval_batch_wire_packed(wire, w.log_n, Tp, out=out, workspace=ws, stream=stream, prf=prf)
         else:
-            dpfpir.eval_batch_wire(wire, w.log_n, T, r0, out=out, workspace=ws, stream=stream)
+            dpfpir.eval_batch_wire(wire, w.log_n, T, r0, out=out, workspace=ws, stream=stream, prf=prf)
         if G > 1:
             shard.reduce_partial_shares(out, dst=0)
 

@@ -40,8 +40,10 @@ extern "C" {
 #define DPF_KEY_MAGIC 0x4B465044u /* bytes 'D','P','F','K' read as LE u32 */
 #define DPF_KEY_VERSION 1
 
-/* PRF of the tree.  ChaCha20 (Table 5) is the hot-path
- * PRF; AES-128 is a later row. */
+/* PRF of the tree: ChaCha20 (Table 5; the default hot-path
+ * PRF) or AES-128 (the paper's baseline PRF, Table 4), both table-free
+ * on the device (AES bitsliced).  PRF_s(c): ChaCha20 keyed by s || 0^128,
+ * bytes [16c, 16c+16) of block 0; AES-128 keyed by s on block 0^120 || c. */
 enum dpf_prf { DPF_PRF_CHACHA20 = 1, DPF_PRF_AES128 = 2 };
 
 enum dpf_status {
@@ -50,7 +52,7 @@ enum dpf_status {
   DPF_EKEY = -2,         /* malformed key: magic/version/party/log_n/prf mismatch */
   DPF_ENOMEM = -3,       /* workspace too small */
   DPF_ECUDA = -4,        /* CUDA launch/config error (reported synchronously) */
-  DPF_EUNSUPPORTED = -6  /* feature not built (e.g. DPF_PRF_AES128), no sm_100 device */
+  DPF_EUNSUPPORTED = -6  /* unknown PRF id, feature not built, no sm_100 device */
 };
 
 /* One party's DPF key (two codeword matrices C_0, C_1; P:349 root
@@ -79,7 +81,7 @@ typedef struct dpf_key {
  * codewords (deterministic for tests); NULL draws the seed from getrandom().
  * Cost: 2*log_n ChaCha20 blocks.  Errors: DPF_EINVAL if log_n not in
  * [1, 32], alpha >= 2^log_n, k0/k1 NULL; DPF_EUNSUPPORTED if prf is not
- * DPF_PRF_CHACHA20. */
+ * DPF_PRF_CHACHA20 or DPF_PRF_AES128. */
 int dpf_gen(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t prf, const uint8_t *rng_seed,
             dpf_key *k0, dpf_key *k1);
 
@@ -142,10 +144,13 @@ int dpf_eval_batch_shard(const dpf_key *keys, uint32_t B, const uint32_t *table_
 /* Device-resident keys: as dpf_eval_batch_shard, but the B keys are already
  * on the device as consecutive wire-format records (dpf_key_serialize
  * output, stride dpf_key_wire_size(log_n) bytes, 16-byte aligned base),
- * e.g. received by the server straight into HBM.  The keys are NOT
- * re-validated (device memory is not read by the host): callers validate at
- * dpf_key_deserialize time.  No host->device traffic; fully asynchronous. */
-int dpf_eval_batch_wire(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n, const uint32_t *table_shard,
+ * e.g. received by the server straight into HBM; `prf` (enum dpf_prf) must be
+ * the keys' PRF.  The keys are NOT re-validated (device memory is not read by
+ * the host): callers validate at dpf_key_deserialize time.  No host->device
+ * traffic; fully asynchronous (AES keys are bitsliced into a private copy in
+ * the workspace). */
+int dpf_eval_batch_wire(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n, uint32_t prf,
+                        const uint32_t *table_shard,
                         uint64_t row_begin, uint64_t row_count, uint32_t D, uint32_t *partial_shares,
                         void *workspace, size_t workspace_bytes, void *stream);
 
@@ -179,7 +184,8 @@ int dpf_table_pack(const uint32_t *table_shard, uint64_t row_begin, uint64_t row
 int dpf_eval_batch_packed(const dpf_key *keys, uint32_t B, const void *packed, uint64_t row_begin,
                           uint64_t row_count, uint32_t D, uint32_t *partial_shares, void *workspace,
                           size_t workspace_bytes, void *stream);
-int dpf_eval_batch_wire_packed(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n, const void *packed,
+int dpf_eval_batch_wire_packed(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n, uint32_t prf,
+                               const void *packed,
                                uint64_t row_begin, uint64_t row_count, uint32_t D, uint32_t *partial_shares,
                                void *workspace, size_t workspace_bytes, void *stream);
 

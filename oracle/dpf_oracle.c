@@ -79,6 +79,90 @@ void oracle_chacha20_block(const uint8_t key[32], uint32_t counter, const uint8_
 }
 
 /* ------------------------------------------------------------------------ */
+/* O1a. AES-128, FIPS-197 (the paper's baseline PRF, Table 4).  */
+/* Byte-oriented, straight from the standard: the S-box is built from its    */
+/* definition (5.1.1: multiplicative inverse in GF(2^8) mod x^8+x^4+x^3+x+1, */
+/* then the affine map with c = 0x63), not typed in.                          */
+/* ------------------------------------------------------------------------ */
+
+static uint8_t gf_mul(uint8_t a, uint8_t b) { /* FIPS-197 4.2 */
+    uint8_t p = 0;
+    int i;
+    for (i = 0; i < 8; i++) {
+        if (b & 1) p ^= a;
+        b >>= 1;
+        a = (uint8_t)((a << 1) ^ ((a & 0x80) ? 0x1B : 0x00));
+    }
+    return p;
+}
+
+static uint8_t aes_sbox_entry(uint8_t x) { /* FIPS-197 5.1.1 */
+    uint8_t inv = 0, b;
+    int y, i;
+    if (x) {
+        for (y = 1; y < 256; y++)
+            if (gf_mul(x, (uint8_t)y) == 1) { inv = (uint8_t)y; break; }
+    }
+    b = 0;
+    for (i = 0; i < 8; i++) {
+        int bit = ((inv >> i) ^ (inv >> ((i + 4) & 7)) ^ (inv >> ((i + 5) & 7)) ^ (inv >> ((i + 6) & 7)) ^
+                   (inv >> ((i + 7) & 7)) ^ (0x63 >> i)) & 1;
+        b |= (uint8_t)(bit << i);
+    }
+    return b;
+}
+
+static uint8_t aes_sbox[256];
+static pthread_once_t aes_once = PTHREAD_ONCE_INIT;
+static void aes_init(void) {
+    int x;
+    for (x = 0; x < 256; x++) aes_sbox[x] = aes_sbox_entry((uint8_t)x);
+}
+
+uint8_t oracle_aes_sbox(uint8_t x) {
+    pthread_once(&aes_once, aes_init);
+    return aes_sbox[x];
+}
+
+/* FIPS-197 5.2 KeyExpansion (Nk = 4, Nr = 10) and 5.1 Cipher.  State s[r + 4c]
+ * = in[r + 4c] (3.4). */
+void oracle_aes128_encrypt(const uint8_t key[16], const uint8_t in[16], uint8_t out[16]) {
+    uint8_t w[176], st[16], t[4], tmp[16];
+    int i, r, c, round;
+    uint8_t rcon = 0x01;
+    pthread_once(&aes_once, aes_init);
+    memcpy(w, key, 16);
+    for (i = 4; i < 44; i++) {
+        memcpy(t, w + 4 * (i - 1), 4);
+        if (i % 4 == 0) {
+            uint8_t u = t[0]; /* RotWord */
+            t[0] = aes_sbox[t[1]]; t[1] = aes_sbox[t[2]]; t[2] = aes_sbox[t[3]]; t[3] = aes_sbox[u]; /* SubWord */
+            t[0] ^= rcon;
+            rcon = (uint8_t)((rcon << 1) ^ ((rcon & 0x80) ? 0x1B : 0));
+        }
+        for (r = 0; r < 4; r++) w[4 * i + r] = (uint8_t)(w[4 * (i - 4) + r] ^ t[r]);
+    }
+    for (i = 0; i < 16; i++) st[i] = (uint8_t)(in[i] ^ w[i]); /* AddRoundKey(0) */
+    for (round = 1; round <= 10; round++) {
+        for (i = 0; i < 16; i++) st[i] = aes_sbox[st[i]];                 /* SubBytes */
+        for (r = 0; r < 4; r++)                                           /* ShiftRows */
+            for (c = 0; c < 4; c++) tmp[r + 4 * c] = st[r + 4 * ((c + r) % 4)];
+        memcpy(st, tmp, 16);
+        if (round != 10) {                                                /* MixColumns */
+            for (c = 0; c < 4; c++) {
+                uint8_t a0 = st[4 * c], a1 = st[4 * c + 1], a2 = st[4 * c + 2], a3 = st[4 * c + 3];
+                st[4 * c] = (uint8_t)(gf_mul(2, a0) ^ gf_mul(3, a1) ^ a2 ^ a3);
+                st[4 * c + 1] = (uint8_t)(a0 ^ gf_mul(2, a1) ^ gf_mul(3, a2) ^ a3);
+                st[4 * c + 2] = (uint8_t)(a0 ^ a1 ^ gf_mul(2, a2) ^ gf_mul(3, a3));
+                st[4 * c + 3] = (uint8_t)(gf_mul(3, a0) ^ a1 ^ a2 ^ gf_mul(2, a3));
+            }
+        }
+        for (i = 0; i < 16; i++) st[i] ^= w[16 * round + i];             /* AddRoundKey */
+    }
+    memcpy(out, st, 16);
+}
+
+/* ------------------------------------------------------------------------ */
 /* O1'. The tree PRF ("PRF_s(x) encrypts a message x with an          */
 /* encryption key s"; ChaCha20 per P:532, Table 5).  Reading R8: key = */
 /* s || 0^128, counter 0, nonce 0; child c = keystream bytes [16c, 16c+16)   */
@@ -86,7 +170,22 @@ void oracle_chacha20_block(const uint8_t key[32], uint32_t counter, const uint8_
 /* R9: one block per internal node yields both children.                    */
 /* ------------------------------------------------------------------------ */
 
-static void prf_both(const uint8_t s[16], uint8_t child0[16], uint8_t child1[16], uint64_t *blocks) {
+#define ORACLE_PRF_CHACHA20 1
+#define ORACLE_PRF_AES128 2
+
+/* Reading R8 (AES): PRF_s(c) = AES-128 with key s on the block 0^120 || c
+ * (big-endian counter, SP 800-38A CTR); one key schedule, two encryptions
+ * per internal node (R9). */
+static void prf_both_aes(const uint8_t s[16], uint8_t child0[16], uint8_t child1[16], uint64_t *blocks) {
+    uint8_t blk[16];
+    memset(blk, 0, 16);
+    oracle_aes128_encrypt(s, blk, child0);
+    blk[15] = 1;
+    oracle_aes128_encrypt(s, blk, child1);
+    if (blocks) *blocks += 1;
+}
+
+static void prf_both_chacha(const uint8_t s[16], uint8_t child0[16], uint8_t child1[16], uint64_t *blocks) {
     uint8_t key[32], nonce[12], ks[64];
     memset(key, 0, sizeof key);
     memcpy(key, s, 16);
@@ -97,9 +196,22 @@ static void prf_both(const uint8_t s[16], uint8_t child0[16], uint8_t child1[16]
     if (blocks) *blocks += 1;
 }
 
+static void prf_both(uint32_t prf, const uint8_t s[16], uint8_t child0[16], uint8_t child1[16], uint64_t *blocks) {
+    if (prf == ORACLE_PRF_AES128)
+        prf_both_aes(s, child0, child1, blocks);
+    else
+        prf_both_chacha(s, child0, child1, blocks);
+}
+
 void oracle_prf(const uint8_t s[16], uint32_t c, uint8_t out[16]) {
     uint8_t c0[16], c1[16];
-    prf_both(s, c0, c1, NULL);
+    prf_both(ORACLE_PRF_CHACHA20, s, c0, c1, NULL);
+    memcpy(out, c ? c1 : c0, 16);
+}
+
+void oracle_prf_aes(const uint8_t s[16], uint32_t c, uint8_t out[16]) {
+    uint8_t c0[16], c1[16];
+    prf_both(ORACLE_PRF_AES128, s, c0, c1, NULL);
     memcpy(out, c ? c1 : c0, 16);
 }
 
@@ -131,6 +243,7 @@ typedef struct {
     uint32_t log_n;
     uint32_t party;
     uint32_t cw_out;
+    uint32_t prf;  /* 1 = ChaCha20, 2 = AES-128 */
     uint8_t root[16];
     uint8_t cw[ORACLE_MAX_LOG_N][2][2][16];
 } oracle_key;
@@ -185,12 +298,13 @@ static void drbg_bytes(drbg *g, uint8_t *out, int n) {
 /* Returns 0, or -1 on invalid arguments.  *blocks += 2n.                    */
 /* ------------------------------------------------------------------------ */
 
-int oracle_gen(uint32_t log_n, uint64_t alpha, uint32_t beta, const uint8_t rng_seed[32],
-               oracle_key *k0, oracle_key *k1, uint64_t *blocks) {
+int oracle_gen_prf(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t prf, const uint8_t rng_seed[32],
+                   oracle_key *k0, oracle_key *k1, uint64_t *blocks) {
     drbg g;
     uint8_t s0[16], s1[16], p0[2][16], p1[2][16], delta[2][16];
     uint32_t d, n = log_n;
     if (log_n < 1 || log_n > ORACLE_MAX_LOG_N || !k0 || !k1 || !rng_seed) return -1;
+    if (prf != ORACLE_PRF_CHACHA20 && prf != ORACLE_PRF_AES128) return -1;
     if (log_n < 64 && alpha >= ((uint64_t)1 << log_n)) return -1;
     memset(k0, 0, sizeof *k0);
     memset(k1, 0, sizeof *k1);
@@ -202,14 +316,15 @@ int oracle_gen(uint32_t log_n, uint64_t alpha, uint32_t beta, const uint8_t rng_
     memcpy(k0->root, s0, 16);
     memcpy(k1->root, s1, 16);
     k0->log_n = k1->log_n = n;
+    k0->prf = k1->prf = prf;
     k0->party = 0;
     k1->party = 1;
     for (d = 1; d <= n; d++) {
         uint32_t keep = (uint32_t)((alpha >> (n - d)) & 1u), lose = 1u - keep, c;
         uint32_t t0 = lsb_of(s0), t1 = lsb_of(s1);
         uint8_t c0cw[2][16], c1cw[2][16], next0[16], next1[16];
-        prf_both(s0, p0[0], p0[1], blocks);
-        prf_both(s1, p1[0], p1[1], blocks);
+        prf_both(prf, s0, p0[0], p0[1], blocks);
+        prf_both(prf, s1, p1[0], p1[1], blocks);
         xor16(delta[lose], p0[lose], p1[lose]);
         memcpy(delta[keep], delta[lose], 16);
         delta[keep][0] = (uint8_t)((delta[keep][0] & 0xFEu) |
@@ -234,6 +349,11 @@ int oracle_gen(uint32_t log_n, uint64_t alpha, uint32_t beta, const uint8_t rng_
     return 0;
 }
 
+int oracle_gen(uint32_t log_n, uint64_t alpha, uint32_t beta, const uint8_t rng_seed[32], oracle_key *k0,
+               oracle_key *k1, uint64_t *blocks) {
+    return oracle_gen_prf(log_n, alpha, beta, ORACLE_PRF_CHACHA20, rng_seed, k0, k1, blocks);
+}
+
 /* ------------------------------------------------------------------------ */
 /* O2. Node step, Eq. 3: child(s, c, d) = PRF_s(c) + C_{s mod 2}  */
 /* [c, d]; "+" in F_{2^lambda} is XOR (R1).  Child bit at depth d of leaf j  */
@@ -244,7 +364,7 @@ static void node_children(const oracle_key *k, const uint8_t s[16], uint32_t d,
                           uint8_t ch0[16], uint8_t ch1[16], uint64_t *blocks) {
     uint8_t p0[16], p1[16];
     uint32_t t = lsb_of(s);
-    prf_both(s, p0, p1, blocks);
+    prf_both(k->prf, s, p0, p1, blocks);
     xor16(ch0, p0, k->cw[d - 1][t][0]);
     xor16(ch1, p1, k->cw[d - 1][t][1]);
 }
@@ -408,8 +528,9 @@ void oracle_naive_pir_shares(uint64_t N, uint64_t alpha, uint32_t beta, const ui
 
 /* ------------------------------------------------------------------------ */
 /* Key wire format (Table 4 payload): */
-/* 32-byte header  magic 'DPFK' (LE u32 0x4B465044) | version 1 | prf 1      */
-/* (ChaCha20) | party | log_n | cw_out (LE u32) | reserved 0 (LE u32) | root  */
+/* 32-byte header  magic 'DPFK' (LE u32 0x4B465044) | version 1 | prf (1 =   */
+/* ChaCha20, 2 = AES-128) | party | log_n | cw_out (LE u32) | reserved 0 |   */
+/* root                                                                      */
 /* then 64 n bytes: for d = 1..n: [t=0: c=0, c=1][t=1: c=0, c=1] x 16 B.     */
 /* ------------------------------------------------------------------------ */
 
@@ -420,7 +541,7 @@ int oracle_key_to_wire(const oracle_key *k, uint8_t *out, size_t cap) {
     size_t need = oracle_key_wire_size(k->log_n);
     if (cap < need) return -1;
     store_le32(out, 0x4B465044u);
-    out[4] = 1; out[5] = 1; out[6] = (uint8_t)k->party; out[7] = (uint8_t)k->log_n;
+    out[4] = 1; out[5] = (uint8_t)k->prf; out[6] = (uint8_t)k->party; out[7] = (uint8_t)k->log_n;
     store_le32(out + 8, k->cw_out);
     store_le32(out + 12, 0);
     memcpy(out + 16, k->root, 16);
@@ -432,11 +553,12 @@ int oracle_key_to_wire(const oracle_key *k, uint8_t *out, size_t cap) {
 
 int oracle_key_from_wire(const uint8_t *in, size_t len, oracle_key *k) {
     uint32_t d, t, c, n;
-    if (len < 32 || load_le32(in) != 0x4B465044u || in[4] != 1 || in[5] != 1) return -2;
+    if (len < 32 || load_le32(in) != 0x4B465044u || in[4] != 1 || (in[5] != 1 && in[5] != 2)) return -2;
     n = in[7];
     if (n < 1 || n > ORACLE_MAX_LOG_N || len != oracle_key_wire_size(n) || in[6] > 1) return -2;
     memset(k, 0, sizeof *k);
     k->log_n = n;
+    k->prf = in[5];
     k->party = in[6];
     k->cw_out = load_le32(in + 8);
     memcpy(k->root, in + 16, 16);

@@ -33,7 +33,7 @@ def build(force: bool = False) -> str:
 
 class OracleKey(ctypes.Structure):
     _fields_ = [("log_n", ctypes.c_uint32), ("party", ctypes.c_uint32), ("cw_out", ctypes.c_uint32),
-                ("root", ctypes.c_uint8 * 16), ("cw", ctypes.c_uint8 * (MAX_LOG_N * 2 * 2 * 16))]
+                ("prf", ctypes.c_uint32), ("root", ctypes.c_uint8 * 16), ("cw", ctypes.c_uint8 * (MAX_LOG_N * 2 * 2 * 16))]
 
 
 _lib = None
@@ -51,6 +51,12 @@ def lib():
         L.oracle_prf.argtypes = [u8p, ctypes.c_uint32, u8p]
         L.oracle_key_struct_size.restype = ctypes.c_size_t
         L.oracle_gen.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, u8p, kp, kp, u64p]
+        L.oracle_gen_prf.argtypes = [ctypes.c_uint32, ctypes.c_uint64, ctypes.c_uint32, ctypes.c_uint32, u8p, kp, kp,
+                                     u64p]
+        L.oracle_aes128_encrypt.argtypes = [u8p, u8p, u8p]
+        L.oracle_aes_sbox.argtypes = [ctypes.c_uint8]
+        L.oracle_aes_sbox.restype = ctypes.c_uint8
+        L.oracle_prf_aes.argtypes = [u8p, ctypes.c_uint32, u8p]
         L.oracle_eval_point.argtypes = [kp, ctypes.c_uint64, u64p]
         L.oracle_eval_point.restype = ctypes.c_uint32
         L.oracle_eval_full.argtypes = [kp, u32p, u64p]
@@ -92,6 +98,25 @@ def chacha20_block(key: bytes, counter: int, nonce: bytes) -> bytes:
     return out.tobytes()
 
 
+PRF_CHACHA20, PRF_AES128 = 1, 2
+
+
+def aes128_encrypt(key: bytes, block: bytes) -> bytes:
+    out = np.zeros(16, np.uint8)
+    lib().oracle_aes128_encrypt(_u8(_bytes_in(key)), _u8(_bytes_in(block)), _u8(out))
+    return out.tobytes()
+
+
+def aes_sbox(x: int) -> int:
+    return lib().oracle_aes_sbox(x)
+
+
+def prf_aes(seed: bytes, c: int) -> bytes:
+    out = np.zeros(16, np.uint8)
+    lib().oracle_prf_aes(_u8(_bytes_in(seed)), c, _u8(out))
+    return out.tobytes()
+
+
 def prf(seed: bytes, c: int) -> bytes:
     out = np.zeros(16, np.uint8)
     lib().oracle_prf(_u8(_bytes_in(seed)), c, _u8(out))
@@ -100,11 +125,11 @@ def prf(seed: bytes, c: int) -> bytes:
 
 # ---------------------------------------------------------------- DPF
 
-def gen(log_n: int, alpha: int, beta: int, rng_seed: bytes, count_blocks: bool = False):
+def gen(log_n: int, alpha: int, beta: int, rng_seed: bytes, count_blocks: bool = False, prf: int = PRF_CHACHA20):
     k0, k1 = OracleKey(), OracleKey()
     blocks = ctypes.c_uint64(0)
-    rc = lib().oracle_gen(log_n, alpha, beta & 0xFFFFFFFF, _u8(_bytes_in(rng_seed)), ctypes.byref(k0),
-                          ctypes.byref(k1), ctypes.byref(blocks))
+    rc = lib().oracle_gen_prf(log_n, alpha, beta & 0xFFFFFFFF, prf, _u8(_bytes_in(rng_seed)), ctypes.byref(k0),
+                              ctypes.byref(k1), ctypes.byref(blocks))
     if rc:
         raise ValueError("oracle_gen rejected arguments (rc=%d)" % rc)
     return (k0, k1, blocks.value) if count_blocks else (k0, k1)

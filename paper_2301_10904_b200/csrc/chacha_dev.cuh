@@ -44,24 +44,34 @@ __device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
   return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
 }
 
+// PRF policies.  ChaCha20 works on plain seeds; AES-128 (aes_dev.cuh) on
+// bitsliced seeds.  Both keep lsb(s) (R5) at bit 0 of word 0.
+struct PrfChacha {
+  static constexpr uint32_t id = 1;  // DPF_PRF_CHACHA20
+  static __device__ __forceinline__ void children(const uint4 s, uint4 &c0, uint4 &c1) { chacha_children(s, c0, c1); }
+  static __device__ __forceinline__ uint32_t word1(const uint4 s) { return s.y; }  // bytes 4..7 (R6)
+};
+
 // Eq. 3 for both children of node s at depth d-1:
 //   child_c = PRF_s(c) XOR C_{lsb(s)}[c, d]          (R1, R5)
 // lvl_cw points at the key's 64-byte codeword column for depth d, laid out
 // [t][c] (wire format): the control bit selects the row by address.
+template <class Prf>
 __device__ __forceinline__ void node_children(const uint4 s, const uint4 *__restrict__ lvl_cw, uint4 &c0,
                                               uint4 &c1) {
   const uint32_t t = s.x & 1u;
   const uint4 k0 = __ldg(lvl_cw + 2 * t);
   const uint4 k1 = __ldg(lvl_cw + 2 * t + 1);
   uint4 p0, p1;
-  chacha_children(s, p0, p1);
+  Prf::children(s, p0, p1);
   c0 = xor4(p0, k0);
   c1 = xor4(p1, k1);
 }
 
 // Leaf conversion (R2, R6, R7), before the party sign: w1(s) + lsb(s) * cw_out.
+template <class Prf>
 __device__ __forceinline__ uint32_t leaf_value(const uint4 s, uint32_t cw_out) {
-  return s.y + ((s.x & 1u) ? cw_out : 0u);
+  return Prf::word1(s) + ((s.x & 1u) ? cw_out : 0u);
 }
 
 }  // namespace dev

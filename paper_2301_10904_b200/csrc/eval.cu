@@ -31,6 +31,7 @@
 #include <vector>
 
 #include "chacha_dev.cuh"
+#include "aes_dev.cuh"
 #include "dpfpir.h"
 
 namespace dpfpir {
@@ -83,6 +84,26 @@ __device__ __forceinline__ void named_sync(uint32_t id, uint32_t nthreads) {
 __device__ __forceinline__ void named_arrive(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+// Backoff wait for warps that are usually far ahead of the barrier they wait
+// on (the T loader): poll, then sleep 64 ns .. 2 us between polls.
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t *bar, uint32_t parity) {
+  uint32_t ns = 64;
+  while (!mbar_test(bar, parity)) {
+    __nanosleep(ns);
+    ns = ns < 2048 ? 2 * ns : 2048;
+  }
+}
 __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, uint32_t bytes, uint64_t *bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -111,6 +132,7 @@ __device__ __forceinline__ const uint4 *key_cw(const uint8_t *k, uint32_t d) {
 // One launch per level k = 1..f.  Level k's nodes intersecting the row range
 // [r0, r1) are [lo_k, hi_k], lo_k = r0 >> (n-k); stored at [i - lo_k].
 // Thread per (key, parent): both children by one block (R9), kept if in range.
+template <class Prf>
 __global__ void expand_level_kernel(const uint8_t *__restrict__ keys, uint32_t kstride, uint32_t B, uint32_t n,
                                     uint32_t k, uint64_t r0, uint64_t r1, const uint4 *__restrict__ in,
                                     uint4 *__restrict__ out, uint64_t cap) {
@@ -125,7 +147,7 @@ __global__ void expand_level_kernel(const uint8_t *__restrict__ keys, uint32_t k
     const uint8_t *key = keys + uint64_t(b) * kstride;
     const uint4 s = (k == 1) ? key_root(key) : in[uint64_t(b) * cap + (p - plo)];
     uint4 c0, c1;
-    node_children(s, key_cw(key, k), c0, c1);
+    node_children<Prf>(s, key_cw(key, k), c0, c1);
     const uint64_t j0 = 2 * p, j1 = 2 * p + 1;
     if (j0 >= lo && j0 <= hi) out[uint64_t(b) * cap + (j0 - lo)] = c0;
     if (j1 >= lo && j1 <= hi) out[uint64_t(b) * cap + (j1 - lo)] = c1;
@@ -136,6 +158,7 @@ __global__ void expand_level_kernel(const uint8_t *__restrict__ keys, uint32_t k
 // key expands level by level in shared memory (ping-pong), then writes level a
 // to `out`.  Removes a-1 kernel boundaries from the top of the tree.
 constexpr uint32_t kTopSmemLevels = 10;
+template <class Prf>
 __global__ void __launch_bounds__(256) expand_top_smem_kernel(const uint8_t *__restrict__ keys, uint32_t kstride,
                                                               uint32_t n, uint32_t a, uint64_t r0, uint64_t r1,
                                                               uint4 *__restrict__ out, uint64_t cap) {
@@ -151,7 +174,7 @@ __global__ void __launch_bounds__(256) expand_top_smem_kernel(const uint8_t *__r
     uint4 *o = buf[k & 1];
     for (uint64_t p = plo + threadIdx.x; p <= phi; p += blockDim.x) {
       uint4 c0, c1;
-      node_children(in[p - plo], key_cw(key, k), c0, c1);
+      node_children<Prf>(in[p - plo], key_cw(key, k), c0, c1);
       if (2 * p >= lo) o[2 * p - lo] = c0;
       if (2 * p + 1 <= hi) o[2 * p + 1 - lo] = c1;
     }
@@ -226,7 +249,7 @@ __device__ __forceinline__ void consume_window(const uint32_t *__restrict__ yb, 
   }
 }
 
-template <int NP, int NC, int KPW, int CPL>
+template <class Prf, int NP, int NC, int KPW, int CPL>
 __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const FusedParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *tfull = reinterpret_cast<uint64_t *>(smem);  // T-tile ring: bulk-copy completion
@@ -277,14 +300,14 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
           // descend (warp-uniform: every thread shares the schedule)
           while (dep + 1 < p.m) {
             uint4 c0, c1;
-            node_children(cur, key_cw(key, p.n - p.m + dep + 1), c0, c1);
+            node_children<Prf>(cur, key_cw(key, p.n - p.m + dep + 1), c0, c1);
             stack[(dep + 1) * (32 * NP) + tix] = c1;
             cur = c0;
             ++dep;
           }
           uint4 l0, l1;
-          node_children(cur, key_cw(key, p.n), l0, l1);
-          uint32_t y0 = leaf_value(l0, cw_out), y1 = leaf_value(l1, cw_out);
+          node_children<Prf>(cur, key_cw(key, p.n), l0, l1);
+          uint32_t y0 = leaf_value<Prf>(l0, cw_out), y1 = leaf_value<Prf>(l1, cw_out);
           if (!inside) {
             const uint64_t row = row_base + 2 * q;
             y0 = (valid && row >= p.r0 && row < p.r1) ? y0 : 0u;
@@ -389,6 +412,7 @@ namespace dpfpir {
 namespace dev {
 
 // Test/debug leaf dump (branch-parallel: n blocks per leaf).
+template <class Prf>
 __global__ void eval_leaves_kernel(const uint8_t *__restrict__ keys, uint32_t kstride, uint32_t B, uint32_t n,
                                    uint32_t *__restrict__ leaves) {
   const uint64_t N = 1ull << n;
@@ -400,10 +424,10 @@ __global__ void eval_leaves_kernel(const uint8_t *__restrict__ keys, uint32_t ks
     uint4 s = key_root(key);
     for (uint32_t d = 1; d <= n; ++d) {
       uint4 c0, c1;
-      node_children(s, key_cw(key, d), c0, c1);
+      node_children<Prf>(s, key_cw(key, d), c0, c1);
       s = ((j >> (n - d)) & 1) ? c1 : c0;
     }
-    const uint32_t v = leaf_value(s, key_cw_out(key));
+    const uint32_t v = leaf_value<Prf>(s, key_cw_out(key));
     leaves[i] = key_party(key) ? 0u - v : v;
   }
 }
@@ -427,15 +451,18 @@ inline uint32_t pow2ceil(uint32_t v) {
 
 struct KernelChoice {
   int NP, KPW, CPL;
-  void (*fn)(const dev::FusedParams);
+  void (*fn)(const dev::FusedParams);      // ChaCha20
+  void (*fn_aes)(const dev::FusedParams);  // AES-128 (bitsliced)
 };
 
 template <int NP, int KPW, int CPL>
 KernelChoice choice() {
-  return {NP, KPW, CPL, &dev::fused_eval_kernel<NP, kNC, KPW, CPL>};
+  return {NP, KPW, CPL, &dev::fused_eval_kernel<dev::PrfChacha, NP, kNC, KPW, CPL>,
+          &dev::fused_eval_kernel<dev::PrfAesBs, NP, kNC, KPW, CPL>};
 }
 
 struct Plan {
+  uint32_t prf;  // DPF_PRF_CHACHA20 / DPF_PRF_AES128
   bool tc;  // tcgen05 contraction on a limb-packed table
   uint32_t nsy, nst;  // y-ring / T-ring depth (tc)
   uint32_t tmem_cols, y_stage_bytes, t_stage_bytes;
@@ -480,12 +507,12 @@ const std::vector<KernelChoice> &tiles() {
 
 // Producer warps of the IMAD kernel: 16 (4 per SMSP, measured best) when the
 // consumer accumulators are small enough to share the register file
-// (Kt*D <= 4096 words per CTA), else 8.  DPF_NP overrides (tuning).
+// (Kt*D <= 4096 words per CTA), else 8.  DPF_NP=8|16 overrides (tuning).
 int producer_warps(uint32_t Kt, uint32_t D) {
   static int forced = [] {
     const char *e = getenv("DPF_NP");
     const int v = e ? atoi(e) : 0;
-    return (v == 8 || v == 12 || v == 16) ? v : 0;
+    return (v == 8 || v == 16) ? v : 0;
   }();
   if (forced) return forced;
   return Kt * D <= 4096 ? 16 : 8;
@@ -493,7 +520,7 @@ int producer_warps(uint32_t Kt, uint32_t D) {
 
 bool pick_kernel(uint32_t Kt, uint32_t D, Plan &pl) {
   const int NP = producer_warps(Kt, D);
-  const std::vector<KernelChoice> &ts = NP == 16 ? tiles<16>() : NP == 12 ? tiles<12>() : tiles<8>();
+  const std::vector<KernelChoice> &ts = NP == 16 ? tiles<16>() : tiles<8>();
   uint64_t best = ~0ull;
   for (const KernelChoice &kc : ts) {
     for (uint32_t CG : {1u, 2u, 4u}) {
@@ -699,16 +726,26 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
   }
   const uint32_t a = std::min(pl.f, dev::kTopSmemLevels);
   if (a >= 1) {
-    dev::expand_top_smem_kernel<<<B, 256, 0, st>>>(keys_dev, kstride, pl.n, a, pl.r0, pl.r1, ws.front[(pl.f - a) & 1],
-                                                   pl.cap);
+    if (pl.prf == DPF_PRF_AES128)
+      dev::expand_top_smem_kernel<dev::PrfAesBs><<<B, 256, 0, st>>>(keys_dev, kstride, pl.n, a, pl.r0, pl.r1,
+                                                                   ws.front[(pl.f - a) & 1], pl.cap);
+    else
+      dev::expand_top_smem_kernel<dev::PrfChacha><<<B, 256, 0, st>>>(keys_dev, kstride, pl.n, a, pl.r0, pl.r1,
+                                                                    ws.front[(pl.f - a) & 1], pl.cap);
     ++nk;
   }
   for (uint32_t k = a + 1; k <= pl.f; ++k) {
     const uint64_t np = ((pl.r1 - 1) >> (pl.n - (k - 1))) - (pl.r0 >> (pl.n - (k - 1))) + 1;
     const uint64_t total = np * B;
     const uint32_t grid = uint32_t(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
-    dev::expand_level_kernel<<<grid, 256, 0, st>>>(keys_dev, kstride, B, pl.n, k, pl.r0, pl.r1,
-                                                   ws.front[(pl.f - k + 1) & 1], ws.front[(pl.f - k) & 1], pl.cap);
+    if (pl.prf == DPF_PRF_AES128)
+      dev::expand_level_kernel<dev::PrfAesBs><<<grid, 256, 0, st>>>(keys_dev, kstride, B, pl.n, k, pl.r0, pl.r1,
+                                                                   ws.front[(pl.f - k + 1) & 1],
+                                                                   ws.front[(pl.f - k) & 1], pl.cap);
+    else
+      dev::expand_level_kernel<dev::PrfChacha><<<grid, 256, 0, st>>>(keys_dev, kstride, B, pl.n, k, pl.r0, pl.r1,
+                                                                    ws.front[(pl.f - k + 1) & 1],
+                                                                    ws.front[(pl.f - k) & 1], pl.cap);
     ++nk;
   }
   const bool timed = g_timer.on && 2 * g_timer.used + 1 < g_timer.ev.size();
@@ -746,7 +783,8 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
     tp.packed_rows = pl.packed_rows;
     tp.y_stage_bytes = pl.y_stage_bytes;
     tp.tmem_cols = pl.tmem_cols;
-    auto fn = pl.nst == 8 ? &dev::fused_eval_tc_kernel<kTcNP, kTcNSY, 8> : &dev::fused_eval_tc_kernel<kTcNP, kTcNSY, 4>;
+    auto fn = pl.prf == DPF_PRF_AES128 ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4>
+                                       : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4>;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
       return DPF_ECUDA;
     if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
@@ -757,11 +795,11 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
     if (kernels) *kernels = nk;
     return DPF_OK;
   }
-  if (cudaFuncSetAttribute(pl.kc.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) !=
-      cudaSuccess)
+  auto kfn = pl.prf == DPF_PRF_AES128 ? pl.kc.fn_aes : pl.kc.fn;
+  if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
     return DPF_ECUDA;
   if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
-  pl.kc.fn<<<pl.grid, 32 * (pl.kc.NP + kNC + 1), pl.smem_bytes, st>>>(p);
+  kfn<<<pl.grid, 32 * (pl.kc.NP + kNC + 1), pl.smem_bytes, st>>>(p);
   if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used++ + 1], st);
   ++nk;
   if (cudaGetLastError() != cudaSuccess) return DPF_ECUDA;
@@ -781,15 +819,20 @@ int check_common(uint32_t B, const uint32_t *table, uint64_t row_begin, uint64_t
   return DPF_OK;
 }
 
-int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uint32_t log_n,
+int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uint32_t log_n, uint32_t prf,
               const uint32_t *table, uint64_t row_begin, uint64_t rows, uint32_t D, uint32_t *out, void *workspace,
               size_t ws_bytes, cudaStream_t st, bool packed = false) {
   uint32_t n = log_n;
   if (keys) {
     if (B == 0) return DPF_EINVAL;
+    prf = keys[0].prf;
+  }
+  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128) return DPF_EUNSUPPORTED;
+  if (keys) {
+    if (B == 0) return DPF_EINVAL;
     n = keys[0].log_n;
     for (uint32_t b = 0; b < B; ++b) {
-      if (!host_key_valid(keys[b])) return keys[b].prf == DPF_PRF_AES128 ? DPF_EUNSUPPORTED : DPF_EKEY;
+      if (!host_key_valid(keys[b])) return DPF_EKEY;
       if (keys[b].log_n != n || keys[b].prf != keys[0].prf) return DPF_EKEY;
     }
   }
@@ -798,6 +841,7 @@ int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uin
   Plan pl;
   rc = packed ? make_tc_plan(B, n, row_begin, rows, D, pl) : make_plan(B, n, row_begin, rows, D, pl);
   if (rc) return rc;
+  pl.prf = prf;
   const uint32_t kstride = uint32_t(dpf_key_wire_size(n));
   Workspace ws;
   const size_t need = layout(pl, B, kstride, &ws, workspace);
@@ -827,9 +871,23 @@ int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uin
     if (cudaEventRecord(sg.done[slot], st) != cudaSuccess) return DPF_ECUDA;
     kd = ws.keys;
   }
+  uint32_t prep = 0;
+  if (prf == DPF_PRF_AES128) {
+    // the AES path works on bitsliced seeds: bitslice roots and codewords once
+    // (a private copy: caller-owned device keys are never modified)
+    if (kd != ws.keys &&
+        cudaMemcpyAsync(ws.keys, kd, size_t(B) * kstride, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return DPF_ECUDA;
+    const uint64_t items = uint64_t(B) * (1 + 4 * n);
+    dev::aes_bitslice_keys_kernel<<<uint32_t(std::min<uint64_t>((items + 255) / 256, 148ull * 8)), 256, 0, st>>>(
+        ws.keys, kstride, B, n);
+    kd = ws.keys;
+    prep = 1;
+  }
   uint32_t nk = 0;
   rc = launch_eval(pl, kd, kstride, B, table, D, out, ws, st, &nk);
   if (rc) return rc;
+  nk += prep;
   g_stats.prf_blocks = pl.prf_blocks;
   g_stats.kernels = nk;
   g_stats.frontier_depth = pl.f;
@@ -885,24 +943,24 @@ extern "C" int dpf_eval_batch_packed(const dpf_key *keys, uint32_t B, const void
                                      uint64_t row_count, uint32_t D, uint32_t *partial, void *workspace,
                                      size_t workspace_bytes, void *stream) {
   if (!keys) return DPF_EINVAL;
-  return eval_impl(keys, B, nullptr, 0, static_cast<const uint32_t *>(packed), row_begin, row_count, D, partial,
+  return eval_impl(keys, B, nullptr, 0, 0, static_cast<const uint32_t *>(packed), row_begin, row_count, D, partial,
                    workspace, workspace_bytes, static_cast<cudaStream_t>(stream), true);
 }
 
-extern "C" int dpf_eval_batch_wire_packed(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n,
+extern "C" int dpf_eval_batch_wire_packed(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n, uint32_t prf,
                                           const void *packed, uint64_t row_begin, uint64_t row_count, uint32_t D,
                                           uint32_t *partial, void *workspace, size_t workspace_bytes, void *stream) {
   if (!keys_wire_dev || (reinterpret_cast<uintptr_t>(keys_wire_dev) & 15)) return DPF_EINVAL;
-  return eval_impl(nullptr, B, keys_wire_dev, log_n, static_cast<const uint32_t *>(packed), row_begin, row_count, D,
-                   partial, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), true);
+  return eval_impl(nullptr, B, keys_wire_dev, log_n, prf, static_cast<const uint32_t *>(packed), row_begin, row_count,
+                   D, partial, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), true);
 }
 
 extern "C" int dpf_eval_batch_shard(const dpf_key *keys, uint32_t B, const uint32_t *table_shard,
                                     uint64_t row_begin, uint64_t row_count, uint32_t D, uint32_t *partial,
                                     void *workspace, size_t workspace_bytes, void *stream) {
   if (!keys) return DPF_EINVAL;
-  return eval_impl(keys, B, nullptr, 0, table_shard, row_begin, row_count, D, partial, workspace, workspace_bytes,
-                   static_cast<cudaStream_t>(stream));
+  return eval_impl(keys, B, nullptr, 0, 0, table_shard, row_begin, row_count, D, partial, workspace,
+                   workspace_bytes, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int dpf_eval_batch(const dpf_key *keys, uint32_t B, const uint32_t *table, uint64_t N, uint32_t D,
@@ -910,11 +968,11 @@ extern "C" int dpf_eval_batch(const dpf_key *keys, uint32_t B, const uint32_t *t
   return dpf_eval_batch_shard(keys, B, table, 0, N, D, shares, workspace, workspace_bytes, stream);
 }
 
-extern "C" int dpf_eval_batch_wire(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n,
+extern "C" int dpf_eval_batch_wire(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n, uint32_t prf,
                                    const uint32_t *table_shard, uint64_t row_begin, uint64_t row_count, uint32_t D,
                                    uint32_t *partial, void *workspace, size_t workspace_bytes, void *stream) {
   if (!keys_wire_dev || (reinterpret_cast<uintptr_t>(keys_wire_dev) & 15)) return DPF_EINVAL;
-  return eval_impl(nullptr, B, keys_wire_dev, log_n, table_shard, row_begin, row_count, D, partial, workspace,
+  return eval_impl(nullptr, B, keys_wire_dev, log_n, prf, table_shard, row_begin, row_count, D, partial, workspace,
                    workspace_bytes, static_cast<cudaStream_t>(stream));
 }
 
@@ -929,7 +987,7 @@ extern "C" int dpf_serve_batch(const dpf_key *keys, uint32_t B, const uint32_t *
   if (workspace_bytes < need + out_bytes) return DPF_ENOMEM;
   uint32_t *dev_out = reinterpret_cast<uint32_t *>(static_cast<uint8_t *>(workspace) + need);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int rc = eval_impl(keys, B, nullptr, 0, table_shard, row_begin, row_count, D, dev_out, workspace, need, st);
+  int rc = eval_impl(keys, B, nullptr, 0, 0, table_shard, row_begin, row_count, D, dev_out, workspace, need, st);
   if (rc) return rc;
   if (cudaMemcpyAsync(shares_host, dev_out, size_t(B) * D * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
     return DPF_ECUDA;
@@ -942,7 +1000,7 @@ extern "C" int dpf_eval_leaves(const dpf_key *keys, uint32_t B, uint32_t *leaves
   if (!keys || B == 0 || !leaves || !workspace) return DPF_EINVAL;
   const uint32_t n = keys[0].log_n;
   for (uint32_t b = 0; b < B; ++b)
-    if (!host_key_valid(keys[b]) || keys[b].log_n != n) return DPF_EKEY;
+    if (!host_key_valid(keys[b]) || keys[b].log_n != n || keys[b].prf != keys[0].prf) return DPF_EKEY;
   if (n > 20) return DPF_EINVAL;
   const uint32_t kstride = uint32_t(dpf_key_wire_size(n));
   if (workspace_bytes < size_t(B) * kstride) return DPF_ENOMEM;
@@ -953,7 +1011,13 @@ extern "C" int dpf_eval_leaves(const dpf_key *keys, uint32_t B, uint32_t *leaves
     return DPF_ECUDA;
   const uint64_t total = (uint64_t(B) << n);
   const uint32_t grid = uint32_t(std::min<uint64_t>((total + 255) / 256, 148ull * 8));
-  dev::eval_leaves_kernel<<<grid, 256, 0, st>>>(static_cast<uint8_t *>(workspace), kstride, B, n, leaves);
+  uint8_t *kd = static_cast<uint8_t *>(workspace);
+  if (keys[0].prf == DPF_PRF_AES128) {
+    dev::aes_bitslice_keys_kernel<<<uint32_t((B * (1 + 4 * n) + 255) / 256), 256, 0, st>>>(kd, kstride, B, n);
+    dev::eval_leaves_kernel<dev::PrfAesBs><<<grid, 256, 0, st>>>(kd, kstride, B, n, leaves);
+  } else {
+    dev::eval_leaves_kernel<dev::PrfChacha><<<grid, 256, 0, st>>>(kd, kstride, B, n, leaves);
+  }
   if (cudaGetLastError() != cudaSuccess) return DPF_ECUDA;
   // staged is pageable: the H2D above completed its staging before return.
   return DPF_OK;

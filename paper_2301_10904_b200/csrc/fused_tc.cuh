@@ -100,7 +100,7 @@ __device__ __forceinline__ void put_leaf_pair(uint8_t *yb, uint32_t ybplane, uin
 // NP producer warps, NSY-deep y ring, NST-deep T ring of (K-chunk, d-tile)
 // entries.  Named barriers: 1..NSY = y stage FULL (producers arrive, the MMA
 // warp syncs); NSY+1 = epilogue.
-template <int NP, int NSY, int NST>
+template <class Prf, int NP, int NSY, int NST>
 __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(const TcParams tp) {
   constexpr int NC = 4;
   const FusedParams &p = tp.f;
@@ -172,14 +172,14 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
           const uint32_t q = win * p.W + qi;
           while (dep + 1 < p.m) {
             uint4 c0, c1;
-            node_children(cur, key_cw(key, p.n - p.m + dep + 1), c0, c1);
+            node_children<Prf>(cur, key_cw(key, p.n - p.m + dep + 1), c0, c1);
             stack[(dep + 1) * (32 * NP) + tix] = c1;
             cur = c0;
             ++dep;
           }
           uint4 l0, l1;
-          node_children(cur, key_cw(key, p.n), l0, l1);
-          uint32_t y0 = leaf_value(l0, cw_out), y1 = leaf_value(l1, cw_out);
+          node_children<Prf>(cur, key_cw(key, p.n), l0, l1);
+          uint32_t y0 = leaf_value<Prf>(l0, cw_out), y1 = leaf_value<Prf>(l1, cw_out);
           if (!inside) {
             const uint64_t row = row_base + 2 * q;
             y0 = (valid && row >= p.r0 && row < p.r1) ? y0 : 0u;
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
           const uint32_t total = __popc(__ballot_sync(0xFFFFFFFFu, ok)) * 4096u;
           for (uint32_t dt = 0; dt < n_dt; ++dt, ++tseq) {
             const uint32_t ts = tseq % NST, tuse = tseq / NST;
-            if (tuse > 0) mbar_wait(&tempty[ts], (tuse - 1) & 1);
+            if (tuse > 0) mbar_wait_backoff(&tempty[ts], (tuse - 1) & 1);
             if (lane == 0) mbar_arrive_expect_tx(&tfull[ts], total);
             __syncwarp();
             if (ok)

@@ -1,6 +1,7 @@
 // host.cc -- client-side half of libdpfpir: Gen, key codec, reconstruct,
-// status strings.  Independent of oracle/ (own ChaCha20, own Gen); the tests
-// check that both produce the same keys from the same DRBG seed.
+// status strings.  Independent of oracle/ (own ChaCha20, own AES-128, own
+// Gen); the tests check that both produce the same keys from the same DRBG
+// seed, for both PRFs.
 //
 // Citations: P:n = PAPER.md line n; R1..R14 = DESIGN.md "Readings".
 #include "dpfpir.h"
@@ -36,14 +37,72 @@ void chacha20_words(const uint32_t key[8], uint32_t counter, const uint32_t nonc
   for (int i = 0; i < 16; ++i) out[i] = w[i] + st[i];
 }
 
-// Tree PRF (R8, R9): one block keyed by s || 0^128 with counter 0, nonce 0;
-// child 0 = words 0..3, child 1 = words 4..7 of the keystream.
-void prf_pair(const Words4 &s, Words4 &c0, Words4 &c1) {
+// Tree PRF (R8, R9).  ChaCha20: one block keyed by s || 0^128 with counter 0,
+// nonce 0; child 0 = words 0..3, child 1 = words 4..7 of the keystream.
+// AES-128: key s, child c = AES_s(0^120 || c).
+void prf_pair_chacha(const Words4 &s, Words4 &c0, Words4 &c1) {
   const uint32_t key[8] = {s[0], s[1], s[2], s[3], 0, 0, 0, 0};
   const uint32_t nonce[3] = {0, 0, 0};
   uint32_t ks[16];
   chacha20_words(key, 0, nonce, ks);
   for (int i = 0; i < 4; ++i) { c0[i] = ks[i]; c1[i] = ks[4 + i]; }
+}
+
+// ---- AES-128 (FIPS-197) for the client-side Gen with DPF_PRF_AES128.
+// Byte-oriented; the S-box is derived at first use from GF(2^8) logarithms
+// (generator 3), then the affine map of FIPS-197 5.1.1.
+struct AesTables {
+  uint8_t sbox[256];
+  AesTables() {
+    uint8_t exp[256], log[256] = {0};
+    uint8_t g = 1;
+    for (int i = 0; i < 255; ++i) {
+      exp[i] = g;
+      log[g] = uint8_t(i);
+      g = uint8_t(g ^ (g << 1) ^ ((g & 0x80) ? 0x1B : 0));  // g *= 3
+    }
+    for (int x = 0; x < 256; ++x) {
+      const uint8_t inv = x ? exp[(255 - log[x]) % 255] : 0;
+      uint8_t b = inv;
+      for (int r = 1; r <= 4; ++r) b ^= uint8_t((inv << r) | (inv >> (8 - r)));
+      sbox[x] = uint8_t(b ^ 0x63);
+    }
+  }
+};
+const AesTables &aes_tables() {
+  static const AesTables t;
+  return t;
+}
+inline uint8_t xt(uint8_t a) { return uint8_t((a << 1) ^ ((a & 0x80) ? 0x1B : 0)); }
+
+void aes128_encrypt_block(const uint8_t key[16], const uint8_t in[16], uint8_t out[16]) {
+  const uint8_t *S = aes_tables().sbox;
+  uint8_t rk[16], st[16];
+  std::memcpy(rk, key, 16);
+  for (int i = 0; i < 16; ++i) st[i] = in[i] ^ rk[i];
+  uint8_t rcon = 1;
+  for (int round = 1; round <= 10; ++round) {
+    uint8_t t[16];
+    for (int c = 0; c < 4; ++c)  // SubBytes + ShiftRows
+      for (int r = 0; r < 4; ++r) t[4 * c + r] = S[st[4 * ((c + r) & 3) + r]];
+    if (round < 10) {
+      for (int c = 0; c < 4; ++c) {  // MixColumns
+        uint8_t *a = t + 4 * c;
+        const uint8_t all = a[0] ^ a[1] ^ a[2] ^ a[3], a0 = a[0];
+        a[0] ^= all ^ xt(a[0] ^ a[1]);
+        a[1] ^= all ^ xt(a[1] ^ a[2]);
+        a[2] ^= all ^ xt(a[2] ^ a[3]);
+        a[3] ^= all ^ xt(a[3] ^ a0);
+      }
+    }
+    // next round key
+    uint8_t w[4] = {uint8_t(S[rk[13]] ^ rcon), S[rk[14]], S[rk[15]], S[rk[12]]};
+    rcon = xt(rcon);
+    for (int c = 0; c < 4; ++c)
+      for (int r = 0; r < 4; ++r) w[r] = rk[4 * c + r] ^= w[r];
+    for (int i = 0; i < 16; ++i) st[i] = t[i] ^ rk[i];
+  }
+  std::memcpy(out, st, 16);
 }
 
 inline uint32_t ld32(const uint8_t *p) {
@@ -54,6 +113,23 @@ inline void st32(uint8_t *p, uint32_t v) {
 }
 inline Words4 from_bytes(const uint8_t *p) { return {ld32(p), ld32(p + 4), ld32(p + 8), ld32(p + 12)}; }
 inline void to_bytes(const Words4 &w, uint8_t *p) { for (int i = 0; i < 4; ++i) st32(p + 4 * i, w[i]); }
+
+void prf_pair_aes(const Words4 &s, Words4 &c0, Words4 &c1) {
+  uint8_t key[16], blk[16] = {0}, o[16];
+  to_bytes(s, key);
+  aes128_encrypt_block(key, blk, o);
+  c0 = from_bytes(o);
+  blk[15] = 1;
+  aes128_encrypt_block(key, blk, o);
+  c1 = from_bytes(o);
+}
+
+void prf_pair(uint32_t prf, const Words4 &s, Words4 &c0, Words4 &c1) {
+  if (prf == DPF_PRF_AES128)
+    prf_pair_aes(s, c0, c1);
+  else
+    prf_pair_chacha(s, c0, c1);
+}
 inline Words4 xor4(const Words4 &a, const Words4 &b) { return {a[0] ^ b[0], a[1] ^ b[1], a[2] ^ b[2], a[3] ^ b[3]}; }
 
 // Gen's randomness: the ChaCha20 keystream under key = rng_seed, nonce 0,
@@ -83,7 +159,8 @@ class KeystreamDrbg {
 };
 
 bool key_ok(const dpf_key &k) {
-  return k.magic == DPF_KEY_MAGIC && k.version == DPF_KEY_VERSION && k.prf == DPF_PRF_CHACHA20 &&
+  return k.magic == DPF_KEY_MAGIC && k.version == DPF_KEY_VERSION &&
+         (k.prf == DPF_PRF_CHACHA20 || k.prf == DPF_PRF_AES128) &&
          k.party <= 1 && k.log_n >= 1 && k.log_n <= DPF_MAX_LOG_N && (k.root[0] & 1u) == k.party &&
          k.reserved == 0;
 }
@@ -97,7 +174,7 @@ extern "C" int dpf_gen(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t p
                        dpf_key *k0, dpf_key *k1) {
   if (!k0 || !k1 || log_n < 1 || log_n > DPF_MAX_LOG_N) return DPF_EINVAL;
   if (alpha >> log_n) return DPF_EINVAL;
-  if (prf != DPF_PRF_CHACHA20) return DPF_EUNSUPPORTED;
+  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128) return DPF_EUNSUPPORTED;
   uint8_t seed[32];
   if (rng_seed) {
     std::memcpy(seed, rng_seed, 32);
@@ -120,7 +197,7 @@ extern "C" int dpf_gen(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t p
     if (p) std::memset(&k, 0, sizeof k);
     k.magic = DPF_KEY_MAGIC;
     k.version = DPF_KEY_VERSION;
-    k.prf = DPF_PRF_CHACHA20;
+    k.prf = uint8_t(prf);
     k.party = uint8_t(p);
     k.log_n = uint8_t(log_n);
     to_bytes(s[p], k.root);
@@ -128,8 +205,8 @@ extern "C" int dpf_gen(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t p
   for (uint32_t d = 1; d <= log_n; ++d) {
     const unsigned keep = unsigned(alpha >> (log_n - d)) & 1u, lose = keep ^ 1u;
     Words4 P[2][2];  // P[party][child]
-    prf_pair(s[0], P[0][0], P[0][1]);
-    prf_pair(s[1], P[1][0], P[1][1]);
+    prf_pair(prf, s[0], P[0][0], P[0][1]);
+    prf_pair(prf, s[1], P[1][0], P[1][1]);
     // Correction (BGI-style, R2/R3): the lose child of the two parties must
     // coincide; the keep child keeps differing control bits.
     Words4 delta[2];

@@ -72,14 +72,14 @@ def lib() -> ctypes.CDLL:
     L.dpf_eval_workspace_bytes.restype = sz
     L.dpf_eval_batch.argtypes = [vp, u32, vp, u64, u32, vp, vp, sz, vp]
     L.dpf_eval_batch_shard.argtypes = [vp, u32, vp, u64, u64, u32, vp, vp, sz, vp]
-    L.dpf_eval_batch_wire.argtypes = [vp, u32, u32, vp, u64, u64, u32, vp, vp, sz, vp]
+    L.dpf_eval_batch_wire.argtypes = [vp, u32, u32, u32, vp, u64, u64, u32, vp, vp, sz, vp]
     L.dpf_serve_batch.argtypes = [vp, u32, vp, u64, u64, u32, vp, vp, sz, vp]
     L.dpf_eval_leaves.argtypes = [vp, u32, vp, vp, sz, vp]
     L.dpf_table_packed_bytes.argtypes = [u64, u64, u32]
     L.dpf_table_packed_bytes.restype = sz
     L.dpf_table_pack.argtypes = [vp, u64, u64, u32, vp, vp]
     L.dpf_eval_batch_packed.argtypes = [vp, u32, vp, u64, u64, u32, vp, vp, sz, vp]
-    L.dpf_eval_batch_wire_packed.argtypes = [vp, u32, u32, vp, u64, u64, u32, vp, vp, sz, vp]
+    L.dpf_eval_batch_wire_packed.argtypes = [vp, u32, u32, u32, vp, u64, u64, u32, vp, vp, sz, vp]
     L.dpf_last_eval_stats.argtypes = [vp]
     L.dpf_kernel_timer_begin.argtypes = [u32]
     L.dpf_kernel_timer_read.argtypes = [vp, u32, vp]
@@ -140,6 +140,10 @@ class KeyBatch:
     @property
     def log_n(self) -> int:
         return int(self.raw[0, 7])
+
+    @property
+    def prf(self) -> int:
+        return int(self.raw[0, 5])
 
 
 def _as_batch(keys) -> KeyBatch:
@@ -262,7 +266,7 @@ def keys_to_wire(keys) -> np.ndarray:
 
 
 def eval_batch_wire(keys_wire_dev, log_n: int, table_shard, row_begin: int = 0, out=None, workspace=None,
-                    stream=None):
+                    stream=None, prf: int = DPF_PRF_CHACHA20):
     """dpf_eval_batch_wire: keys already in HBM as wire records (uint8 CUDA tensor [B, 32+64n])."""
     import torch
     _check_table(table_shard)
@@ -272,7 +276,7 @@ def eval_batch_wire(keys_wire_dev, log_n: int, table_shard, row_begin: int = 0, 
         out = torch.empty((B, D), dtype=torch.int32, device=table_shard.device)
     need = eval_workspace_bytes(B, log_n, rows, D)
     ws = workspace if workspace is not None else _workspace(need, table_shard.device)
-    _check(lib().dpf_eval_batch_wire(keys_wire_dev.data_ptr(), B, log_n, table_shard.data_ptr(), row_begin, rows, D,
+    _check(lib().dpf_eval_batch_wire(keys_wire_dev.data_ptr(), B, log_n, prf, table_shard.data_ptr(), row_begin, rows, D,
                                      out.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(),
                                      _stream_ptr(stream)), "dpf_eval_batch_wire")
     return out
@@ -322,7 +326,8 @@ def eval_batch_packed(keys, packed: PackedTable, out=None, workspace=None, strea
     return out
 
 
-def eval_batch_wire_packed(keys_wire_dev, log_n: int, packed: PackedTable, out=None, workspace=None, stream=None):
+def eval_batch_wire_packed(keys_wire_dev, log_n: int, packed: PackedTable, out=None, workspace=None, stream=None,
+                           prf: int = DPF_PRF_CHACHA20):
     """dpf_eval_batch_wire_packed: device-resident wire keys, packed table."""
     import torch
     B, D = keys_wire_dev.shape[0], packed.D
@@ -330,7 +335,7 @@ def eval_batch_wire_packed(keys_wire_dev, log_n: int, packed: PackedTable, out=N
         out = torch.empty((B, D), dtype=torch.int32, device=packed.data.device)
     need = eval_workspace_bytes(B, log_n, packed.row_count, D)
     ws = workspace if workspace is not None else _workspace(need, packed.data.device)
-    _check(lib().dpf_eval_batch_wire_packed(keys_wire_dev.data_ptr(), B, log_n, packed.data.data_ptr(),
+    _check(lib().dpf_eval_batch_wire_packed(keys_wire_dev.data_ptr(), B, log_n, prf, packed.data.data_ptr(),
                                             packed.row_begin, packed.row_count, D, out.data_ptr(), ws.data_ptr(),
                                             ws.numel() * ws.element_size(), _stream_ptr(stream)),
            "dpf_eval_batch_wire_packed")

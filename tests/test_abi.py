@@ -51,6 +51,17 @@ def test_gen_equals_oracle_gen(lib, oracle):
             assert dpfpir.key_serialize(k1) == oracle.key_to_wire(o1)
 
 
+def test_gen_aes_equals_oracle_gen(lib, oracle):
+    r = np.random.default_rng(9)
+    for n in (1, 5, 14, 20):
+        alpha = int(r.integers(0, 1 << n))
+        seed = bytes(r.integers(0, 256, 32, dtype=np.uint8))
+        k0, k1 = dpfpir.gen(n, alpha, 12345, seed, prf=dpfpir.DPF_PRF_AES128)
+        o0, o1 = oracle.gen(n, alpha, 12345, seed, prf=oracle.PRF_AES128)
+        assert dpfpir.key_serialize(k0) == oracle.key_to_wire(o0)
+        assert dpfpir.key_serialize(k1) == oracle.key_to_wire(o1)
+
+
 def test_gen_keys_satisfy_contract_under_oracle_eval(lib, oracle):
     for alpha in (0, 5, 63):
         k0, k1 = dpfpir.gen(6, alpha, 1, bytes(32))
@@ -96,7 +107,7 @@ def test_gen_errors(lib):
     with pytest.raises(dpfpir.DpfError):
         dpfpir.gen(0, 0)
     with pytest.raises(dpfpir.DpfError) as e:
-        dpfpir.gen(4, 1, prf=dpfpir.DPF_PRF_AES128)
+        dpfpir.gen(4, 1, prf=7)
     assert e.value.code == dpfpir.DPF_EUNSUPPORTED
 
 

@@ -218,3 +218,50 @@ def test_packed_tc_c3_sampled(dp, oracle):
     want = oracle.answer_batch(ok, T, threads=2)
     for i, b in enumerate(sample):
         np.testing.assert_array_equal(sh0[b], want[i])
+
+
+# ---------------------------------------------------------------- AES-128 PRF (row f1)
+
+def make_aes_keys(dp, oracle, n, alphas, seed):
+    keys, okeys = [], []
+    for i, (a, s) in enumerate(zip(alphas, synth.gen_seeds(len(alphas), seed))):
+        k = dp.gen(n, int(a), 1, s, prf=dp.DPF_PRF_AES128)[i % 2]
+        keys.append(k)
+        okeys.append(oracle.key_from_wire(dp.key_serialize(k)))
+    return keys, okeys
+
+
+def test_aes_leaves_match_oracle(dp, oracle):
+    for n, B in ((1, 2), (4, 3), (10, 2)):
+        keys, okeys = make_aes_keys(dp, oracle, n, synth.alphas(B, 1 << n, n), 50 + n)
+        got = dp.as_u32(dp.eval_leaves(keys))
+        for b in range(B):
+            np.testing.assert_array_equal(got[b], oracle.eval_full(okeys[b]))
+
+
+@pytest.mark.parametrize("n,N,D,B,packed", [
+    (10, 1000, 16, 3, False), (12, 4096, 64, 37, False), (13, 5000, 32, 64, False), (9, 512, 4, 1, False),
+    (12, 4096, 256, 40, True), (11, 2048, 128, 64, True), (12, 3000, 384, 33, True),
+])
+def test_aes_parity(dp, oracle, n, N, D, B, packed):
+    T = synth.table(N, D, 600 + n)
+    keys, okeys = make_aes_keys(dp, oracle, n, synth.alphas(B, N, 600 + n), 600 + n)
+    Td = to_dev(T)
+    got = dp.as_u32(dp.eval_batch_packed(keys, dp.table_pack(Td)) if packed else dp.eval_batch(keys, Td))
+    np.testing.assert_array_equal(got, oracle.answer_batch(okeys, T, threads=8))
+
+
+def test_aes_wire_shard_and_reconstruct(dp, oracle):
+    n, N, D, B = 14, 12000, 64, 24
+    T = synth.table(N, D, 77)
+    al = synth.alphas(B, N, 77)
+    pairs = [dp.gen(n, int(a), 1, s, prf=dp.DPF_PRF_AES128) for a, s in zip(al, synth.gen_seeds(B, 77))]
+    Td = to_dev(T)
+    k0 = [p[0] for p in pairs]
+    wire = torch.from_numpy(dp.keys_to_wire(k0)).cuda()
+    sh0 = dp.as_u32(dp.eval_batch_wire(wire, n, Td, prf=dp.DPF_PRF_AES128))
+    np.testing.assert_array_equal(sh0, dp.as_u32(dp.eval_batch(k0, Td)))
+    np.testing.assert_array_equal(dp.keys_to_wire(k0), wire.cpu().numpy())  # caller's device keys untouched
+    part = dp.as_u32(dp.eval_batch_shard([p[1] for p in pairs], to_dev(T[5000:]), 5000)) + \
+        dp.as_u32(dp.eval_batch_shard([p[1] for p in pairs], to_dev(T[:5000]), 0))
+    np.testing.assert_array_equal(dp.reconstruct(sh0, part), T[al.astype(np.int64)])
