@@ -40,7 +40,12 @@ sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
 
-ALU_OPS_PER_BLOCK = 640  # XOR + rotate per ChaCha20 block (80 quarter rounds x 8), DESIGN.md "Roofline"
+# ALU-pipe ops per tree node: ChaCha20 = 320 XOR + 320
+# rotate per block (80 quarter rounds; the adds run on the FMA pipe).  AES-128
+# (bitsliced, table-free) = the compiled ALU instructions of one node's two
+# encryptions + key schedule in this formulation (9 x 411 + 336 + 40 setup;
+# Boyar-Peralta S-box = 95 LOP3): a better circuit would lower it.
+ALU_OPS_PER_BLOCK = {"chacha20": 640, "aes128": 4075}
 METRIC = "DPF-PIR queries/sec"
 UNIT = "queries/s"
 
@@ -318,8 +323,9 @@ def main():
     fused_blocks = w.B * (rows >> m) * ((1 << m) - 1)  # algorithmic blocks per launch (no padding)
     kern_avg_ms = sum(kernel_ms) / len(kernel_ms)
     alu_peak = 148 * 64 * pk["sm_max_mhz"] * 1e6  # ALU-pipe lane-ops/s
-    achieved = ALU_OPS_PER_BLOCK * fused_blocks / (kern_avg_ms * 1e-3)
-    qps_roof = alu_peak / (ALU_OPS_PER_BLOCK * (rows - 1 + g))
+    ops_per_block = ALU_OPS_PER_BLOCK[args.prf]
+    achieved = ops_per_block * fused_blocks / (kern_avg_ms * 1e-3)
+    qps_roof = alu_peak / (ops_per_block * (rows - 1 + g))
     hbm_qps_roof = G * pk["hbm_gbs"] * 1e9 * w.B / (4.0 * w.N * w.D)
     traffic = _ncu_traffic(w.name)
     roofline = {
@@ -327,7 +333,9 @@ def main():
         "frac": achieved / alu_peak, "traffic": traffic,
         "kernel": "fused_eval_tc_kernel" if use_packed else "fused_eval_kernel", "kernel_ms": kern_avg_ms,
         "kernel_share_of_step": kern_avg_ms / ms_per_step,
-        "ops": "640 ALU-pipe int32 ops (LOP3 xor + SHF rotate) per ChaCha20 block x %d blocks per launch" % fused_blocks,
+        "ops": ("640 ALU-pipe int32 ops (LOP3 xor + SHF rotate) per ChaCha20 block" if args.prf == "chacha20" else
+                "4075 ALU-pipe ops per bitsliced AES-128 node (2 blocks + key schedule)") +
+               " x %d blocks per launch" % fused_blocks,
         "peak_basis": "148 SMs x 64 ALU lanes/clk x %.0f MHz (%s)" % (pk["sm_max_mhz"], pk["source"]),
         "qps_at_prf_roofline": qps_roof, "frac_qps": value / qps_roof, "qps_at_hbm_roofline": hbm_qps_roof,
     }
@@ -351,6 +359,7 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": w.name + ": " + w.note, "log_n": w.log_n, "N": w.N, "D": w.D, "B": w.B,
+                       "prf": args.prf,
                        "parallelism": "row-shard x%d + NCCL reduce" % G if G > 1 else "1 GPU",
                        "keys": "device-resident wire keys (dpf_eval_batch_wire%s)" % ("_packed" if use_packed else ""),
                        "table": "limb-packed (dpf_table_pack, tcgen05 kind::i8 contraction)" if use_packed

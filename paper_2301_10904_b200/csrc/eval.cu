@@ -192,22 +192,46 @@ __global__ void copy_roots_kernel(const uint8_t *__restrict__ keys, uint32_t kst
 }
 
 // ----------------------------------------------------------------- a3..a6: fused
-struct FusedParams {
-  const uint8_t *keys;
+// One (key batch, table shard) evaluation.  A launch runs one group (the
+// dpf_eval_batch* entry points) or many (dpf_eval_grouped: e.g. the 26
+// tables x hot/full splits of the co-design workload) sharing the kernel
+// configuration below; work items are numbered group after group.
+struct GroupDesc {
+  const uint8_t *keys;    // device keys (wire layout; AES: bitsliced copy)
   const uint4 *frontier;  // [B][cap], node i at depth f (absolute lo_f + i)
-  const uint32_t *T;      // shard base: row r0
+  const uint32_t *T;      // shard base: row r0 (tcgen05 path: the limb-packed table)
   uint32_t *shares;       // [B][D]
   uint64_t cap;           // frontier stride per key
   uint64_t F;             // frontier nodes per key
   uint64_t lo_f;          // absolute index of frontier node 0
   uint64_t r0, r1;        // valid absolute rows
-  uint32_t kstride, B, n, m, D;
+  uint64_t r0a, packed_rows;  // tcgen05 path: 8-row-aligned packed range
+  uint32_t kstride, B, n, m;
+  uint32_t nwin, n_ktiles;  // windows per item = 2^(m-1) / W; key tiles
+  uint32_t item_base;       // first work item of this group
+  uint32_t key_base;        // first key of this group (grouped top BFS)
+};
+
+struct FusedParams {
+  GroupDesc g0;              // the group when n_groups == 1
+  const GroupDesc *groups;   // device array when n_groups > 1 (sorted by item_base)
+  uint32_t n_groups, n_items, D;
   uint32_t Kt, Ft, tasks;  // tasks = Kt * Ft <= 32 * NP (lanes >= tasks idle)
   uint32_t W;              // leaf pairs per producer thread per window
-  uint32_t n_ktiles, n_items, nwin;  // windows per item = 2^(m-1) / W
   uint32_t CG, KG;         // consumer col groups / key groups
   uint32_t y_stage_words, t_stage_words;
 };
+
+__device__ __forceinline__ GroupDesc group_of(const FusedParams &p, uint32_t item) {
+  if (p.n_groups <= 1) return p.g0;
+  uint32_t lo = 0, hi = p.n_groups - 1;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (__ldg(&p.groups[mid].item_base) <= item) lo = mid;
+    else hi = mid - 1;
+  }
+  return p.groups[lo];
+}
 
 template <int NP, int NC>
 struct Smem {
@@ -256,8 +280,8 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
   constexpr uint32_t kFullThreads = 32 * (NP + NC), kEmptyThreads = 32 * (NP + NC + 1);
   // windows this CTA will run (consumers skip the EMPTY arrive for the last
   // two, which no producer will ever wait for)
-  const uint32_t my_items = blockIdx.x < p.n_items ? (p.n_items - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  const uint32_t total_w = my_items * p.nwin;
+  uint32_t total_w = 0;
+  for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) total_w += group_of(p, item).nwin;
   uint32_t *ybuf = reinterpret_cast<uint32_t *>(smem + 128);
   uint32_t *tbuf = ybuf + 2 * p.y_stage_words;
   uint4 *stack = reinterpret_cast<uint4 *>(tbuf + 2 * p.t_stage_words);
@@ -272,7 +296,6 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
   __syncthreads();
 
   const uint32_t nslots = p.Ft * 2 * p.W;
-  const uint32_t nq = 1u << (p.m - 1);
 
   if (warp < NP) {
     // ------------------------------------------------------------ producers
@@ -281,37 +304,40 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
     const uint32_t kl = lane_on ? tix % p.Kt : 0, nl = lane_on ? tix / p.Kt : 0;
     uint32_t wseq = 0;
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
-      const uint32_t kt = item % p.n_ktiles, ng = item / p.n_ktiles;
+      const GroupDesc g = group_of(p, item);
+      const uint32_t li = item - g.item_base;
+      const uint32_t kt = li % g.n_ktiles, ng = li / g.n_ktiles;
+      const uint32_t nq = 1u << (g.m - 1);
       const uint32_t b = kt * p.Kt + kl;
       const uint64_t node = uint64_t(ng) * p.Ft + nl;
-      const bool valid = lane_on && b < p.B && node < p.F;
-      const uint8_t *key = p.keys + uint64_t(valid ? b : 0) * p.kstride;
+      const bool valid = lane_on && b < g.B && node < g.F;
+      const uint8_t *key = g.keys + uint64_t(valid ? b : 0) * g.kstride;
       const uint32_t cw_out = key_cw_out(key);
-      uint4 cur = valid ? p.frontier[uint64_t(b) * p.cap + node] : make_uint4(0, 0, 0, 0);
-      const uint64_t row_base = (p.lo_f + node) << p.m;
-      const bool inside = valid && row_base >= p.r0 && row_base + (1ull << p.m) <= p.r1;
+      uint4 cur = valid ? g.frontier[uint64_t(b) * g.cap + node] : make_uint4(0, 0, 0, 0);
+      const uint64_t row_base = (g.lo_f + node) << g.m;
+      const bool inside = valid && row_base >= g.r0 && row_base + (1ull << g.m) <= g.r1;
       uint32_t dep = 0;
-      for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
+      for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
         const uint32_t stage = wseq & 1, use = wseq >> 1;
         if (use > 0) named_sync(3 + stage, kEmptyThreads);
         uint32_t *yb = ybuf + stage * p.y_stage_words;
         for (uint32_t qi = 0; qi < p.W; ++qi) {
           const uint32_t q = win * p.W + qi;
           // descend (warp-uniform: every thread shares the schedule)
-          while (dep + 1 < p.m) {
+          while (dep + 1 < g.m) {
             uint4 c0, c1;
-            node_children<Prf>(cur, key_cw(key, p.n - p.m + dep + 1), c0, c1);
+            node_children<Prf>(cur, key_cw(key, g.n - g.m + dep + 1), c0, c1);
             stack[(dep + 1) * (32 * NP) + tix] = c1;
             cur = c0;
             ++dep;
           }
           uint4 l0, l1;
-          node_children<Prf>(cur, key_cw(key, p.n), l0, l1);
+          node_children<Prf>(cur, key_cw(key, g.n), l0, l1);
           uint32_t y0 = leaf_value<Prf>(l0, cw_out), y1 = leaf_value<Prf>(l1, cw_out);
           if (!inside) {
             const uint64_t row = row_base + 2 * q;
-            y0 = (valid && row >= p.r0 && row < p.r1) ? y0 : 0u;
-            y1 = (valid && row + 1 >= p.r0 && row + 1 < p.r1) ? y1 : 0u;
+            y0 = (valid && row >= g.r0 && row < g.r1) ? y0 : 0u;
+            y1 = (valid && row + 1 >= g.r0 && row + 1 < g.r1) ? y1 : 0u;
           }
           if (lane_on) {
             const uint32_t slot = nl * 2 * p.W + 2 * qi;
@@ -319,7 +345,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
             yb[(slot + 1) * p.Kt + kl] = y1;
           }
           if (q + 1 < nq) {  // pop: the right sibling at depth m-1-ctz(q+1)
-            const uint32_t k = p.m - 1 - (__ffs(q + 1) - 1);
+            const uint32_t k = g.m - 1 - (__ffs(q + 1) - 1);
             cur = stack[k * (32 * NP) + tix];
             dep = k;
           }
@@ -341,8 +367,9 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
       for (int c = 0; c < CPL; ++c) acc[k][c] = 0;
     uint32_t wseq = 0;
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
-      const uint32_t kt = item % p.n_ktiles;
-      for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
+      const GroupDesc g = group_of(p, item);
+      const uint32_t kt = (item - g.item_base) % g.n_ktiles;
+      for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
         const uint32_t stage = wseq & 1, use = wseq >> 1;
         named_sync(1 + stage, kFullThreads);
         mbar_wait(&tfull[stage], use & 1);
@@ -356,12 +383,12 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
 #pragma unroll
         for (int k = 0; k < KPW; ++k) {
           const uint32_t b = kt * p.Kt + key0 + k;
-          if (key0 + k < p.Kt && b < p.B) {
-            const uint32_t neg = key_party(p.keys + uint64_t(b) * p.kstride);
+          if (key0 + k < p.Kt && b < g.B) {
+            const uint32_t neg = key_party(g.keys + uint64_t(b) * g.kstride);
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
               const uint32_t col = colbase + 32 * c;
-              if (col < p.D) red_add_u32(p.shares + uint64_t(b) * p.D + col, neg ? 0u - acc[k][c] : acc[k][c]);
+              if (col < p.D) red_add_u32(g.shares + uint64_t(b) * p.D + col, neg ? 0u - acc[k][c] : acc[k][c]);
             }
           }
 #pragma unroll
@@ -375,17 +402,18 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
     const uint64_t seg_rows = 2 * p.W;
     const uint32_t row_bytes = p.D * 4;
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
-      const uint32_t ng = item / p.n_ktiles;
-      for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
+      const GroupDesc g = group_of(p, item);
+      const uint32_t ng = (item - g.item_base) / g.n_ktiles;
+      for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
         const uint32_t stage = wseq & 1, use = wseq >> 1;
         if (use > 0) named_sync(3 + stage, kEmptyThreads);
         uint32_t *tb = tbuf + stage * p.t_stage_words;
         uint32_t my_bytes = 0;
         for (uint32_t nl = lane; nl < p.Ft; nl += 32) {
           const uint64_t node = uint64_t(ng) * p.Ft + nl;
-          if (node >= p.F) continue;
-          const uint64_t s0 = ((p.lo_f + node) << p.m) + seg_rows * win;
-          const uint64_t a = s0 > p.r0 ? s0 : p.r0, e = (s0 + seg_rows) < p.r1 ? (s0 + seg_rows) : p.r1;
+          if (node >= g.F) continue;
+          const uint64_t s0 = ((g.lo_f + node) << g.m) + seg_rows * win;
+          const uint64_t a = s0 > g.r0 ? s0 : g.r0, e = (s0 + seg_rows) < g.r1 ? (s0 + seg_rows) : g.r1;
           if (a < e) my_bytes += uint32_t(e - a) * row_bytes;
         }
         const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, my_bytes);
@@ -393,11 +421,11 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
         __syncwarp();
         for (uint32_t nl = lane; nl < p.Ft; nl += 32) {
           const uint64_t node = uint64_t(ng) * p.Ft + nl;
-          if (node >= p.F) continue;
-          const uint64_t s0 = ((p.lo_f + node) << p.m) + seg_rows * win;
-          const uint64_t a = s0 > p.r0 ? s0 : p.r0, e = (s0 + seg_rows) < p.r1 ? (s0 + seg_rows) : p.r1;
+          if (node >= g.F) continue;
+          const uint64_t s0 = ((g.lo_f + node) << g.m) + seg_rows * win;
+          const uint64_t a = s0 > g.r0 ? s0 : g.r0, e = (s0 + seg_rows) < g.r1 ? (s0 + seg_rows) : g.r1;
           if (a < e)
-            bulk_g2s(tb + (uint64_t(nl) * seg_rows + (a - s0)) * p.D, p.T + (a - p.r0) * p.D,
+            bulk_g2s(tb + (uint64_t(nl) * seg_rows + (a - s0)) * p.D, g.T + (a - g.r0) * p.D,
                      uint32_t(e - a) * row_bytes, &tfull[stage]);
         }
       }
@@ -750,27 +778,35 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
   }
   const bool timed = g_timer.on && 2 * g_timer.used + 1 < g_timer.ev.size();
   dev::FusedParams p;
-  p.keys = keys_dev;
-  p.frontier = ws.front[0];
-  p.T = table;
-  p.shares = out;
-  p.cap = pl.cap;
-  p.F = pl.F;
-  p.lo_f = pl.lo_f;
-  p.r0 = pl.r0;
-  p.r1 = pl.r1;
-  p.kstride = kstride;
-  p.B = B;
-  p.n = pl.n;
-  p.m = pl.m;
+  std::memset(&p, 0, sizeof p);
+  dev::GroupDesc &g = p.g0;
+  g.keys = keys_dev;
+  g.frontier = ws.front[0];
+  g.T = table;
+  g.shares = out;
+  g.cap = pl.cap;
+  g.F = pl.F;
+  g.lo_f = pl.lo_f;
+  g.r0 = pl.r0;
+  g.r1 = pl.r1;
+  g.r0a = pl.r0a;
+  g.packed_rows = pl.packed_rows;
+  g.kstride = kstride;
+  g.B = B;
+  g.n = pl.n;
+  g.m = pl.m;
+  g.nwin = pl.nwin;
+  g.n_ktiles = pl.n_ktiles;
+  g.item_base = 0;
+  g.key_base = 0;
+  p.groups = nullptr;
+  p.n_groups = 1;
+  p.n_items = pl.n_items;
   p.D = D;
   p.Kt = pl.Kt;
   p.Ft = pl.Ft;
   p.tasks = pl.tasks;
   p.W = pl.W;
-  p.n_ktiles = pl.n_ktiles;
-  p.n_items = pl.n_items;
-  p.nwin = pl.nwin;
   p.CG = pl.CG;
   p.KG = pl.KG;
   p.y_stage_words = pl.y_stage_words;
@@ -778,9 +814,6 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
   if (pl.tc) {
     dev::TcParams tp;
     tp.f = p;
-    tp.packed = reinterpret_cast<const uint8_t *>(table);
-    tp.r0a = pl.r0a;
-    tp.packed_rows = pl.packed_rows;
     tp.y_stage_bytes = pl.y_stage_bytes;
     tp.tmem_cols = pl.tmem_cols;
     auto fn = pl.prf == DPF_PRF_AES128 ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4>

@@ -28,9 +28,7 @@ namespace dpfpir {
 namespace dev {
 
 struct TcParams {
-  FusedParams f;
-  const uint8_t *packed;  // limb-packed rows [r0a, r0a + packed_rows)
-  uint64_t r0a, packed_rows;
+  FusedParams f;  // groups: T = the limb-packed rows [r0a, r0a + packed_rows)
   uint32_t y_stage_bytes, tmem_cols;
 };
 
@@ -151,43 +149,45 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
     // single-site "one block per iteration" loop and a 4-leaf "quad" form.)
     const uint32_t tix = warp * 32 + lane;
     const uint32_t kl = tix % p.Kt, nl = tix / p.Kt;
-    const uint32_t nq = 1u << (p.m - 1);
     uint32_t wseq = 0;
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
-      const uint32_t kt = item % p.n_ktiles, ng = item / p.n_ktiles;
+      const GroupDesc g = group_of(p, item);
+      const uint32_t li = item - g.item_base;
+      const uint32_t kt = li % g.n_ktiles, ng = li / g.n_ktiles;
+      const uint32_t nq = 1u << (g.m - 1);
       const uint32_t b = kt * p.Kt + kl;
       const uint64_t node = uint64_t(ng) * p.Ft + nl;
-      const bool valid = b < p.B && node < p.F;
-      const uint8_t *key = p.keys + uint64_t(valid ? b : 0) * p.kstride;
+      const bool valid = b < g.B && node < g.F;
+      const uint8_t *key = g.keys + uint64_t(valid ? b : 0) * g.kstride;
       const uint32_t cw_out = key_cw_out(key);
-      uint4 cur = valid ? p.frontier[uint64_t(b) * p.cap + node] : make_uint4(0, 0, 0, 0);
-      const uint64_t row_base = (p.lo_f + node) << p.m;
-      const bool inside = valid && row_base >= p.r0 && row_base + (1ull << p.m) <= p.r1;
+      uint4 cur = valid ? g.frontier[uint64_t(b) * g.cap + node] : make_uint4(0, 0, 0, 0);
+      const uint64_t row_base = (g.lo_f + node) << g.m;
+      const bool inside = valid && row_base >= g.r0 && row_base + (1ull << g.m) <= g.r1;
       uint32_t dep = 0;
-      for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
+      for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
         const uint32_t ys = wseq % NSY, yuse = wseq / NSY;
         if (yuse > 0) mbar_wait(&yempty[ys], (yuse - 1) & 1);
         uint8_t *yb = ybuf + ys * tp.y_stage_bytes;
         for (uint32_t qi = 0; qi < p.W; ++qi) {
           const uint32_t q = win * p.W + qi;
-          while (dep + 1 < p.m) {
+          while (dep + 1 < g.m) {
             uint4 c0, c1;
-            node_children<Prf>(cur, key_cw(key, p.n - p.m + dep + 1), c0, c1);
+            node_children<Prf>(cur, key_cw(key, g.n - g.m + dep + 1), c0, c1);
             stack[(dep + 1) * (32 * NP) + tix] = c1;
             cur = c0;
             ++dep;
           }
           uint4 l0, l1;
-          node_children<Prf>(cur, key_cw(key, p.n), l0, l1);
+          node_children<Prf>(cur, key_cw(key, g.n), l0, l1);
           uint32_t y0 = leaf_value<Prf>(l0, cw_out), y1 = leaf_value<Prf>(l1, cw_out);
           if (!inside) {
             const uint64_t row = row_base + 2 * q;
-            y0 = (valid && row >= p.r0 && row < p.r1) ? y0 : 0u;
-            y1 = (valid && row + 1 >= p.r0 && row + 1 < p.r1) ? y1 : 0u;
+            y0 = (valid && row >= g.r0 && row < g.r1) ? y0 : 0u;
+            y1 = (valid && row + 1 >= g.r0 && row + 1 < g.r1) ? y1 : 0u;
           }
           put_leaf_pair(yb, ybplane, p.Kt, kl, nl * W2 + 2 * qi, y0, y1);
           if (q + 1 < nq) {  // pop the right sibling at depth m-1-ctz(q+1)
-            const uint32_t k = p.m - 1 - (__ffs(q + 1) - 1);
+            const uint32_t k = g.m - 1 - (__ffs(q + 1) - 1);
             cur = stack[k * (32 * NP) + tix];
             dep = k;
           }
@@ -205,10 +205,11 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
     const uint32_t ybase = smem_u32(ybuf), tbase = smem_u32(tbuf);
     uint32_t wseq = 0, tseq = 0, it = 0;
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
-      const uint32_t kt = item % p.n_ktiles;
+      const GroupDesc g = group_of(p, item);
+      const uint32_t kt = (item - g.item_base) % g.n_ktiles;
       if (q == 0) {
         if (it > 0) mbar_wait(accempty, (it - 1) & 1);  // epilogue drained the accumulators
-        for (uint32_t win = 0; win < p.nwin; ++win, ++wseq) {
+        for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
           const uint32_t ys = wseq % NSY;
           named_sync(1 + ys, 32 * (NP + 1));
           tc_fence_after();
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
           }
           if (lane == 0) {
             umma_commit(&yempty[ys]);                     // y stage reusable
-            if (win + 1 == p.nwin) umma_commit(accfull);  // item's accumulators complete
+            if (win + 1 == g.nwin) umma_commit(accfull);  // item's accumulators complete
           }
           __syncwarp();
         }
@@ -264,10 +265,10 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             const uint32_t bkey = kt * p.Kt + h * 16 + j;
-            if (bkey < p.B && d < D) {
+            if (bkey < g.B && d < D) {
               const uint32_t val = v[j] + (x[j] << 16) + (z[j] << 24);  // A0 + 2^8 A1 + 2^16 A2 + 2^24 A3
-              const uint32_t neg = key_party(p.keys + uint64_t(bkey) * p.kstride);
-              red_add_u32(p.shares + uint64_t(bkey) * D + d, neg ? 0u - val : val);
+              const uint32_t neg = key_party(g.keys + uint64_t(bkey) * g.kstride);
+              red_add_u32(g.shares + uint64_t(bkey) * D + d, neg ? 0u - val : val);
             }
           }
         }
@@ -280,16 +281,18 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
     // ------------------------------------------------------------ T loader
     // Per (window, 32-leaf chunk, d-tile): 4 nodes x one 4 KB packed block.
     uint32_t tseq = 0;
-    const uint64_t pend = tp.r0a + tp.packed_rows;
     const uint32_t n_dt = D / 128, n_cc = Kw / 32;
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
-      const uint32_t ng = item / p.n_ktiles;
-      for (uint32_t win = 0; win < p.nwin; ++win) {
+      const GroupDesc g = group_of(p, item);
+      const uint64_t pend = g.r0a + g.packed_rows;
+      const uint8_t *packed = reinterpret_cast<const uint8_t *>(g.T);
+      const uint32_t ng = (item - g.item_base) / g.n_ktiles;
+      for (uint32_t win = 0; win < g.nwin; ++win) {
         for (uint32_t cc = 0; cc < n_cc; ++cc) {
           // lane j < 4: node 4cc + j, rows [s0, s0 + 8) (one packed block)
           const uint64_t node = uint64_t(ng) * p.Ft + 4 * cc + (lane & 3);
-          const uint64_t s0 = ((p.lo_f + node) << p.m) + uint64_t(W2) * win;
-          const bool ok = lane < 4 && node < p.F && s0 >= tp.r0a && s0 < pend;
+          const uint64_t s0 = ((g.lo_f + node) << g.m) + uint64_t(W2) * win;
+          const bool ok = lane < 4 && node < g.F && s0 >= g.r0a && s0 < pend;
           const uint32_t total = __popc(__ballot_sync(0xFFFFFFFFu, ok)) * 4096u;
           for (uint32_t dt = 0; dt < n_dt; ++dt, ++tseq) {
             const uint32_t ts = tseq % NST, tuse = tseq / NST;
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
             __syncwarp();
             if (ok)
               bulk_g2s(tbuf + ts * kTcTStageBytes + lane * 4096u,
-                       tp.packed + ((s0 - tp.r0a) >> 3) * (32ull * D) + dt * 4096ull, 4096u, &tfull[ts]);
+                       packed + ((s0 - g.r0a) >> 3) * (32ull * D) + dt * 4096ull, 4096u, &tfull[ts]);
           }
         }
       }
