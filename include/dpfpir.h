@@ -189,6 +189,34 @@ int dpf_eval_batch_wire_packed(const uint8_t *keys_wire_dev, uint32_t B, uint32_
                                uint64_t row_begin, uint64_t row_count, uint32_t D, uint32_t *partial_shares,
                                void *workspace, size_t workspace_bytes, void *stream);
 
+/* ---- grouped evaluation: many (key batch, table) pairs in one launch ----
+ * For workloads of many small tables, e.g. the co-design setting of P:645-659
+ * (each inference queries a small hot table and the full table of each of
+ * several embedding tables, with a fixed number of keys per table).  All
+ * groups share D and the PRF; tables are row-major (IMAD contraction).
+ * Group g computes exactly what dpf_eval_batch_wire would:
+ *   shares[b][d] = sum_{row_begin <= j < row_begin+row_count}
+ *                    Eval(keys[b], j) * table[j - row_begin][d]  (mod 2^32) */
+typedef struct dpf_eval_group {
+  const uint8_t *keys_wire; /* DEVICE: B wire-format keys (stride dpf_key_wire_size(log_n)), 16-B aligned */
+  uint32_t B;               /* keys in this group, >= 1 */
+  uint32_t log_n;           /* depth of these keys' trees */
+  const uint32_t *table;    /* DEVICE: row_count x D uint32, row-major, 16-B aligned */
+  uint64_t row_begin, row_count;
+  uint32_t *shares;         /* DEVICE: B x D, overwritten */
+} dpf_eval_group;
+
+/* Workspace bytes for dpf_eval_grouped (0 on invalid arguments). */
+size_t dpf_eval_grouped_workspace_bytes(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D,
+                                        uint32_t prf);
+
+/* Evaluate n_groups groups (host array of descriptors; the device buffers
+ * they point to stay caller-owned) with one zeroing, one top-BFS and one
+ * fused launch (+ one key-bitslicing launch per group for AES).  Asynchronous
+ * on `stream`.  Errors: DPF_EINVAL, DPF_ENOMEM, DPF_EUNSUPPORTED, DPF_ECUDA. */
+int dpf_eval_grouped(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D, uint32_t prf, void *workspace,
+                     size_t workspace_bytes, void *stream);
+
 /* End-to-end serving call: as dpf_eval_batch_shard, but shares_host is a HOST
  * buffer (pinned for best speed) that receives the B x D answers; the call
  * synchronises `stream` before returning.  The table stays device-resident

@@ -210,6 +210,7 @@ struct GroupDesc {
   uint32_t nwin, n_ktiles;  // windows per item = 2^(m-1) / W; key tiles
   uint32_t item_base;       // first work item of this group
   uint32_t key_base;        // first key of this group (grouped top BFS)
+  uint4 *frontier_alt;      // grouped top BFS ping-pong buffer (f > kTopSmemLevels)
 };
 
 struct FusedParams {
@@ -439,6 +440,78 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
 namespace dpfpir {
 namespace dev {
 
+// ---------------------------------------------------------- grouped launches
+// Zero every group's answer buffer (one launch instead of one memset per group).
+__global__ void zero_shares_grouped_kernel(const GroupDesc *__restrict__ groups, uint32_t n_groups, uint32_t D) {
+  for (uint32_t gi = blockIdx.y; gi < n_groups; gi += gridDim.y) {
+    const GroupDesc &g = groups[gi];
+    const uint64_t words = uint64_t(g.B) * D;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < words; i += uint64_t(gridDim.x) * blockDim.x)
+      g.shares[i] = 0;
+  }
+}
+
+// a2 for all groups in one launch: one CTA per (group, key) expands levels
+// 1..f_g (f_g <= kTopSmemLevels) in shared memory, writes the frontier.
+template <class Prf>
+__global__ void __launch_bounds__(256) expand_top_grouped_kernel(const GroupDesc *__restrict__ groups,
+                                                                 uint32_t n_groups) {
+  __shared__ uint4 buf[2][1u << kTopSmemLevels];
+  uint32_t lo = 0, hi = n_groups - 1;  // group of this CTA's key
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if (groups[mid].key_base <= blockIdx.x) lo = mid;
+    else hi = mid - 1;
+  }
+  const GroupDesc &g = groups[lo];
+  const uint32_t b = blockIdx.x - g.key_base;
+  const uint8_t *key = g.keys + uint64_t(b) * g.kstride;
+  const uint32_t n = g.n, f = g.n - g.m, a = f < kTopSmemLevels ? f : kTopSmemLevels;
+  const uint64_t r0 = g.r0, r1 = g.r1;
+  // level a lands where the remaining levels' ping-pong ends on `frontier`
+  uint4 *out = (((f - a) & 1) ? g.frontier_alt : const_cast<uint4 *>(g.frontier)) + uint64_t(b) * g.cap;
+  if (threadIdx.x == 0) buf[0][0] = key_root(key);
+  __syncthreads();
+  for (uint32_t k = 1; k <= a; ++k) {
+    const uint64_t plo = r0 >> (n - (k - 1)), phi = (r1 - 1) >> (n - (k - 1));
+    const uint64_t lo_k = r0 >> (n - k), hi_k = (r1 - 1) >> (n - k);
+    const uint4 *in = buf[(k - 1) & 1];
+    uint4 *o = buf[k & 1];
+    for (uint64_t p = plo + threadIdx.x; p <= phi; p += blockDim.x) {
+      uint4 c0, c1;
+      node_children<Prf>(in[p - plo], key_cw(key, k), c0, c1);
+      if (2 * p >= lo_k) o[2 * p - lo_k] = c0;
+      if (2 * p + 1 <= hi_k) o[2 * p + 1 - lo_k] = c1;
+    }
+    __syncthreads();
+  }
+  const uint64_t cnt = ((r1 - 1) >> (n - a)) - (r0 >> (n - a)) + 1;
+  for (uint64_t i = threadIdx.x; i < cnt; i += blockDim.x) out[i] = buf[a & 1][i];
+}
+
+// Level k > kTopSmemLevels of every group whose frontier is deeper: grid.y =
+// group; thread per (key, parent), both children by one block.
+template <class Prf>
+__global__ void expand_level_grouped_kernel(const GroupDesc *__restrict__ groups, uint32_t k) {
+  const GroupDesc &g = groups[blockIdx.y];
+  const uint32_t n = g.n, f = g.n - g.m;
+  if (k > f) return;
+  const uint64_t plo = g.r0 >> (n - (k - 1)), phi = (g.r1 - 1) >> (n - (k - 1));
+  const uint64_t lo = g.r0 >> (n - k), hi = (g.r1 - 1) >> (n - k);
+  const uint64_t np = phi - plo + 1, total = np * g.B;
+  const uint4 *in = ((f - k + 1) & 1) ? g.frontier_alt : g.frontier;
+  uint4 *out = ((f - k) & 1) ? g.frontier_alt : const_cast<uint4 *>(g.frontier);
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total; i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t b = uint32_t(i / np);
+    const uint64_t p = plo + (i % np);
+    const uint8_t *key = g.keys + uint64_t(b) * g.kstride;
+    uint4 c0, c1;
+    node_children<Prf>(in[uint64_t(b) * g.cap + (p - plo)], key_cw(key, k), c0, c1);
+    if (2 * p >= lo && 2 * p <= hi) out[uint64_t(b) * g.cap + (2 * p - lo)] = c0;
+    if (2 * p + 1 >= lo && 2 * p + 1 <= hi) out[uint64_t(b) * g.cap + (2 * p + 1 - lo)] = c1;
+  }
+}
+
 // Test/debug leaf dump (branch-parallel: n blocks per leaf).
 template <class Prf>
 __global__ void eval_leaves_kernel(const uint8_t *__restrict__ keys, uint32_t kstride, uint32_t B, uint32_t n,
@@ -468,6 +541,7 @@ namespace {
 constexpr int kNC = 4;  // consumer warps
 constexpr size_t kAlign = 256;
 constexpr uint32_t kMaxTStageBytes = 64 * 1024;
+constexpr uint32_t kTopSmemLevelsHost = 10;  // == dev::kTopSmemLevels
 constexpr uint32_t kMaxTStageBytesW1 = 80 * 1024;  // leaves room for a 64 KB DFS stack
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
@@ -1084,5 +1158,247 @@ extern "C" int dpf_kernel_timer_read(float *ms, uint32_t capacity, uint32_t *cou
 extern "C" int dpf_last_eval_stats(dpf_eval_stats *out) {
   if (!out) return DPF_EINVAL;
   *out = g_stats;
+  return DPF_OK;
+}
+
+// =================================================================== grouped
+namespace dpfpir {
+namespace {
+
+struct GroupedPlan {
+  Plan cfg;  // shared kernel configuration (Kt, Ft, W, tiles, SMEM)
+  std::vector<dev::GroupDesc> desc;
+  std::vector<uint32_t> order;  // launch order (largest subtrees first)
+  size_t front_bytes, keys_bytes, desc_bytes, total_bytes;
+};
+
+// Shared configuration for all groups (same D and PRF): key tile from the
+// largest batch; per group the subtree depth m_g keeps >= Ft frontier nodes
+// per key and f_g = n_g - m_g <= kTopSmemLevels (one grouped top launch);
+// items ordered by subtree size so the static round-robin stays balanced.
+int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t prf, GroupedPlan &gp) {
+  if (!gs || G == 0 || D == 0 || D > 1024 || (D & 3)) return DPF_EINVAL;
+  uint32_t Bmax = 0;
+  for (uint32_t i = 0; i < G; ++i) {
+    const dpf_eval_group &g = gs[i];
+    if (!g.keys_wire || !g.table || !g.shares || g.B == 0 || g.log_n < 1 || g.log_n > DPF_MAX_LOG_N ||
+        g.row_count == 0)
+      return DPF_EINVAL;
+    const uint64_t dom = 1ull << g.log_n;
+    if (g.row_begin >= dom || g.row_count > dom - g.row_begin) return DPF_EINVAL;
+    if ((reinterpret_cast<uintptr_t>(g.table) & 15) || (reinterpret_cast<uintptr_t>(g.keys_wire) & 15))
+      return DPF_EINVAL;
+    Bmax = std::max(Bmax, g.B);
+  }
+  Plan &pl = gp.cfg;
+  // Shared key tile: the Kt (power of two) that minimises the padded work
+  // sum_g ceil(B_g / Kt) * Kt * rows_g (lanes of missing keys idle), larger
+  // Kt on ties (fewer table re-reads).
+  uint32_t best_kt = 1;
+  double best_cost = 0;
+  for (uint32_t kt = 1; kt <= 32; kt <<= 1) {
+    if (kt * D > 8192) break;
+    double cost = 0;
+    for (uint32_t i = 0; i < G; ++i) cost += double((gs[i].B + kt - 1) / kt) * kt * double(gs[i].row_count);
+    if (kt == 1 || cost <= best_cost) {
+      best_cost = cost;
+      best_kt = kt;
+    }
+  }
+  // reuse the single-group planner for the shared part (tile, Ft, SMEM rules)
+  int rc = make_plan(best_kt, 20, 0, 1u << 20, D, pl);
+  if (rc) return rc;
+  pl.prf = prf;
+  (void)Bmax;
+  const uint32_t NP = uint32_t(pl.kc.NP);
+  const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((64 * 1024) / (32 * NP * 16)));
+  gp.desc.assign(G, dev::GroupDesc{});
+  uint32_t m_min_all = 32;
+  for (uint32_t i = 0; i < G; ++i) {
+    const dpf_eval_group &g = gs[i];
+    dev::GroupDesc &d = gp.desc[i];
+    const uint32_t n = g.log_n;
+    uint32_t lg_rows = 0;
+    while ((2ull << lg_rows) <= g.row_count) ++lg_rows;  // floor(log2(rows))
+    uint32_t lg_ft = 0;
+    while ((2u << lg_ft) <= pl.Ft) ++lg_ft;
+    uint32_t m = lg_rows > lg_ft ? lg_rows - lg_ft : 1;
+    m = std::max(1u, std::min(std::min(m, n), m_cap));
+    d.n = n;
+    d.m = m;
+    d.r0 = g.row_begin;
+    d.r1 = g.row_begin + g.row_count;
+    d.lo_f = d.r0 >> m;
+    d.F = ((d.r1 - 1) >> m) - d.lo_f + 1;
+    d.cap = d.F;
+    d.B = g.B;
+    d.kstride = uint32_t(dpf_key_wire_size(n));
+    d.n_ktiles = (g.B + pl.Kt - 1) / pl.Kt;
+    d.T = g.table;
+    d.shares = g.shares;
+    m_min_all = std::min(m_min_all, m);
+  }
+  // window: W leaf pairs must divide every group's 2^(m-1)
+  uint32_t W = std::min<uint32_t>(8, 1u << (m_min_all - 1));
+  const size_t stack_bytes = size_t(m_cap) * 32 * NP * 16;
+  for (;; W >>= 1) {
+    pl.W = W;
+    pl.y_stage_words = uint32_t(align_up(size_t(pl.Kt) * pl.Ft * 2 * W, 32));
+    pl.t_stage_words = uint32_t(align_up(size_t(pl.Ft) * 2 * W * D + 32u * pl.kc.CPL * pl.CG, 32));
+    pl.smem_bytes = 128 + 4 * (2 * size_t(pl.y_stage_words) + 2 * size_t(pl.t_stage_words)) + stack_bytes;
+    if (pl.smem_bytes <= 227 * 1024) break;
+    if (W == 1) return DPF_EINVAL;
+  }
+  // launch order: larger subtrees (bigger items) first
+  gp.order.resize(G);
+  for (uint32_t i = 0; i < G; ++i) gp.order[i] = i;
+  std::stable_sort(gp.order.begin(), gp.order.end(),
+                   [&](uint32_t a, uint32_t b) { return gp.desc[a].m > gp.desc[b].m; });
+  uint64_t items = 0, keys = 0;
+  gp.front_bytes = 0;
+  gp.keys_bytes = 0;
+  uint64_t blocks = 0;
+  for (uint32_t oi : gp.order) {
+    dev::GroupDesc &d = gp.desc[oi];
+    d.nwin = (1u << (d.m - 1)) / W;
+    d.item_base = uint32_t(items);
+    d.key_base = uint32_t(keys);
+    items += uint64_t(d.n_ktiles) * ((d.F + pl.Ft - 1) / pl.Ft);
+    keys += d.B;
+    gp.front_bytes += 2 * align_up(size_t(d.B) * d.cap * 16, kAlign);
+    gp.keys_bytes += align_up(size_t(d.B) * d.kstride, kAlign);
+    uint64_t top = 0;
+    for (uint32_t k = 0; k < d.n - d.m; ++k) top += ((d.r1 - 1) >> (d.n - k)) - (d.r0 >> (d.n - k)) + 1;
+    blocks += uint64_t(d.B) * top + uint64_t(d.n_ktiles) * ((d.F + pl.Ft - 1) / pl.Ft) * pl.tasks * ((1ull << d.m) - 1);
+  }
+  if (items > 0x7FFFFFFFull || keys > 0x7FFFFFFFull) return DPF_EINVAL;
+  pl.n_items = uint32_t(items);
+  pl.prf_blocks = blocks;
+  pl.grid = std::min<uint32_t>(pl.n_items, uint32_t(num_sms()));
+  gp.desc_bytes = align_up(size_t(G) * sizeof(dev::GroupDesc), kAlign);
+  gp.total_bytes = gp.front_bytes + gp.keys_bytes + gp.desc_bytes;
+  return DPF_OK;
+}
+
+thread_local Staging g_desc_staging;
+
+}  // namespace
+}  // namespace dpfpir
+
+extern "C" size_t dpf_eval_grouped_workspace_bytes(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D,
+                                                   uint32_t prf) {
+  GroupedPlan gp;
+  if (make_grouped_plan(groups, n_groups, D, prf, gp) != DPF_OK) return 0;
+  return gp.total_bytes;
+}
+
+extern "C" int dpf_eval_grouped(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D, uint32_t prf,
+                                void *workspace, size_t workspace_bytes, void *stream) {
+  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128) return DPF_EUNSUPPORTED;
+  if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & (kAlign - 1))) return DPF_EINVAL;
+  GroupedPlan gp;
+  int rc = make_grouped_plan(groups, n_groups, D, prf, gp);
+  if (rc) return rc;
+  if (workspace_bytes < gp.total_bytes) return DPF_ENOMEM;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  uint8_t *base = static_cast<uint8_t *>(workspace);
+  uint8_t *front = base, *kbuf = base + gp.front_bytes, *dbuf = kbuf + gp.keys_bytes;
+  // device-side keys: ChaCha uses the caller's wire keys in place; AES gets a
+  // bitsliced private copy
+  size_t foff = 0, koff = 0;
+  for (uint32_t oi : gp.order) {
+    dev::GroupDesc &d = gp.desc[oi];
+    const dpf_eval_group &g = groups[oi];
+    d.frontier = reinterpret_cast<uint4 *>(front + foff);
+    foff += align_up(size_t(d.B) * d.cap * 16, kAlign);
+    d.frontier_alt = reinterpret_cast<uint4 *>(front + foff);
+    foff += align_up(size_t(d.B) * d.cap * 16, kAlign);
+    if (prf == DPF_PRF_AES128) {
+      uint8_t *kd = kbuf + koff;
+      if (cudaMemcpyAsync(kd, g.keys_wire, size_t(d.B) * d.kstride, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return DPF_ECUDA;
+      const uint64_t n_items = uint64_t(d.B) * (1 + 4 * d.n);
+      dev::aes_bitslice_keys_kernel<<<uint32_t(std::min<uint64_t>((n_items + 255) / 256, 148ull * 8)), 256, 0, st>>>(
+          kd, d.kstride, d.B, d.n);
+      d.keys = kd;
+    } else {
+      d.keys = g.keys_wire;
+    }
+    koff += align_up(size_t(d.B) * d.kstride, kAlign);
+  }
+  // descriptors in launch order (sorted by item_base) -> pinned staging -> device
+  std::vector<dev::GroupDesc> sorted;
+  sorted.reserve(n_groups);
+  for (uint32_t oi : gp.order) sorted.push_back(gp.desc[oi]);
+  Staging &sg = g_desc_staging;
+  const int slot = sg.next;
+  sg.next ^= 1;
+  const size_t db = sorted.size() * sizeof(dev::GroupDesc);
+  if (sg.done[slot]) cudaEventSynchronize(sg.done[slot]);
+  if (sg.cap[slot] < db) {
+    if (sg.buf[slot]) cudaFreeHost(sg.buf[slot]);
+    sg.buf[slot] = nullptr;
+    sg.cap[slot] = 0;
+    if (cudaHostAlloc(&sg.buf[slot], db, cudaHostAllocDefault) != cudaSuccess) return DPF_ECUDA;
+    sg.cap[slot] = db;
+  }
+  if (!sg.done[slot] && cudaEventCreateWithFlags(&sg.done[slot], cudaEventDisableTiming) != cudaSuccess)
+    return DPF_ECUDA;
+  std::memcpy(sg.buf[slot], sorted.data(), db);
+  if (cudaMemcpyAsync(dbuf, sg.buf[slot], db, cudaMemcpyHostToDevice, st) != cudaSuccess) return DPF_ECUDA;
+  if (cudaEventRecord(sg.done[slot], st) != cudaSuccess) return DPF_ECUDA;
+  const dev::GroupDesc *ddesc = reinterpret_cast<const dev::GroupDesc *>(dbuf);
+  uint32_t nk = prf == DPF_PRF_AES128 ? n_groups : 0;
+  // a7 zeroing, a2 top BFS, then the fused kernel over all groups' items
+  dev::zero_shares_grouped_kernel<<<dim3(64, std::min<uint32_t>(n_groups, 1024)), 256, 0, st>>>(ddesc, n_groups, D);
+  uint64_t total_keys = 0;
+  for (const auto &d : sorted) total_keys += d.B;
+  if (prf == DPF_PRF_AES128)
+    dev::expand_top_grouped_kernel<dev::PrfAesBs><<<uint32_t(total_keys), 256, 0, st>>>(ddesc, n_groups);
+  else
+    dev::expand_top_grouped_kernel<dev::PrfChacha><<<uint32_t(total_keys), 256, 0, st>>>(ddesc, n_groups);
+  nk += 2;
+  uint32_t f_max = 0;
+  for (const auto &d : sorted) f_max = std::max(f_max, d.n - d.m);
+  for (uint32_t k = kTopSmemLevelsHost + 1; k <= f_max; ++k) {  // deeper frontiers: one launch per level
+    const dim3 grid(148 * 4, n_groups);
+    if (prf == DPF_PRF_AES128)
+      dev::expand_level_grouped_kernel<dev::PrfAesBs><<<grid, 256, 0, st>>>(ddesc, k);
+    else
+      dev::expand_level_grouped_kernel<dev::PrfChacha><<<grid, 256, 0, st>>>(ddesc, k);
+    ++nk;
+  }
+  const Plan &pl = gp.cfg;
+  dev::FusedParams p;
+  std::memset(&p, 0, sizeof p);
+  p.g0 = sorted[0];
+  p.groups = ddesc;
+  p.n_groups = n_groups;
+  p.n_items = pl.n_items;
+  p.D = D;
+  p.Kt = pl.Kt;
+  p.Ft = pl.Ft;
+  p.tasks = pl.tasks;
+  p.W = pl.W;
+  p.CG = pl.CG;
+  p.KG = pl.KG;
+  p.y_stage_words = pl.y_stage_words;
+  p.t_stage_words = pl.t_stage_words;
+  auto kfn = prf == DPF_PRF_AES128 ? pl.kc.fn_aes : pl.kc.fn;
+  if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
+    return DPF_ECUDA;
+  const bool timed = g_timer.on && 2 * g_timer.used + 1 < g_timer.ev.size();
+  if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
+  kfn<<<pl.grid, 32 * (pl.kc.NP + kNC + 1), pl.smem_bytes, st>>>(p);
+  if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used++ + 1], st);
+  ++nk;
+  if (cudaGetLastError() != cudaSuccess) return DPF_ECUDA;
+  g_stats.prf_blocks = pl.prf_blocks;
+  g_stats.kernels = nk;
+  g_stats.frontier_depth = 0;
+  g_stats.keys_per_tile = pl.Kt;
+  g_stats.nodes_per_tile = pl.Ft;
+  g_stats.work_items = pl.n_items;
+  g_stats.grid = pl.grid;
   return DPF_OK;
 }

@@ -48,6 +48,13 @@ class DpfEvalStats(ctypes.Structure):
                 ("work_items", ctypes.c_uint32), ("grid", ctypes.c_uint32)]
 
 
+class DpfEvalGroup(ctypes.Structure):
+    """dpf_eval_group (include/dpfpir.h)."""
+    _fields_ = [("keys_wire", ctypes.c_void_p), ("B", ctypes.c_uint32), ("log_n", ctypes.c_uint32),
+                ("table", ctypes.c_void_p), ("row_begin", ctypes.c_uint64), ("row_count", ctypes.c_uint64),
+                ("shares", ctypes.c_void_p)]
+
+
 KEY_BYTES = ctypes.sizeof(DpfKey)
 _lib = None
 
@@ -80,6 +87,9 @@ def lib() -> ctypes.CDLL:
     L.dpf_table_pack.argtypes = [vp, u64, u64, u32, vp, vp]
     L.dpf_eval_batch_packed.argtypes = [vp, u32, vp, u64, u64, u32, vp, vp, sz, vp]
     L.dpf_eval_batch_wire_packed.argtypes = [vp, u32, u32, u32, vp, u64, u64, u32, vp, vp, sz, vp]
+    L.dpf_eval_grouped_workspace_bytes.argtypes = [vp, u32, u32, u32]
+    L.dpf_eval_grouped_workspace_bytes.restype = sz
+    L.dpf_eval_grouped.argtypes = [vp, u32, u32, u32, vp, sz, vp]
     L.dpf_last_eval_stats.argtypes = [vp]
     L.dpf_kernel_timer_begin.argtypes = [u32]
     L.dpf_kernel_timer_read.argtypes = [vp, u32, vp]
@@ -95,6 +105,7 @@ EXPORTED_SYMBOLS = ("dpf_gen", "dpf_key_wire_size", "dpf_key_serialize", "dpf_ke
                     "dpf_eval_workspace_bytes", "dpf_eval_batch", "dpf_eval_batch_shard", "dpf_eval_batch_wire",
                     "dpf_serve_batch", "dpf_eval_leaves", "dpf_last_eval_stats", "dpf_kernel_timer_begin",
                     "dpf_table_packed_bytes", "dpf_table_pack", "dpf_eval_batch_packed", "dpf_eval_batch_wire_packed",
+                    "dpf_eval_grouped_workspace_bytes", "dpf_eval_grouped",
                     "dpf_kernel_timer_read", "dpf_strerror", "dpf_version")
 
 
@@ -340,6 +351,38 @@ def eval_batch_wire_packed(keys_wire_dev, log_n: int, packed: PackedTable, out=N
                                             ws.numel() * ws.element_size(), _stream_ptr(stream)),
            "dpf_eval_batch_wire_packed")
     return out
+
+
+def _group_array(groups):
+    arr = (DpfEvalGroup * len(groups))()
+    for i, g in enumerate(groups):
+        keys_wire, log_n, table, row_begin, shares = g
+        arr[i].keys_wire = keys_wire.data_ptr()
+        arr[i].B = keys_wire.shape[0]
+        arr[i].log_n = log_n
+        arr[i].table = table.data_ptr()
+        arr[i].row_begin = row_begin
+        arr[i].row_count = table.shape[0]
+        arr[i].shares = shares.data_ptr()
+    return arr
+
+
+def eval_grouped_workspace_bytes(groups, D: int, prf: int = DPF_PRF_CHACHA20) -> int:
+    return lib().dpf_eval_grouped_workspace_bytes(_group_array(groups), len(groups), D, prf)
+
+
+def eval_grouped(groups, D: int, prf: int = DPF_PRF_CHACHA20, workspace=None, stream=None):
+    """dpf_eval_grouped.  groups: list of (keys_wire_dev uint8 [B, 32+64n], log_n,
+    table_shard int32 [rows, D], row_begin, shares int32 [B, D]); all CUDA tensors."""
+    arr = _group_array(groups)
+    need = lib().dpf_eval_grouped_workspace_bytes(arr, len(groups), D, prf)
+    if need == 0:
+        raise DpfError(DPF_EINVAL, "dpf_eval_grouped_workspace_bytes")
+    dev = groups[0][2].device
+    ws = workspace if workspace is not None else _workspace(need, dev)
+    _check(lib().dpf_eval_grouped(arr, len(groups), D, prf, ws.data_ptr(), ws.numel() * ws.element_size(),
+                                  _stream_ptr(stream)), "dpf_eval_grouped")
+    return [g[4] for g in groups]
 
 
 def serve_workspace_bytes(B: int, log_n: int, rows: int, D: int) -> int:

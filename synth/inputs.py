@@ -14,7 +14,7 @@ import dataclasses
 
 import numpy as np
 
-__all__ = ["Workload", "CONFIGS", "table", "table_rows", "alphas", "betas", "gen_seeds", "rng"]
+__all__ = ["Workload", "CONFIGS", "CODESIGN_LOG2_ROWS", "CODESIGN_D", "codesign_frequency", "codesign_needed", "table", "table_rows", "alphas", "betas", "gen_seeds", "rng"]
 
 _STREAM_TABLE, _STREAM_ALPHA, _STREAM_BETA, _STREAM_GEN = 1, 2, 3, 4
 
@@ -85,3 +85,29 @@ CONFIGS = {
     "c4": Workload("c4", 24, 1 << 24, 64, 512, 0x7AB1E004, "2^24 x 64, B=512, row-sharded over G GPUs"),
     "t5": Workload("t5", 20, 1 << 20, 64, 512, 0x7AB1E005, "Table 5 shape: 2^20 x 64, B=512 (context)"),
 }
+
+
+# Config c5 (BASELINE.json): 26 recommendation tables of mixed sizes, D = 32.
+# log2 row counts [12..22, 12..22, 12..15]; accesses Zipf(1.0)
+# per table (embedding accesses are heavily skewed).
+CODESIGN_LOG2_ROWS = list(range(12, 23)) + list(range(12, 23)) + list(range(12, 16))
+CODESIGN_D = 32
+
+
+def codesign_frequency(table_id: int, n_rows: int, seed: int = 0xC0DE5) -> np.ndarray:
+    """Zipf(1.0) access frequency of each row, over a random row permutation."""
+    g = rng(seed + table_id, 11)
+    perm = g.permutation(n_rows)
+    freq = np.empty(n_rows, np.float64)
+    freq[perm] = 1.0 / np.arange(1, n_rows + 1)
+    return freq
+
+
+def codesign_needed(table_id: int, n_rows: int, n_inferences: int, per_inference: int,
+                    seed: int = 0xC0DE5) -> np.ndarray:
+    """Rows each inference needs from one table: `per_inference` draws from
+    the table's Zipf(1.0) access distribution.  int64 [n_inferences, per_inference]."""
+    freq = codesign_frequency(table_id, n_rows, seed)
+    p = freq / freq.sum()
+    g = rng(seed + table_id, 12)
+    return g.choice(n_rows, size=(n_inferences, per_inference), p=p)

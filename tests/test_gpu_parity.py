@@ -265,3 +265,29 @@ def test_aes_wire_shard_and_reconstruct(dp, oracle):
     part = dp.as_u32(dp.eval_batch_shard([p[1] for p in pairs], to_dev(T[5000:]), 5000)) + \
         dp.as_u32(dp.eval_batch_shard([p[1] for p in pairs], to_dev(T[:5000]), 0))
     np.testing.assert_array_equal(dp.reconstruct(sh0, part), T[al.astype(np.int64)])
+
+
+# ---------------------------------------------------------------- grouped launches (row f2)
+
+@pytest.mark.parametrize("prf", [1, 2])
+def test_grouped_equals_per_group_and_oracle(dp, oracle, prf):
+    D = 32
+    shapes = [(12, 4096, 0, 4096, 5), (9, 300, 0, 300, 17), (14, 9000, 1000, 7000, 40), (1, 2, 0, 2, 3),
+              (13, 8192, 0, 8192, 64), (10, 1024, 512, 512, 1)]
+    groups, expect = [], []
+    for i, (n, N, r0, rows, B) in enumerate(shapes):
+        T = synth.table(N, D, 900 + i)
+        al = synth.alphas(B, N, 900 + i)
+        keys = [dp.gen(n, int(a), 1, s, prf=prf)[(j + i) % 2]
+                for j, (a, s) in enumerate(zip(al, synth.gen_seeds(B, 900 + i)))]
+        okeys = [oracle.key_from_wire(dp.key_serialize(k)) for k in keys]
+        Tsh = T[r0:r0 + rows]
+        wire = torch.from_numpy(dp.keys_to_wire(keys)).cuda()
+        out = torch.empty((B, D), dtype=torch.int32, device="cuda")
+        groups.append((wire, n, to_dev(Tsh), r0, out))
+        expect.append(oracle.answer_batch(okeys, Tsh, row_begin=r0, threads=8))
+    dp.eval_grouped(groups, D, prf=prf)
+    torch.cuda.synchronize()
+    for (wire, n, Td, r0, out), want in zip(groups, expect):
+        np.testing.assert_array_equal(dp.as_u32(out), want)
+        np.testing.assert_array_equal(dp.as_u32(dp.eval_batch_wire(wire, n, Td, r0, prf=prf)), want)

@@ -1,0 +1,106 @@
+"""Co-design workload (BASELINE config c5, row f2) on one GPU.
+
+26 embedding tables (log2 rows [12..22, 12..22, 12..15], D = 32, Zipf(1.0)
+accesses), each split into a hot table (top `--hot` fraction of rows) and the
+full table.  Every inference needs `--need` rows per table; the
+client routes them to Q_hot hot / Q_full full keys per table (dummy-padded,
+excess dropped).  The server answers a batch of inferences with ONE
+dpf_eval_grouped call over the 52 (table, hot|full) groups; compared with 52
+separate dpf_eval_batch_wire calls.  Batch sweep over inferences per batch.
+    python tools/codesign_bench.py [--batches 1 4 16 64 256 1024]
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import synth  # noqa: E402
+from paper_2301_10904_b200 import codesign, dpfpir  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--batches", type=int, nargs="+", default=[1, 4, 16, 64, 256, 1024])
+ap.add_argument("--hot", type=float, default=0.1)
+ap.add_argument("--q-hot", type=int, default=2)
+ap.add_argument("--q-full", type=int, default=1)
+ap.add_argument("--need", type=int, default=3)
+ap.add_argument("--steps", type=int, default=5)
+ap.add_argument("--check", type=int, default=2, help="inferences whose rows are reconstructed and checked")
+a = ap.parse_args()
+D = synth.CODESIGN_D
+rng = np.random.default_rng(0)
+tables = []
+for t, lg in enumerate(synth.CODESIGN_LOG2_ROWS):
+    N = 1 << lg
+    T = synth.table(N, D, 0xC5000 + t)
+    sp = codesign.HotSplit.from_frequency(synth.codesign_frequency(t, N), a.hot)
+    H = sp.hot_table(T)
+    tables.append(dict(N=N, T=T, Td=torch.from_numpy(T.view(np.int32)).cuda(), split=sp, hmap=sp.hot_index(),
+                       Hd=torch.from_numpy(H.view(np.int32)).cuda(), nH=codesign.log2_domain(sp.n_hot),
+                       nF=codesign.log2_domain(N)))
+torch.cuda.synchronize()
+seed_iter = iter(synth.gen_seeds(200000, 0xC5))
+for Binf in a.batches:
+    # client: plan + keys (outside the timed region: client work)
+    groups0, groups1, real = [], [], []
+    dropped = 0
+    for t, tb in enumerate(tables):
+        need = synth.codesign_needed(t, tb["N"], Binf, a.need)
+        plans = [codesign.plan_table(r, tb["split"], tb["hmap"], a.q_hot, a.q_full, rng) for r in need]
+        dropped += sum(p.dropped for p in plans)
+        for kind, tbl, n, idxs in (("hot", tb["Hd"], tb["nH"], [p.hot_idx for p in plans]),
+                                   ("full", tb["Td"], tb["nF"], [p.full_idx for p in plans])):
+            flat = np.concatenate(idxs)
+            pairs = [dpfpir.gen(n, int(i), 1, next(seed_iter)) for i in flat]
+            for party, gl in ((0, groups0), (1, groups1)):
+                wire = torch.from_numpy(dpfpir.keys_to_wire([p[party] for p in pairs])).cuda()
+                out = torch.empty((len(flat), D), dtype=torch.int32, device="cuda")
+                gl.append((wire, n, tbl, 0, out))
+            real.append((t, kind, plans))
+    n_keys = sum(g[0].shape[0] for g in groups0)
+    ws = torch.empty(dpfpir.eval_grouped_workspace_bytes(groups0, D), dtype=torch.uint8, device="cuda")
+
+    def grouped():
+        dpfpir.eval_grouped(groups0, D, workspace=ws)
+
+    def separate():
+        for (wire, n, tbl, r0, out) in groups0:
+            dpfpir.eval_batch_wire(wire, n, tbl, r0, out=out)
+
+    res = {}
+    for name, fn in (("grouped", grouped), ("separate", separate)):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.steps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        res[name] = e0.elapsed_time(e1) / a.steps
+    # correctness: second server, reconstruct the first inferences' real queries
+    grouped()
+    dpfpir.eval_grouped(groups1, D)
+    torch.cuda.synchronize()
+    ok = True
+    for gi, (t, kind, plans) in enumerate(real):
+        ans = dpfpir.reconstruct(dpfpir.as_u32(groups0[gi][4]), dpfpir.as_u32(groups1[gi][4]))
+        q = a.q_hot if kind == "hot" else a.q_full
+        for inf in range(min(a.check, Binf)):
+            p = plans[inf]
+            rows = p.hot_rows if kind == "hot" else p.full_idx
+            mask = p.hot_real if kind == "hot" else p.full_real
+            for j in np.nonzero(mask)[0]:
+                ok &= bool(np.array_equal(ans[inf * q + j], tables[t]["T"][rows[j]]))
+    blocks = sum(g[0].shape[0] * (g[2].shape[0] - 1) for g in groups0)  # nodes over each table's rows
+    ms = res["grouped"]
+    print(json.dumps({"workload": "c5 co-design", "inferences_per_batch": Binf, "keys_per_batch": n_keys,
+                      "q_hot": a.q_hot, "q_full": a.q_full, "hot_fraction": a.hot, "need_per_table": a.need,
+                      "dropped_rows": dropped, "ms_grouped": round(ms, 4), "ms_separate": round(res["separate"], 4),
+                      "inferences_per_s": round(Binf / (ms * 1e-3), 1), "dpf_queries_per_s": round(n_keys / (ms * 1e-3)),
+                      "alu_frac": round(640 * blocks / (ms * 1e-3) / (148 * 64 * 1965e6), 3),
+                      "rows_reconstructed_ok": ok}), flush=True)
