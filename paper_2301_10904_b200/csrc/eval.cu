@@ -219,8 +219,9 @@ struct FusedParams {
   uint32_t n_groups, n_items, D;
   uint32_t Kt, Ft, tasks;  // tasks = Kt * Ft <= 32 * NP (lanes >= tasks idle)
   uint32_t W;              // leaf pairs per producer thread per window
-  uint32_t CG, KG;         // consumer col groups / key groups
-  uint32_t y_stage_words, t_stage_words;
+  uint32_t CG, KG, SG;     // consumer col groups / key groups / slot groups
+  uint32_t y_stage_words, t_stage_words;  // t: one T-ring entry (CN nodes x 2W rows x D + pad)
+  uint32_t CN, n_chunks, NST;             // IMAD kernel: nodes per T entry, entries per window, ring depth
 };
 
 __device__ __forceinline__ GroupDesc group_of(const FusedParams &p, uint32_t item) {
@@ -246,11 +247,15 @@ struct Smem {
 template <int KPW, int CPL>
 __device__ __forceinline__ void consume_window(const uint32_t *__restrict__ yb, const uint32_t *__restrict__ tb,
                                                uint32_t nslots, uint32_t Kt, uint32_t D, uint32_t key0,
-                                               uint32_t colbase, uint32_t (&acc)[KPW][CPL]) {
-  const uint32_t *yp = yb + key0;
-  const uint32_t *tp = tb + colbase;
-#pragma unroll 2
-  for (uint32_t s = 0; s < nslots; ++s) {
+                                               uint32_t colbase, uint32_t s0, uint32_t sstep,
+                                               uint32_t (&acc)[KPW][CPL]) {
+  // slots s0, s0 + sstep, ... (slot groups: small key tiles spread the
+  // window's leaves over several consumer warps)
+  const uint32_t *yp = yb + key0 + s0 * Kt;
+  const uint32_t *tp = tb + colbase + s0 * D;
+  const uint32_t ystep = sstep * Kt, tstep = sstep * D;
+#pragma unroll 4
+  for (uint32_t s = s0; s < nslots; s += sstep) {
     uint32_t tv[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) tv[c] = tp[32 * c];
@@ -269,34 +274,34 @@ __device__ __forceinline__ void consume_window(const uint32_t *__restrict__ yb, 
     for (int k = 0; k < KPW; ++k)
 #pragma unroll
       for (int c = 0; c < CPL; ++c) acc[k][c] += yv[k] * tv[c];
-    yp += Kt;
-    tp += D;
+    yp += ystep;
+    tp += tstep;
   }
 }
 
 template <class Prf, int NP, int NC, int KPW, int CPL>
 __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const FusedParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint64_t *tfull = reinterpret_cast<uint64_t *>(smem);  // T-tile ring: bulk-copy completion
-  constexpr uint32_t kFullThreads = 32 * (NP + NC), kEmptyThreads = 32 * (NP + NC + 1);
+  uint64_t *tfull = reinterpret_cast<uint64_t *>(smem);  // T ring [NST]: bulk-copy completion
+  uint64_t *tempty = tfull + 8;                          // T ring [NST]: consumers done (count NC)
+  constexpr uint32_t kFullThreads = 32 * (NP + NC), kEmptyThreads = 32 * (NP + NC);
   // windows this CTA will run (consumers skip the EMPTY arrive for the last
   // two, which no producer will ever wait for)
   uint32_t total_w = 0;
   for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) total_w += group_of(p, item).nwin;
   uint32_t *ybuf = reinterpret_cast<uint32_t *>(smem + 128);
   uint32_t *tbuf = ybuf + 2 * p.y_stage_words;
-  uint4 *stack = reinterpret_cast<uint4 *>(tbuf + 2 * p.t_stage_words);
+  uint4 *stack = reinterpret_cast<uint4 *>(tbuf + p.NST * p.t_stage_words);
 
   const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (uint32_t s = 0; s < p.NST; ++s) {
       mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], NC);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-
-  const uint32_t nslots = p.Ft * 2 * p.W;
 
   if (warp < NP) {
     // ------------------------------------------------------------ producers
@@ -357,8 +362,9 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
   } else if (warp < NP + NC) {
     // ------------------------------------------------------------ consumers
     const uint32_t cwarp = warp - NP;
-    const uint32_t kg = cwarp / p.CG, cg = cwarp % p.CG;
-    const bool active = kg < p.KG;
+    const uint32_t tile = cwarp % (p.KG * p.CG), sg = cwarp / (p.KG * p.CG);
+    const uint32_t kg = tile / p.CG, cg = tile % p.CG;
+    const bool active = sg < p.SG;
     const uint32_t key0 = kg * KPW;
     const uint32_t colbase = cg * CPL * 32 + lane;
     uint32_t acc[KPW][CPL];
@@ -366,17 +372,25 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
     for (int k = 0; k < KPW; ++k)
 #pragma unroll
       for (int c = 0; c < CPL; ++c) acc[k][c] = 0;
-    uint32_t wseq = 0;
+    uint32_t wseq = 0, tseq = 0;
+    const uint32_t seg = 2 * p.W;  // rows per node per window
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       const GroupDesc g = group_of(p, item);
       const uint32_t kt = (item - g.item_base) % g.n_ktiles;
       for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
-        const uint32_t stage = wseq & 1, use = wseq >> 1;
+        const uint32_t stage = wseq & 1;
         named_sync(1 + stage, kFullThreads);
-        mbar_wait(&tfull[stage], use & 1);
-        if (active)
-          consume_window<KPW, CPL>(ybuf + stage * p.y_stage_words, tbuf + stage * p.t_stage_words, nslots, p.Kt,
-                                   p.D, key0, colbase, acc);
+        const uint32_t *yb = ybuf + stage * p.y_stage_words;
+        for (uint32_t ch = 0; ch < p.n_chunks; ++ch, ++tseq) {
+          const uint32_t ts = tseq % p.NST, tuse = tseq / p.NST;
+          const uint32_t n0 = ch * p.CN, nn = min(p.CN, p.Ft - n0);
+          mbar_wait(&tfull[ts], tuse & 1);
+          if (active)
+            consume_window<KPW, CPL>(yb + n0 * seg * p.Kt, tbuf + ts * p.t_stage_words, nn * seg, p.Kt, p.D, key0,
+                                     colbase, sg, p.SG, acc);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[ts]);
+        }
         if (wseq + 2 < total_w) named_arrive(3 + stage, kEmptyThreads);
       }
       // a6/a7: flush this item's partial answers, party sign applied once.
@@ -399,35 +413,40 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
     }
   } else {
     // ------------------------------------------------------------ T loader
-    uint32_t wseq = 0;
+    // T ring of (window, node chunk) entries: CN nodes x 2W rows, one
+    // cp.async.bulk per node segment, decoupled from the y ring.
+    uint32_t tseq = 0;
     const uint64_t seg_rows = 2 * p.W;
     const uint32_t row_bytes = p.D * 4;
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       const GroupDesc g = group_of(p, item);
       const uint32_t ng = (item - g.item_base) / g.n_ktiles;
-      for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
-        const uint32_t stage = wseq & 1, use = wseq >> 1;
-        if (use > 0) named_sync(3 + stage, kEmptyThreads);
-        uint32_t *tb = tbuf + stage * p.t_stage_words;
-        uint32_t my_bytes = 0;
-        for (uint32_t nl = lane; nl < p.Ft; nl += 32) {
-          const uint64_t node = uint64_t(ng) * p.Ft + nl;
-          if (node >= g.F) continue;
-          const uint64_t s0 = ((g.lo_f + node) << g.m) + seg_rows * win;
-          const uint64_t a = s0 > g.r0 ? s0 : g.r0, e = (s0 + seg_rows) < g.r1 ? (s0 + seg_rows) : g.r1;
-          if (a < e) my_bytes += uint32_t(e - a) * row_bytes;
-        }
-        const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, my_bytes);
-        if (lane == 0) mbar_arrive_expect_tx(&tfull[stage], total);
-        __syncwarp();
-        for (uint32_t nl = lane; nl < p.Ft; nl += 32) {
-          const uint64_t node = uint64_t(ng) * p.Ft + nl;
-          if (node >= g.F) continue;
-          const uint64_t s0 = ((g.lo_f + node) << g.m) + seg_rows * win;
-          const uint64_t a = s0 > g.r0 ? s0 : g.r0, e = (s0 + seg_rows) < g.r1 ? (s0 + seg_rows) : g.r1;
-          if (a < e)
-            bulk_g2s(tb + (uint64_t(nl) * seg_rows + (a - s0)) * p.D, g.T + (a - g.r0) * p.D,
-                     uint32_t(e - a) * row_bytes, &tfull[stage]);
+      for (uint32_t win = 0; win < g.nwin; ++win) {
+        for (uint32_t ch = 0; ch < p.n_chunks; ++ch, ++tseq) {
+          const uint32_t ts = tseq % p.NST, tuse = tseq / p.NST;
+          if (tuse > 0) mbar_wait(&tempty[ts], (tuse - 1) & 1);
+          uint32_t *tb = tbuf + ts * p.t_stage_words;
+          const uint32_t n0 = ch * p.CN, n1 = min(p.Ft, n0 + p.CN);
+          uint32_t my_bytes = 0;
+          for (uint32_t nl = n0 + lane; nl < n1; nl += 32) {
+            const uint64_t node = uint64_t(ng) * p.Ft + nl;
+            if (node >= g.F) continue;
+            const uint64_t s0 = ((g.lo_f + node) << g.m) + seg_rows * win;
+            const uint64_t a = s0 > g.r0 ? s0 : g.r0, e = (s0 + seg_rows) < g.r1 ? (s0 + seg_rows) : g.r1;
+            if (a < e) my_bytes += uint32_t(e - a) * row_bytes;
+          }
+          const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, my_bytes);
+          if (lane == 0) mbar_arrive_expect_tx(&tfull[ts], total);
+          __syncwarp();
+          for (uint32_t nl = n0 + lane; nl < n1; nl += 32) {
+            const uint64_t node = uint64_t(ng) * p.Ft + nl;
+            if (node >= g.F) continue;
+            const uint64_t s0 = ((g.lo_f + node) << g.m) + seg_rows * win;
+            const uint64_t a = s0 > g.r0 ? s0 : g.r0, e = (s0 + seg_rows) < g.r1 ? (s0 + seg_rows) : g.r1;
+            if (a < e)
+              bulk_g2s(tb + (uint64_t(nl - n0) * seg_rows + (a - s0)) * p.D, g.T + (a - g.r0) * p.D,
+                       uint32_t(e - a) * row_bytes, &tfull[ts]);
+          }
         }
       }
     }
@@ -540,9 +559,8 @@ namespace {
 
 constexpr int kNC = 4;  // consumer warps
 constexpr size_t kAlign = 256;
-constexpr uint32_t kMaxTStageBytes = 64 * 1024;
 constexpr uint32_t kTopSmemLevelsHost = 10;  // == dev::kTopSmemLevels
-constexpr uint32_t kMaxTStageBytesW1 = 80 * 1024;  // leaves room for a 64 KB DFS stack
+constexpr uint32_t kTEntryBytes = 32 * 1024;   // IMAD kernel T-ring entry
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 inline uint32_t pow2ceil(uint32_t v) {
@@ -569,9 +587,9 @@ struct Plan {
   uint32_t nsy, nst;  // y-ring / T-ring depth (tc)
   uint32_t tmem_cols, y_stage_bytes, t_stage_bytes;
   uint64_t r0a, packed_rows;
-  uint32_t n, m, f, Kt, Ft, tasks, W, CG, KG, n_ktiles, n_items, nwin, grid;
+  uint32_t n, m, f, Kt, Ft, tasks, W, CG, KG, SG, n_ktiles, n_items, nwin, grid;
   uint64_t r0, r1, F, lo_f, cap;
-  uint32_t y_stage_words, t_stage_words;
+  uint32_t y_stage_words, t_stage_words, CN, n_chunks, NST;
   size_t smem_bytes;
   KernelChoice kc;
   uint64_t prf_blocks;
@@ -630,17 +648,51 @@ bool pick_kernel(uint32_t Kt, uint32_t D, Plan &pl) {
       if (Kt % uint32_t(kc.KPW) || Kt / kc.KPW > KG) continue;
       if (32u * kc.CPL * CG < D) continue;
       const uint32_t per_warp = kc.CPL + (kc.KPW + 3) / 4 + kc.KPW * kc.CPL;
+      const uint32_t sg = kNC / ((Kt / kc.KPW) * CG);  // slot groups share the window
       const uint32_t total = per_warp * CG * (Kt / kc.KPW);
-      const uint64_t score = (uint64_t(per_warp) << 32) | total;
+      const uint64_t score = (uint64_t(per_warp * 16 / sg) << 32) | total;
       if (score < best) {
         best = score;
         pl.CG = CG;
         pl.KG = Kt / kc.KPW;
+        pl.SG = kNC / (pl.KG * CG);  // idle warps take other slots of the window
         pl.kc = kc;
       }
     }
   }
   return best != ~0ull;
+}
+
+// Subtree depth m: the largest m (<= m_cap) that still gives >= 8 work items
+// per SM (measured: beyond that, deeper top BFS costs more than balance gains).
+uint32_t choose_m_target(const Plan &pl, uint32_t n, uint64_t r0, uint32_t m_min, uint32_t m_cap) {
+  const uint64_t target = 8ull * num_sms();
+  uint32_t best = m_min;
+  for (uint32_t m = std::min<uint32_t>(n, m_cap); m >= m_min; --m) {
+    const uint64_t F = ((pl.r1 - 1) >> m) - (r0 >> m) + 1;
+    const uint64_t items = uint64_t(pl.n_ktiles) * ((F + pl.Ft - 1) / pl.Ft);
+    best = m;
+    if (items >= target) break;
+  }
+  return best;
+}
+
+// Window / T-ring sizing for the IMAD kernel; false if SMEM does not fit.
+bool set_windows(Plan &pl, uint32_t W, uint32_t D, size_t stack_bytes) {
+  pl.W = W;
+  pl.y_stage_words = uint32_t(align_up(size_t(pl.Kt) * pl.Ft * 2 * W, 32));
+  const uint32_t pad = 32u * pl.kc.CPL * pl.CG;  // lanes whose columns exceed D read past the last row
+  uint32_t CN = pl.Ft;
+  while (CN > 1 && (size_t(CN) * 2 * W * D + pad) * 4 > kTEntryBytes) CN >>= 1;
+  if ((size_t(CN) * 2 * W * D + pad) * 4 > kTEntryBytes) return false;
+  pl.CN = CN;
+  pl.n_chunks = (pl.Ft + CN - 1) / CN;
+  pl.t_stage_words = uint32_t(align_up(size_t(CN) * 2 * W * D + pad, 32));
+  const size_t fixed = 128 + 4 * 2 * size_t(pl.y_stage_words) + stack_bytes;
+  if (fixed + 2 * 4 * size_t(pl.t_stage_words) > 227 * 1024) return false;
+  pl.NST = uint32_t(std::min<size_t>(8, (227 * 1024 - fixed) / (4 * size_t(pl.t_stage_words))));
+  pl.smem_bytes = fixed + 4 * size_t(pl.NST) * pl.t_stage_words;
+  return true;
 }
 
 int make_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl) {
@@ -654,23 +706,18 @@ int make_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Pl
   if (!pick_kernel(pl.Kt, D, pl)) return DPF_EINVAL;
   const uint32_t NP = uint32_t(pl.kc.NP);
   pl.Ft = 32 * NP / pl.Kt;
-  // T stage must fit: Ft * 2 rows * D words at W = 1, plus the column padding.
-  while ((uint64_t(pl.Ft) * 2 * D + 32u * pl.kc.CPL * pl.CG) * 4 > kMaxTStageBytesW1 && pl.Ft > 1) pl.Ft >>= 1;
+  // one T-ring entry must hold at least one node's 2-row segment
+  while ((uint64_t(2) * D + 32u * pl.kc.CPL * pl.CG) * 4 > kTEntryBytes && pl.Ft > 1) pl.Ft >>= 1;
   pl.tasks = pl.Kt * pl.Ft;
   pl.n_ktiles = (B + pl.Kt - 1) / pl.Kt;
-  // Subtree depth m (frontier depth f = n - m): the largest m that still
-  // gives >= 8 work items per SM; the SMEM DFS stack (m x 16 B per producer
-  // thread) is capped at 64 KB.
-  const uint64_t target = 8ull * num_sms();
+  // Subtree depth m (frontier depth f = n - m) from a cost model; the SMEM
+  // DFS stack (m x 16 B per producer thread) is capped at 64 KB.
   const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((64 * 1024) / (32 * NP * 16)));
-  uint32_t best_m = 1;
-  for (uint32_t m = std::min<uint32_t>(n, m_cap); m >= 1; --m) {
-    const uint64_t F = ((pl.r1 - 1) >> m) - (r0 >> m) + 1;
-    const uint64_t items = uint64_t(pl.n_ktiles) * ((F + pl.Ft - 1) / pl.Ft);
-    best_m = m;
-    if (items >= target) break;
+  pl.m = choose_m_target(pl, n, r0, 1, m_cap);
+  if (const char *e = getenv("DPF_FORCE_M")) {  // tuning override
+    const uint32_t fm = uint32_t(atoi(e));
+    if (fm >= 1 && fm <= std::min<uint32_t>(n, m_cap)) pl.m = fm;
   }
-  pl.m = best_m;
   pl.f = n - pl.m;
   pl.lo_f = r0 >> pl.m;
   pl.F = ((pl.r1 - 1) >> pl.m) - pl.lo_f + 1;
@@ -678,41 +725,23 @@ int make_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Pl
   const uint64_t items = uint64_t(pl.n_ktiles) * ((pl.F + pl.Ft - 1) / pl.Ft);
   if (items > 0x7FFFFFFFull) return DPF_EINVAL;
   pl.n_items = uint32_t(items);
-  // Window: W leaf pairs per thread; T stage = Ft*2W rows, y stage = Kt*Ft*2W.
+  // Window: W leaf pairs per thread (y stage = Kt*Ft*2W words <= 16 KB); T
+  // ring entries of CN nodes x 2W rows (<= 32 KB), NST of them.
   const uint32_t nq = 1u << (pl.m - 1);
   uint32_t W = std::min<uint32_t>(8, nq);
-  while (W > 1 && uint64_t(pl.Ft) * 2 * W * D * 4 > kMaxTStageBytes) W >>= 1;
+  while (W > 1 && uint64_t(pl.Kt) * pl.Ft * 2 * W * 4 > 16 * 1024) W >>= 1;
   const size_t stack_bytes = size_t(pl.m) * 32 * NP * 16;
   for (;; W >>= 1) {
-    pl.W = W;
-    pl.nwin = nq / W;
-    pl.y_stage_words = uint32_t(align_up(size_t(pl.Kt) * pl.Ft * 2 * W, 32));
-    // + padding: lanes whose columns exceed D read past the last row.
-    pl.t_stage_words = uint32_t(align_up(size_t(pl.Ft) * 2 * W * D + 32u * pl.kc.CPL * pl.CG, 32));
-    pl.smem_bytes = 128 + 4 * (2 * size_t(pl.y_stage_words) + 2 * size_t(pl.t_stage_words)) + stack_bytes;
-    if (pl.smem_bytes <= 227 * 1024) break;
+    if (set_windows(pl, W, D, stack_bytes)) break;
     if (W == 1) return DPF_EINVAL;
   }
+  pl.nwin = nq / pl.W;
   pl.grid = std::min<uint32_t>(pl.n_items, uint32_t(num_sms()));
   // PRF blocks: top levels (nodes intersecting the range) + fused subtrees.
   uint64_t top = 0;
   for (uint32_t k = 0; k < pl.f; ++k) top += ((pl.r1 - 1) >> (n - k)) - (r0 >> (n - k)) + 1;
   pl.prf_blocks = uint64_t(B) * top + uint64_t(pl.n_items) * pl.tasks * ((1ull << pl.m) - 1);
   return DPF_OK;
-}
-
-// Subtree depth m for a plan: the largest m <= m_cap that still gives >= 8
-// work items per SM (and >= m_min).
-uint32_t choose_m(const Plan &pl, uint32_t n, uint64_t r0, uint32_t m_min, uint32_t m_cap) {
-  const uint64_t target = 8ull * num_sms();
-  uint32_t best = m_min;
-  for (uint32_t m = std::min<uint32_t>(n, m_cap); m >= m_min; --m) {
-    const uint64_t F = ((pl.r1 - 1) >> m) - (r0 >> m) + 1;
-    const uint64_t items = uint64_t(pl.n_ktiles) * ((F + pl.Ft - 1) / pl.Ft);
-    best = m;
-    if (items >= target) break;
-  }
-  return best;
 }
 
 constexpr uint32_t kTcNP = 16;   // producer warps (4 per SMSP)
@@ -747,7 +776,7 @@ int make_tc_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D,
   const size_t fixed = 1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(kTcNSY) * pl.y_stage_bytes;
   const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / (32 * kTcNP * 16)));
   if (m_cap < 3) return DPF_EINVAL;
-  pl.m = choose_m(pl, n, r0, 3, m_cap);
+  pl.m = choose_m_target(pl, n, r0, 3, m_cap);
   pl.f = n - pl.m;
   pl.lo_f = r0 >> pl.m;
   pl.F = ((pl.r1 - 1) >> pl.m) - pl.lo_f + 1;
@@ -883,8 +912,12 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
   p.W = pl.W;
   p.CG = pl.CG;
   p.KG = pl.KG;
+  p.SG = pl.SG;
   p.y_stage_words = pl.y_stage_words;
   p.t_stage_words = pl.t_stage_words;
+  p.CN = pl.CN;
+  p.n_chunks = pl.n_chunks;
+  p.NST = pl.NST;
   if (pl.tc) {
     dev::TcParams tp;
     tp.f = p;
@@ -1241,12 +1274,9 @@ int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t
   // window: W leaf pairs must divide every group's 2^(m-1)
   uint32_t W = std::min<uint32_t>(8, 1u << (m_min_all - 1));
   const size_t stack_bytes = size_t(m_cap) * 32 * NP * 16;
+  while (W > 1 && uint64_t(pl.Kt) * pl.Ft * 2 * W * 4 > 16 * 1024) W >>= 1;
   for (;; W >>= 1) {
-    pl.W = W;
-    pl.y_stage_words = uint32_t(align_up(size_t(pl.Kt) * pl.Ft * 2 * W, 32));
-    pl.t_stage_words = uint32_t(align_up(size_t(pl.Ft) * 2 * W * D + 32u * pl.kc.CPL * pl.CG, 32));
-    pl.smem_bytes = 128 + 4 * (2 * size_t(pl.y_stage_words) + 2 * size_t(pl.t_stage_words)) + stack_bytes;
-    if (pl.smem_bytes <= 227 * 1024) break;
+    if (set_windows(pl, W, D, stack_bytes)) break;
     if (W == 1) return DPF_EINVAL;
   }
   // launch order: larger subtrees (bigger items) first
@@ -1382,8 +1412,12 @@ extern "C" int dpf_eval_grouped(const dpf_eval_group *groups, uint32_t n_groups,
   p.W = pl.W;
   p.CG = pl.CG;
   p.KG = pl.KG;
+  p.SG = pl.SG;
   p.y_stage_words = pl.y_stage_words;
   p.t_stage_words = pl.t_stage_words;
+  p.CN = pl.CN;
+  p.n_chunks = pl.n_chunks;
+  p.NST = pl.NST;
   auto kfn = prf == DPF_PRF_AES128 ? pl.kc.fn_aes : pl.kc.fn;
   if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
     return DPF_ECUDA;
