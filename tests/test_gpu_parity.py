@@ -291,3 +291,22 @@ def test_grouped_equals_per_group_and_oracle(dp, oracle, prf):
     for (wire, n, Td, r0, out), want in zip(groups, expect):
         np.testing.assert_array_equal(dp.as_u32(out), want)
         np.testing.assert_array_equal(dp.as_u32(dp.eval_batch_wire(wire, n, Td, r0, prf=prf)), want)
+
+
+def test_deep_domains_small_shards(dp, oracle):
+    """log_n up to 32 with a small shard anywhere in the domain: the top BFS
+    descends the path to the shard (SMEM levels + grid-wide levels)."""
+    D, B = 16, 6
+    for n, r0, rows in ((28, (1 << 27) + 12345, 3000), (32, (1 << 32) - 4096, 4096), (24, 0, 1000),
+                        (31, 1 << 30, 2048)):
+        T = synth.table(rows, D, n)
+        al = [r0 + (i * 997) % rows for i in range(B)]
+        pairs = [dp.gen(n, a, 1, s) for a, s in zip(al, synth.gen_seeds(B, n))]
+        Td = to_dev(T)
+        s0 = dp.as_u32(dp.eval_batch_shard([p[0] for p in pairs], Td, r0))
+        s1 = dp.as_u32(dp.eval_batch_shard([p[1] for p in pairs], Td, r0))
+        np.testing.assert_array_equal(dp.reconstruct(s0, s1), T[[a - r0 for a in al]])
+        # spot-check one key against the oracle's point evaluations over the shard
+        ok = oracle.key_from_wire(dp.key_serialize(pairs[0][0]))
+        y = np.array([oracle.eval_point(ok, r0 + j) for j in range(rows)], np.uint32)
+        np.testing.assert_array_equal(s0[0], oracle.contract(y, T))
