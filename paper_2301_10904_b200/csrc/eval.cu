@@ -427,6 +427,23 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
           if (tuse > 0) mbar_wait(&tempty[ts], (tuse - 1) & 1);
           uint32_t *tb = tbuf + ts * p.t_stage_words;
           const uint32_t n0 = ch * p.CN, n1 = min(p.Ft, n0 + p.CN);
+          if (g.nwin == 1) {
+            // one window covers whole subtrees: the chunk's rows are contiguous
+            // in the table -> a single bulk copy (small key tiles stream the
+            // table, and per-node copies of a few KB starve the TMA unit)
+            const uint64_t nb = uint64_t(ng) * p.Ft;
+            const uint64_t nend = min(uint64_t(n1) + nb, g.F);
+            const uint64_t s0 = (g.lo_f + nb + n0) << g.m;
+            const uint64_t s1 = nend > nb + n0 ? (g.lo_f + nend) << g.m : s0;
+            const uint64_t a = s0 > g.r0 ? s0 : g.r0, e = s1 < g.r1 ? s1 : g.r1;
+            const uint32_t bytes = a < e ? uint32_t(e - a) * row_bytes : 0u;
+            if (lane == 0) {
+              mbar_arrive_expect_tx(&tfull[ts], bytes);
+              if (bytes) bulk_g2s(tb + (a - s0) * p.D, g.T + (a - g.r0) * p.D, bytes, &tfull[ts]);
+            }
+            __syncwarp();
+            continue;
+          }
           uint32_t my_bytes = 0;
           for (uint32_t nl = n0 + lane; nl < n1; nl += 32) {
             const uint64_t node = uint64_t(ng) * p.Ft + nl;
