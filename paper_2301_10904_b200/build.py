@@ -18,7 +18,8 @@ CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(PKG, "libdpfpir.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("host.cc", "eval.cu")]
-HEADERS = [os.path.join(CSRC, "chacha_dev.cuh"), os.path.join(INCLUDE, "dpfpir.h")]
+HEADERS = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))) + [
+    os.path.join(INCLUDE, "dpfpir.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
