@@ -24,6 +24,12 @@
  * sizes; numpy uint32 matmul for the contraction; naive PIR
  * (P:293-294); reconstruction = beta * T[alpha]; shard linearity
  * (P:536-540).
+ *
+ * SURVEY 8(f) row f4 (prf 3, reading R20): early-terminated leaves -- pinned
+ * by the same DPF contract (exhaustive at small n), Convert == the library
+ * ChaCha20 keystream block 1, block counts 2^(h+1)-1 / h+1 / 2h+2, key size
+ * 32 + 64 (log_n - 3), and tree columns identical to a depth-h ChaCha20 key
+ * drawn from the same DRBG seed.
  */
 #include <stdint.h>
 #include <stdlib.h>
@@ -172,6 +178,14 @@ void oracle_aes128_encrypt(const uint8_t key[16], const uint8_t in[16], uint8_t 
 
 #define ORACLE_PRF_CHACHA20 1
 #define ORACLE_PRF_AES128 2
+/* SURVEY 8(f) row f4, reading R20: the ChaCha20 tree with early-terminated
+ * leaves.  The GGM tree stops ET_BITS = 4 levels early (tree depth
+ * h = log_n - 4); each final node s yields the 16 leaves 16i..16i+15 from the
+ * 16 words of ONE ChaCha20 block, Convert(s) (below), corrected by a 16-word
+ * leaf codeword.  Levels 1..h follow Eq. 3 exactly as for ChaCha20. */
+#define ORACLE_PRF_CHACHA20_ET 3
+#define ORACLE_ET_BITS 4
+#define ORACLE_ET_LEAVES 16
 
 /* Reading R8 (AES): PRF_s(c) = AES-128 with key s on the block 0^120 || c
  * (big-endian counter, SP 800-38A CTR); one key schedule, two encryptions
@@ -197,11 +211,29 @@ static void prf_both_chacha(const uint8_t s[16], uint8_t child0[16], uint8_t chi
 }
 
 static void prf_both(uint32_t prf, const uint8_t s[16], uint8_t child0[16], uint8_t child1[16], uint64_t *blocks) {
+    /* ORACLE_PRF_CHACHA20_ET expands its tree levels with ChaCha20 (R20) */
     if (prf == ORACLE_PRF_AES128)
         prf_both_aes(s, child0, child1, blocks);
     else
         prf_both_chacha(s, child0, child1, blocks);
 }
+
+/* R20: Convert(s) = the 16 little-endian words of the ChaCha20 block keyed by
+ * s || 0^128 with counter 1 and nonce 0 (block 1 of the same keystream whose
+ * block 0 is the tree PRF: a final node is never expanded, and the distinct
+ * counter keeps conversion and expansion outputs apart). */
+static void convert_chacha(const uint8_t s[16], uint32_t w[ORACLE_ET_LEAVES], uint64_t *blocks) {
+    uint8_t key[32], nonce[12], ks[64];
+    int i;
+    memset(key, 0, sizeof key);
+    memcpy(key, s, 16);
+    memset(nonce, 0, sizeof nonce);
+    oracle_chacha20_block(key, 1u, nonce, ks);
+    for (i = 0; i < ORACLE_ET_LEAVES; i++) w[i] = load_le32(ks + 4 * i);
+    if (blocks) *blocks += 1;
+}
+
+void oracle_convert(const uint8_t s[16], uint32_t w[ORACLE_ET_LEAVES]) { convert_chacha(s, w, NULL); }
 
 void oracle_prf(const uint8_t s[16], uint32_t c, uint8_t out[16]) {
     uint8_t c0[16], c1[16];
@@ -246,7 +278,14 @@ typedef struct {
     uint32_t prf;  /* 1 = ChaCha20, 2 = AES-128 */
     uint8_t root[16];
     uint8_t cw[ORACLE_MAX_LOG_N][2][2][16];
+    uint32_t cw_leaf[ORACLE_ET_LEAVES]; /* R20 (prf 3 only): leaf correction words CWL[0..15] */
 } oracle_key;
+
+/* Depth of the GGM tree: log_n levels, or log_n - ET_BITS with early
+ * termination (R20). */
+static uint32_t tree_depth(uint32_t prf, uint32_t log_n) {
+    return prf == ORACLE_PRF_CHACHA20_ET ? log_n - ORACLE_ET_BITS : log_n;
+}
 
 size_t oracle_key_struct_size(void) { return sizeof(oracle_key); }
 
@@ -296,6 +335,11 @@ static void drbg_bytes(drbg *g, uint8_t *out, int n) {
 /*  3. cw_out = (-1)^{lsb(s_1)} (beta - w1(s_0) + w1(s_1))  mod 2^32.         */
 /* Draw order: r0, r1, then C_0[0][d], C_0[1][d] for d = 1..n.               */
 /* Returns 0, or -1 on invalid arguments.  *blocks += 2n.                    */
+/* Early termination (R20, prf 3, 5 <= log_n <= 32): step 2 runs for         */
+/* d = 1..h = log_n - 4 only (same bits of alpha, MSB first); then with      */
+/* W_x = Convert(s_x) and a = alpha mod 16, for k = 0..15:                   */
+/*  3'. CWL[k] = (-1)^{lsb(s_1)} (beta [k = a] - W_0[k] + W_1[k])  mod 2^32, */
+/*     cw_out = 0.  *blocks += 2h + 2.                                       */
 /* ------------------------------------------------------------------------ */
 
 int oracle_gen_prf(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t prf, const uint8_t rng_seed[32],
@@ -304,7 +348,8 @@ int oracle_gen_prf(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t prf, 
     uint8_t s0[16], s1[16], p0[2][16], p1[2][16], delta[2][16];
     uint32_t d, n = log_n;
     if (log_n < 1 || log_n > ORACLE_MAX_LOG_N || !k0 || !k1 || !rng_seed) return -1;
-    if (prf != ORACLE_PRF_CHACHA20 && prf != ORACLE_PRF_AES128) return -1;
+    if (prf != ORACLE_PRF_CHACHA20 && prf != ORACLE_PRF_AES128 && prf != ORACLE_PRF_CHACHA20_ET) return -1;
+    if (prf == ORACLE_PRF_CHACHA20_ET && log_n <= ORACLE_ET_BITS) return -1;
     if (log_n < 64 && alpha >= ((uint64_t)1 << log_n)) return -1;
     memset(k0, 0, sizeof *k0);
     memset(k1, 0, sizeof *k1);
@@ -319,7 +364,7 @@ int oracle_gen_prf(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t prf, 
     k0->prf = k1->prf = prf;
     k0->party = 0;
     k1->party = 1;
-    for (d = 1; d <= n; d++) {
+    for (d = 1; d <= tree_depth(prf, n); d++) {
         uint32_t keep = (uint32_t)((alpha >> (n - d)) & 1u), lose = 1u - keep, c;
         uint32_t t0 = lsb_of(s0), t1 = lsb_of(s1);
         uint8_t c0cw[2][16], c1cw[2][16], next0[16], next1[16];
@@ -342,6 +387,17 @@ int oracle_gen_prf(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t prf, 
         memcpy(s1, next1, 16);
     }
     memcpy(k1->cw, k0->cw, sizeof k0->cw);
+    if (prf == ORACLE_PRF_CHACHA20_ET) {
+        uint32_t w0[ORACLE_ET_LEAVES], w1[ORACLE_ET_LEAVES], kk;
+        convert_chacha(s0, w0, blocks);
+        convert_chacha(s1, w1, blocks);
+        for (kk = 0; kk < ORACLE_ET_LEAVES; kk++) {
+            uint32_t v = (kk == (uint32_t)(alpha % ORACLE_ET_LEAVES) ? beta : 0u) - w0[kk] + w1[kk];
+            k0->cw_leaf[kk] = k1->cw_leaf[kk] = lsb_of(s1) ? (0u - v) : v;
+        }
+        k0->cw_out = k1->cw_out = 0;
+        return 0;
+    }
     {
         uint32_t v = beta - w1_of(s0) + w1_of(s1);
         k0->cw_out = k1->cw_out = lsb_of(s1) ? (0u - v) : v;
@@ -375,24 +431,35 @@ static uint32_t leaf_value(const oracle_key *k, const uint8_t s[16]) {
     return k->party ? (0u - v) : v;
 }
 
+/* R20 leaf conversion with early termination: final node s (depth h) holds
+ * leaves 16i..16i+15; leaf 16i + kk gets
+ *   y = (-1)^party (W[kk] + lsb(s) CWL[kk]),  W = Convert(s)  (one block). */
+static uint32_t et_leaf_value(const oracle_key *k, const uint8_t s[16], uint32_t kk, uint64_t *blocks) {
+    uint32_t w[ORACLE_ET_LEAVES], v;
+    convert_chacha(s, w, blocks);
+    v = w[kk] + lsb_of(s) * k->cw_leaf[kk];
+    return k->party ? (0u - v) : v;
+}
+
 /* O3. Eval(k, j) = P(log L, j)  (Eq. 1): root, then n node steps
  * along the bits of j.  Exactly n PRF blocks. */
 uint32_t oracle_eval_point(const oracle_key *k, uint64_t j, uint64_t *blocks) {
     uint8_t s[16], ch0[16], ch1[16];
     uint32_t d, n = k->log_n;
     memcpy(s, k->root, 16);
-    for (d = 1; d <= n; d++) {
+    for (d = 1; d <= tree_depth(k->prf, n); d++) {
         uint32_t bit = (uint32_t)((j >> (n - d)) & 1u);
         node_children(k, s, d, ch0, ch1, blocks);
         memcpy(s, bit ? ch1 : ch0, 16);
     }
+    if (k->prf == ORACLE_PRF_CHACHA20_ET) return et_leaf_value(k, s, (uint32_t)(j % ORACLE_ET_LEAVES), blocks);
     return leaf_value(k, s);
 }
 
 /* O4. Full-domain expansion in level order ("level-by-level"): all
  * 2^n leaf seeds, N-1 blocks.  leaf_seeds is caller-owned 16 * 2^n bytes. */
 static int expand_all(const oracle_key *k, uint8_t *seeds, uint64_t *blocks) {
-    uint32_t d, n = k->log_n;
+    uint32_t d, n = tree_depth(k->prf, k->log_n); /* R20: final nodes at depth h */
     uint64_t i, width;
     memcpy(seeds, k->root, 16);
     for (d = 1; d <= n; d++) {
@@ -410,7 +477,7 @@ static int expand_all(const oracle_key *k, uint8_t *seeds, uint64_t *blocks) {
 }
 
 int oracle_eval_full_seeds(const oracle_key *k, uint8_t *leaf_seeds, uint64_t *blocks) {
-    if (!k || !leaf_seeds || k->log_n < 1 || k->log_n > 30) return -1;
+    if (!k || !leaf_seeds || k->log_n < 1 || k->log_n > 30 || k->prf == ORACLE_PRF_CHACHA20_ET) return -1;
     return expand_all(k, leaf_seeds, blocks);
 }
 
@@ -423,7 +490,22 @@ int oracle_eval_full(const oracle_key *k, uint32_t *y, uint64_t *blocks) {
     seeds = (uint8_t *)malloc((size_t)(16 * N));
     if (!seeds) return -3;
     expand_all(k, seeds, blocks);
-    for (j = 0; j < N; j++) y[j] = leaf_value(k, seeds + 16 * j);
+    if (k->prf == ORACLE_PRF_CHACHA20_ET) {
+        /* R20: 2^h final nodes, one Convert block each -> 16 leaves */
+        uint64_t i;
+        uint32_t kk;
+        for (i = 0; i < (N >> ORACLE_ET_BITS); i++) {
+            uint32_t w[ORACLE_ET_LEAVES];
+            const uint8_t *sf = seeds + 16 * i;
+            convert_chacha(sf, w, blocks);
+            for (kk = 0; kk < ORACLE_ET_LEAVES; kk++) {
+                uint32_t v = w[kk] + lsb_of(sf) * k->cw_leaf[kk];
+                y[i * ORACLE_ET_LEAVES + kk] = k->party ? (0u - v) : v;
+            }
+        }
+    } else {
+        for (j = 0; j < N; j++) y[j] = leaf_value(k, seeds + 16 * j);
+    }
     free(seeds);
     return 0;
 }
@@ -536,34 +618,48 @@ void oracle_naive_pir_shares(uint64_t N, uint64_t alpha, uint32_t beta, const ui
 
 size_t oracle_key_wire_size(uint32_t log_n) { return 32u + 64u * (size_t)log_n; }
 
+/* R20 (prf 3): the h = log_n - 4 codeword columns, then CWL[0..15] as 16 LE
+ * words (64 bytes): 32 + 64 (log_n - 3) bytes. */
+size_t oracle_key_wire_size_prf(uint32_t log_n, uint32_t prf) {
+    if (prf == ORACLE_PRF_CHACHA20_ET) return 32u + 64u * (size_t)(log_n - ORACLE_ET_BITS) + 64u;
+    return oracle_key_wire_size(log_n);
+}
+
 int oracle_key_to_wire(const oracle_key *k, uint8_t *out, size_t cap) {
-    uint32_t d, t, c;
-    size_t need = oracle_key_wire_size(k->log_n);
+    uint32_t d, t, c, h = tree_depth(k->prf, k->log_n);
+    size_t need = oracle_key_wire_size_prf(k->log_n, k->prf);
     if (cap < need) return -1;
     store_le32(out, 0x4B465044u);
     out[4] = 1; out[5] = (uint8_t)k->prf; out[6] = (uint8_t)k->party; out[7] = (uint8_t)k->log_n;
     store_le32(out + 8, k->cw_out);
     store_le32(out + 12, 0);
     memcpy(out + 16, k->root, 16);
-    for (d = 0; d < k->log_n; d++)
+    for (d = 0; d < h; d++)
         for (t = 0; t < 2; t++)
             for (c = 0; c < 2; c++) memcpy(out + 32 + 64 * d + 32 * t + 16 * c, k->cw[d][t][c], 16);
+    if (k->prf == ORACLE_PRF_CHACHA20_ET)
+        for (c = 0; c < ORACLE_ET_LEAVES; c++) store_le32(out + 32 + 64 * h + 4 * c, k->cw_leaf[c]);
     return (int)need;
 }
 
 int oracle_key_from_wire(const uint8_t *in, size_t len, oracle_key *k) {
-    uint32_t d, t, c, n;
-    if (len < 32 || load_le32(in) != 0x4B465044u || in[4] != 1 || (in[5] != 1 && in[5] != 2)) return -2;
+    uint32_t d, t, c, n, h;
+    if (len < 32 || load_le32(in) != 0x4B465044u || in[4] != 1 || in[5] < 1 || in[5] > 3) return -2;
     n = in[7];
-    if (n < 1 || n > ORACLE_MAX_LOG_N || len != oracle_key_wire_size(n) || in[6] > 1) return -2;
+    if (n < 1 || n > ORACLE_MAX_LOG_N || in[6] > 1) return -2;
+    if (in[5] == ORACLE_PRF_CHACHA20_ET && n <= ORACLE_ET_BITS) return -2;
+    if (len != oracle_key_wire_size_prf(n, in[5])) return -2;
+    h = tree_depth(in[5], n);
     memset(k, 0, sizeof *k);
     k->log_n = n;
     k->prf = in[5];
     k->party = in[6];
     k->cw_out = load_le32(in + 8);
     memcpy(k->root, in + 16, 16);
-    for (d = 0; d < n; d++)
+    for (d = 0; d < h; d++)
         for (t = 0; t < 2; t++)
             for (c = 0; c < 2; c++) memcpy(k->cw[d][t][c], in + 32 + 64 * d + 32 * t + 16 * c, 16);
+    if (k->prf == ORACLE_PRF_CHACHA20_ET)
+        for (c = 0; c < ORACLE_ET_LEAVES; c++) k->cw_leaf[c] = load_le32(in + 32 + 64 * h + 4 * c);
     return 0;
 }

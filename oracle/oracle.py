@@ -33,7 +33,8 @@ def build(force: bool = False) -> str:
 
 class OracleKey(ctypes.Structure):
     _fields_ = [("log_n", ctypes.c_uint32), ("party", ctypes.c_uint32), ("cw_out", ctypes.c_uint32),
-                ("prf", ctypes.c_uint32), ("root", ctypes.c_uint8 * 16), ("cw", ctypes.c_uint8 * (MAX_LOG_N * 2 * 2 * 16))]
+                ("prf", ctypes.c_uint32), ("root", ctypes.c_uint8 * 16), ("cw", ctypes.c_uint8 * (MAX_LOG_N * 2 * 2 * 16)),
+                ("cw_leaf", ctypes.c_uint32 * 16)]
 
 
 _lib = None
@@ -69,6 +70,9 @@ def lib():
         L.oracle_naive_pir_shares.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint32, u32p, u32p]
         L.oracle_key_wire_size.argtypes = [ctypes.c_uint32]
         L.oracle_key_wire_size.restype = ctypes.c_size_t
+        L.oracle_key_wire_size_prf.argtypes = [ctypes.c_uint32, ctypes.c_uint32]
+        L.oracle_key_wire_size_prf.restype = ctypes.c_size_t
+        L.oracle_convert.argtypes = [u8p, u32p]
         L.oracle_key_to_wire.argtypes = [kp, u8p, ctypes.c_size_t]
         L.oracle_key_from_wire.argtypes = [u8p, ctypes.c_size_t, kp]
         assert L.oracle_key_struct_size() == ctypes.sizeof(OracleKey)
@@ -99,6 +103,16 @@ def chacha20_block(key: bytes, counter: int, nonce: bytes) -> bytes:
 
 
 PRF_CHACHA20, PRF_AES128 = 1, 2
+# R20 / SURVEY 8(f) f4: ChaCha20 tree with early-terminated leaves (16 per final node)
+PRF_CHACHA20_ET = 3
+ET_BITS = 4
+
+
+def convert(seed: bytes) -> np.ndarray:
+    """R20 Convert(s): the 16 LE words of ChaCha20(key = s || 0^128, counter 1, nonce 0)."""
+    w = np.zeros(16, np.uint32)
+    lib().oracle_convert(_u8(_bytes_in(seed)), _u32(w))
+    return w
 
 
 def aes128_encrypt(key: bytes, block: bytes) -> bytes:
@@ -196,12 +210,12 @@ def naive_pir_shares(N: int, alpha: int, beta: int, r0: np.ndarray) -> np.ndarra
     return r1
 
 
-def key_wire_size(log_n: int) -> int:
-    return lib().oracle_key_wire_size(log_n)
+def key_wire_size(log_n: int, prf: int = PRF_CHACHA20) -> int:
+    return lib().oracle_key_wire_size_prf(log_n, prf)
 
 
 def key_to_wire(k: OracleKey) -> bytes:
-    out = np.zeros(key_wire_size(k.log_n), np.uint8)
+    out = np.zeros(key_wire_size(k.log_n, k.prf), np.uint8)
     n = lib().oracle_key_to_wire(ctypes.byref(k), _u8(out), out.size)
     assert n == out.size
     return out.tobytes()
