@@ -44,7 +44,18 @@ extern "C" {
  * PRF) or AES-128 (the paper's baseline PRF, Table 4), both table-free
  * on the device (AES bitsliced).  PRF_s(c): ChaCha20 keyed by s || 0^128,
  * bytes [16c, 16c+16) of block 0; AES-128 keyed by s on block 0^120 || c. */
-enum dpf_prf { DPF_PRF_CHACHA20 = 1, DPF_PRF_AES128 = 2 };
+enum dpf_prf { DPF_PRF_CHACHA20 = 1, DPF_PRF_AES128 = 2, DPF_PRF_CHACHA20_ET = 3 };
+
+/* DPF_PRF_CHACHA20_ET (reading R20): the
+ * ChaCha20 tree with early-terminated leaves.  Requires 5 <= log_n <= 32.
+ * The tree of Eq. 3 runs to depth h = log_n - 4 only; final node i holds the
+ * 16 rows 16i..16i+15, whose leaf shares come from ONE ChaCha20 block
+ * Convert(s) (key s || 0^128, counter 1, nonce 0: 16 LE words W[0..15]):
+ *   Eval(k, 16i + c) = (-1)^party (W[c] + lsb(s) * CWL[c])  mod 2^32.
+ * 2^(h+1) - 1 = N/8 - 1 blocks per key instead of N - 1.  Not the paper's
+ * key format (Table 4's 64 log2 L bytes): the key carries h codeword columns
+ * plus the 16-word leaf codeword CWL (32 + 64 (log_n - 3) wire bytes). */
+#define DPF_ET_BITS 4
 
 enum dpf_status {
   DPF_OK = 0,
@@ -59,6 +70,8 @@ enum dpf_status {
  * P(0,0) = C_0[0,0]).  Reading R3: the root (column 0) is stored separately
  * and is party-specific; columns d = 1..log_n are cw[d-1][t][c] = C_t[c, d],
  * shared by both parties (R4).  cw_out is the final Z_2^32 correction (R7).
+ * DPF_PRF_CHACHA20_ET (R20): columns d = 1..h = log_n - 4 as above; cw[h]
+ * (the next 64 bytes) holds CWL[0..15] as 16 little-endian u32; cw_out = 0.
  * POD, fixed size, caller-owned.  Invariant: lsb(root[0]) == party. */
 typedef struct dpf_key {
   uint32_t magic;        /* DPF_KEY_MAGIC */
@@ -79,9 +92,9 @@ typedef struct dpf_key {
  * j < 2^log_n: Eval(k0,j) + Eval(k1,j) = beta if j == alpha else 0 (mod 2^32).
  * rng_seed: 32 bytes keying the ChaCha20 DRBG that draws the roots and
  * codewords (deterministic for tests); NULL draws the seed from getrandom().
- * Cost: 2*log_n ChaCha20 blocks.  Errors: DPF_EINVAL if log_n not in
- * [1, 32], alpha >= 2^log_n, k0/k1 NULL; DPF_EUNSUPPORTED if prf is not
- * DPF_PRF_CHACHA20 or DPF_PRF_AES128. */
+ * Cost: 2*log_n ChaCha20 blocks (ET: 2h + 2).  Errors: DPF_EINVAL if log_n
+ * not in [1, 32] ([5, 32] for DPF_PRF_CHACHA20_ET), alpha >= 2^log_n, k0/k1
+ * NULL; DPF_EUNSUPPORTED if prf is not one of enum dpf_prf. */
 int dpf_gen(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t prf, const uint8_t *rng_seed,
             dpf_key *k0, dpf_key *k1);
 
@@ -90,16 +103,23 @@ int dpf_gen(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t prf, const u
  * entries).  Returns 0 if log_n is out of range. */
 size_t dpf_key_wire_size(uint32_t log_n);
 
+/* Wire size for a given scheme: dpf_key_wire_size(log_n) for ChaCha20 and
+ * AES-128; 32 + 64 (log_n - 3) for DPF_PRF_CHACHA20_ET (h codeword columns +
+ * the 64-byte CWL).  0 if (log_n, prf) is invalid. */
+size_t dpf_key_wire_size_prf(uint32_t log_n, uint32_t prf);
+
 /* Serialize k into out[0..cap).  Wire format:
  * magic u32 | version u8 | prf u8 | party u8 | log_n u8 | cw_out u32 |
  * reserved u32 | root[16] | for d=1..n: cw[d-1][0][0], cw[d-1][0][1],
- * cw[d-1][1][0], cw[d-1][1][1] (16 B each).  *written (optional) receives
- * the byte count.  Errors: DPF_EINVAL (NULL, cap too small), DPF_EKEY. */
+ * cw[d-1][1][0], cw[d-1][1][1] (16 B each).  ET keys: d = 1..h, then CWL
+ * (64 B).  *written (optional) receives the byte count
+ * (dpf_key_wire_size_prf).  Errors: DPF_EINVAL (NULL, cap too small),
+ * DPF_EKEY. */
 int dpf_key_serialize(const dpf_key *k, uint8_t *out, size_t cap, size_t *written);
 
 /* Parse a wire key.  Errors: DPF_EINVAL (NULL), DPF_EKEY (bad magic/version/
- * prf/party, log_n out of range, len != dpf_key_wire_size(log_n),
- * lsb(root) != party, reserved != 0). */
+ * prf/party, log_n out of range, len != dpf_key_wire_size_prf(log_n, prf),
+ * lsb(root) != party, reserved != 0, ET key with cw_out != 0). */
 int dpf_key_deserialize(const uint8_t *in, size_t len, dpf_key *k);
 
 /* Client-side reconstruction: out[i] = share0[i] + share1[i] mod 2^32.
@@ -145,7 +165,7 @@ int dpf_eval_batch_shard(const dpf_key *keys, uint32_t B, const uint32_t *table_
  * on the device as consecutive wire-format records (dpf_key_serialize
  * output, stride dpf_key_wire_size(log_n) bytes, 16-byte aligned base),
  * e.g. received by the server straight into HBM; `prf` (enum dpf_prf) must be
- * the keys' PRF.  The keys are NOT re-validated (device memory is not read by
+ * the keys' PRF (stride dpf_key_wire_size_prf(log_n, prf) for ET keys).  The keys are NOT re-validated (device memory is not read by
  * the host): callers validate at dpf_key_deserialize time.  No host->device
  * traffic; fully asynchronous (AES keys are bitsliced into a private copy in
  * the workspace). */
@@ -246,6 +266,14 @@ typedef struct dpf_eval_stats {
   uint32_t grid;          /* fused-kernel CTAs */
 } dpf_eval_stats;
 int dpf_last_eval_stats(dpf_eval_stats *out);
+
+/* Host-only launch planning (no device calls): the plan dpf_eval_batch_shard
+ * (packed = 0) or dpf_eval_batch_packed (packed = 1) would use for B keys of
+ * scheme `prf` over rows [row_begin, row_begin + row_count) of D words; fills
+ * *out like dpf_last_eval_stats (kernels = 0).  Errors: DPF_EINVAL (invalid
+ * shape or no plan), DPF_EUNSUPPORTED (prf). */
+int dpf_eval_plan(uint32_t B, uint32_t log_n, uint32_t prf, uint64_t row_begin, uint64_t row_count, uint32_t D,
+                  int packed, dpf_eval_stats *out);
 
 /* Optional instrumentation (used by bench.py): after dpf_kernel_timer_begin(C)
  * each of the next C evaluations on this thread records a CUDA event pair on

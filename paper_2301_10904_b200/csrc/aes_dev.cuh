@@ -172,6 +172,7 @@ __device__ __forceinline__ uint32_t bs_word1(uint4 s) {
 
 struct PrfAesBs {
   static constexpr uint32_t id = 2;  // DPF_PRF_AES128
+  static constexpr bool kEt = false;
   static __device__ __forceinline__ void children(const uint4 s, uint4 &c0, uint4 &c1) { aes_children_bs(s, c0, c1); }
   static __device__ __forceinline__ uint32_t word1(const uint4 s) { return bs_word1(s); }
 };

@@ -38,6 +38,24 @@ __device__ __forceinline__ void chacha_children(const uint4 s, uint4 &c0, uint4 
   c0 = make_uint4(x0 + 0x61707865u, x1 + 0x3320646eu, x2 + 0x79622d32u, x3 + 0x6b206574u);
   c1 = make_uint4(x4 + s.x, x5 + s.y, x6 + s.z, x7 + s.w);
 }
+
+// R20 (early-terminated leaves, f4): Convert(s) = all 16 words of the
+// ChaCha20 block keyed by s || 0^128 with counter 1, nonce 0 (full
+// feed-forward).  Same 640 ALU-pipe ops as an expansion block.
+__device__ __forceinline__ void chacha_convert16(const uint4 s, uint32_t (&o)[16]) {
+  uint32_t x0 = 0x61707865u, x1 = 0x3320646eu, x2 = 0x79622d32u, x3 = 0x6b206574u;
+  uint32_t x4 = s.x, x5 = s.y, x6 = s.z, x7 = s.w;
+  uint32_t x8 = 0, x9 = 0, x10 = 0, x11 = 0, x12 = 1, x13 = 0, x14 = 0, x15 = 0;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    DPF_QR(x0, x4, x8, x12) DPF_QR(x1, x5, x9, x13) DPF_QR(x2, x6, x10, x14) DPF_QR(x3, x7, x11, x15)
+    DPF_QR(x0, x5, x10, x15) DPF_QR(x1, x6, x11, x12) DPF_QR(x2, x7, x8, x13) DPF_QR(x3, x4, x9, x14)
+  }
+  o[0] = x0 + 0x61707865u; o[1] = x1 + 0x3320646eu; o[2] = x2 + 0x79622d32u; o[3] = x3 + 0x6b206574u;
+  o[4] = x4 + s.x; o[5] = x5 + s.y; o[6] = x6 + s.z; o[7] = x7 + s.w;
+  o[8] = x8; o[9] = x9; o[10] = x10; o[11] = x11;
+  o[12] = x12 + 1u; o[13] = x13; o[14] = x14; o[15] = x15;
+}
 #undef DPF_QR
 
 __device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
@@ -46,10 +64,20 @@ __device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
 
 // PRF policies.  ChaCha20 works on plain seeds; AES-128 (aes_dev.cuh) on
 // bitsliced seeds.  Both keep lsb(s) (R5) at bit 0 of word 0.
+// kEt: early-terminated leaves (R20): the tree stops kEtBits levels above the
+// rows and each final node yields 2^kEtBits leaves from one Convert block.
 struct PrfChacha {
   static constexpr uint32_t id = 1;  // DPF_PRF_CHACHA20
+  static constexpr bool kEt = false;
   static __device__ __forceinline__ void children(const uint4 s, uint4 &c0, uint4 &c1) { chacha_children(s, c0, c1); }
   static __device__ __forceinline__ uint32_t word1(const uint4 s) { return s.y; }  // bytes 4..7 (R6)
+};
+struct PrfChachaEt {
+  static constexpr uint32_t id = 3;  // DPF_PRF_CHACHA20_ET
+  static constexpr bool kEt = true;
+  static constexpr uint32_t kEtBits = 4;
+  static __device__ __forceinline__ void children(const uint4 s, uint4 &c0, uint4 &c1) { chacha_children(s, c0, c1); }
+  static __device__ __forceinline__ uint32_t word1(const uint4 s) { return s.y; }  // unused (no per-seed leaves)
 };
 
 // Eq. 3 for both children of node s at depth d-1:
@@ -72,6 +100,24 @@ __device__ __forceinline__ void node_children(const uint4 s, const uint4 *__rest
 template <class Prf>
 __device__ __forceinline__ uint32_t leaf_value(const uint4 s, uint32_t cw_out) {
   return Prf::word1(s) + ((s.x & 1u) ? cw_out : 0u);
+}
+
+// R20 leaf conversion of a final node s, before the party sign:
+// y[c] = Convert(s)[c] + lsb(s) * CWL[c]  (16 leaves 16i..16i+15).
+__device__ __forceinline__ void leaf_values16(const uint4 s, const uint32_t (&cwl)[16], uint32_t (&y)[16]) {
+  chacha_convert16(s, y);
+  const uint32_t t = s.x & 1u;
+#pragma unroll
+  for (int c = 0; c < 16; ++c) y[c] += t * cwl[c];
+}
+
+// CWL of a wire key: the 16 LE words in the column after tree level h.
+__device__ __forceinline__ void load_cwl(const uint4 *__restrict__ col, uint32_t (&cwl)[16]) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint4 v = __ldg(col + i);
+    cwl[4 * i] = v.x; cwl[4 * i + 1] = v.y; cwl[4 * i + 2] = v.z; cwl[4 * i + 3] = v.w;
+  }
 }
 
 }  // namespace dev

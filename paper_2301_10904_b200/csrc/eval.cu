@@ -218,7 +218,8 @@ struct FusedParams {
   const GroupDesc *groups;   // device array when n_groups > 1 (sorted by item_base)
   uint32_t n_groups, n_items, D;
   uint32_t Kt, Ft, tasks;  // tasks = Kt * Ft <= 32 * NP (lanes >= tasks idle)
-  uint32_t W;              // leaf pairs per producer thread per window
+  uint32_t W;              // units per producer thread per window (unit: a leaf pair; ET: a final node)
+  uint32_t R;              // table rows per node per window: 2W, or 16W with early termination (R20)
   uint32_t CG, KG, SG;     // consumer col groups / key groups / slot groups
   uint32_t y_stage_words, t_stage_words;  // t: one T-ring entry (CN nodes x 2W rows x D + pad)
   uint32_t CN, n_chunks, NST;             // IMAD kernel: nodes per T entry, entries per window, ring depth
@@ -320,9 +321,59 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
       const uint8_t *key = g.keys + uint64_t(valid ? b : 0) * g.kstride;
       const uint32_t cw_out = key_cw_out(key);
       uint4 cur = valid ? g.frontier[uint64_t(b) * g.cap + node] : make_uint4(0, 0, 0, 0);
-      const uint64_t row_base = (g.lo_f + node) << g.m;
-      const bool inside = valid && row_base >= g.r0 && row_base + (1ull << g.m) <= g.r1;
+      constexpr uint32_t V = Prf::kEt ? 4u : 0u;  // log2(rows per subtree leaf)
+      const uint64_t row_base = (g.lo_f + node) << (g.m + V);
+      const bool inside = valid && row_base >= g.r0 && row_base + (1ull << (g.m + V)) <= g.r1;
       uint32_t dep = 0;
+      if constexpr (Prf::kEt) {
+        // R20: units are final nodes (16 rows each, one Convert block); the
+        // leaf-parent expansion at even units yields both, the right one waits
+        uint32_t cwl[16];
+        load_cwl(key_cw(key, g.n + 1), cwl);
+        uint4 pend = make_uint4(0, 0, 0, 0);
+        const uint32_t npairs = 1u << (g.m - 1);
+        for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
+          const uint32_t stage = wseq & 1, use = wseq >> 1;
+          if (use > 0) named_sync(3 + stage, kEmptyThreads);
+          uint32_t *yb = ybuf + stage * p.y_stage_words;
+          for (uint32_t qi = 0; qi < p.W; ++qi) {
+            const uint32_t q = win * p.W + qi;
+            uint4 sf;
+            if ((q & 1) == 0) {
+              while (dep + 1 < g.m) {
+                uint4 c0, c1;
+                node_children<Prf>(cur, key_cw(key, g.n - g.m + dep + 1), c0, c1);
+                stack[(dep + 1) * (32 * NP) + tix] = c1;
+                cur = c0;
+                ++dep;
+              }
+              node_children<Prf>(cur, key_cw(key, g.n), sf, pend);
+            } else {
+              sf = pend;
+            }
+            uint32_t y[16];
+            leaf_values16(sf, cwl, y);
+            if (!inside) {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                const uint64_t row = row_base + 16ull * q + c;
+                y[c] = (valid && row >= g.r0 && row < g.r1) ? y[c] : 0u;
+              }
+            }
+            if (lane_on) {
+              const uint32_t slot = nl * p.R + 16 * qi;
+#pragma unroll
+              for (int c = 0; c < 16; ++c) yb[(slot + c) * p.Kt + kl] = y[c];
+            }
+            if ((q & 1) && (q >> 1) + 1 < npairs) {  // pop for the next leaf-parent
+              const uint32_t k = g.m - 1 - (__ffs((q >> 1) + 1) - 1);
+              cur = stack[k * (32 * NP) + tix];
+              dep = k;
+            }
+          }
+          named_arrive(1 + stage, kFullThreads);
+        }
+      } else {
       for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
         const uint32_t stage = wseq & 1, use = wseq >> 1;
         if (use > 0) named_sync(3 + stage, kEmptyThreads);
@@ -346,7 +397,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
             y1 = (valid && row + 1 >= g.r0 && row + 1 < g.r1) ? y1 : 0u;
           }
           if (lane_on) {
-            const uint32_t slot = nl * 2 * p.W + 2 * qi;
+            const uint32_t slot = nl * p.R + 2 * qi;
             yb[slot * p.Kt + kl] = y0;
             yb[(slot + 1) * p.Kt + kl] = y1;
           }
@@ -358,6 +409,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
         }
         named_arrive(1 + stage, kFullThreads);
       }
+      }  // !kEt
     }
   } else if (warp < NP + NC) {
     // ------------------------------------------------------------ consumers
@@ -373,7 +425,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
 #pragma unroll
       for (int c = 0; c < CPL; ++c) acc[k][c] = 0;
     uint32_t wseq = 0, tseq = 0;
-    const uint32_t seg = 2 * p.W;  // rows per node per window
+    const uint32_t seg = p.R;  // rows per node per window
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       const GroupDesc g = group_of(p, item);
       const uint32_t kt = (item - g.item_base) % g.n_ktiles;
@@ -416,8 +468,9 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
     // T ring of (window, node chunk) entries: CN nodes x 2W rows, one
     // cp.async.bulk per node segment, decoupled from the y ring.
     uint32_t tseq = 0;
-    const uint64_t seg_rows = 2 * p.W;
+    const uint64_t seg_rows = p.R;
     const uint32_t row_bytes = p.D * 4;
+    constexpr uint32_t V = Prf::kEt ? 4u : 0u;
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       const GroupDesc g = group_of(p, item);
       const uint32_t ng = (item - g.item_base) / g.n_ktiles;
@@ -433,8 +486,8 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
             // table, and per-node copies of a few KB starve the TMA unit)
             const uint64_t nb = uint64_t(ng) * p.Ft;
             const uint64_t nend = min(uint64_t(n1) + nb, g.F);
-            const uint64_t s0 = (g.lo_f + nb + n0) << g.m;
-            const uint64_t s1 = nend > nb + n0 ? (g.lo_f + nend) << g.m : s0;
+            const uint64_t s0 = (g.lo_f + nb + n0) << (g.m + V);
+            const uint64_t s1 = nend > nb + n0 ? (g.lo_f + nend) << (g.m + V) : s0;
             const uint64_t a = s0 > g.r0 ? s0 : g.r0, e = s1 < g.r1 ? s1 : g.r1;
             const uint32_t bytes = a < e ? uint32_t(e - a) * row_bytes : 0u;
             if (lane == 0) {
@@ -448,7 +501,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
           for (uint32_t nl = n0 + lane; nl < n1; nl += 32) {
             const uint64_t node = uint64_t(ng) * p.Ft + nl;
             if (node >= g.F) continue;
-            const uint64_t s0 = ((g.lo_f + node) << g.m) + seg_rows * win;
+            const uint64_t s0 = ((g.lo_f + node) << (g.m + V)) + seg_rows * win;
             const uint64_t a = s0 > g.r0 ? s0 : g.r0, e = (s0 + seg_rows) < g.r1 ? (s0 + seg_rows) : g.r1;
             if (a < e) my_bytes += uint32_t(e - a) * row_bytes;
           }
@@ -458,7 +511,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
           for (uint32_t nl = n0 + lane; nl < n1; nl += 32) {
             const uint64_t node = uint64_t(ng) * p.Ft + nl;
             if (node >= g.F) continue;
-            const uint64_t s0 = ((g.lo_f + node) << g.m) + seg_rows * win;
+            const uint64_t s0 = ((g.lo_f + node) << (g.m + V)) + seg_rows * win;
             const uint64_t a = s0 > g.r0 ? s0 : g.r0, e = (s0 + seg_rows) < g.r1 ? (s0 + seg_rows) : g.r1;
             if (a < e)
               bulk_g2s(tb + (uint64_t(nl - n0) * seg_rows + (a - s0)) * p.D, g.T + (a - g.r0) * p.D,
@@ -559,12 +612,23 @@ __global__ void eval_leaves_kernel(const uint8_t *__restrict__ keys, uint32_t ks
     const uint64_t j = i & (N - 1);
     const uint8_t *key = keys + uint64_t(b) * kstride;
     uint4 s = key_root(key);
-    for (uint32_t d = 1; d <= n; ++d) {
+    constexpr uint32_t V = Prf::kEt ? 4u : 0u;
+    for (uint32_t d = 1; d + V <= n; ++d) {
       uint4 c0, c1;
       node_children<Prf>(s, key_cw(key, d), c0, c1);
       s = ((j >> (n - d)) & 1) ? c1 : c0;
     }
-    const uint32_t v = leaf_value<Prf>(s, key_cw_out(key));
+    uint32_t v;
+    if constexpr (Prf::kEt) {  // R20: word j mod 16 of the final node's Convert block
+      uint32_t cwl[16], y[16];
+      load_cwl(key_cw(key, n - V + 1), cwl);
+      leaf_values16(s, cwl, y);
+      v = y[0];
+#pragma unroll
+      for (int c = 1; c < 16; ++c) v = (uint32_t(j & 15) == uint32_t(c)) ? y[c] : v;
+    } else {
+      v = leaf_value<Prf>(s, key_cw_out(key));
+    }
     leaves[i] = key_party(key) ? 0u - v : v;
   }
 }
@@ -590,17 +654,27 @@ struct KernelChoice {
   int NP, KPW, CPL;
   void (*fn)(const dev::FusedParams);      // ChaCha20
   void (*fn_aes)(const dev::FusedParams);  // AES-128 (bitsliced)
+  void (*fn_et)(const dev::FusedParams);   // ChaCha20, early-terminated leaves (R20)
+  void (*get(uint32_t prf) const)(const dev::FusedParams) {
+    return prf == DPF_PRF_AES128 ? fn_aes : prf == DPF_PRF_CHACHA20_ET ? fn_et : fn;
+  }
 };
 
 template <int NP, int KPW, int CPL>
 KernelChoice choice() {
   return {NP, KPW, CPL, &dev::fused_eval_kernel<dev::PrfChacha, NP, kNC, KPW, CPL>,
-          &dev::fused_eval_kernel<dev::PrfAesBs, NP, kNC, KPW, CPL>};
+          &dev::fused_eval_kernel<dev::PrfAesBs, NP, kNC, KPW, CPL>,
+          &dev::fused_eval_kernel<dev::PrfChachaEt, NP, kNC, KPW, CPL>};
 }
 
 struct Plan {
-  uint32_t prf;  // DPF_PRF_CHACHA20 / DPF_PRF_AES128
+  uint32_t prf;  // DPF_PRF_CHACHA20 / DPF_PRF_AES128 / DPF_PRF_CHACHA20_ET
   bool tc;  // tcgen05 contraction on a limb-packed table
+  // Early termination (R20): v = 4, the tree (depth n = log_n - 4) ends at
+  // final nodes of 16 rows.  nr0/nr1: the row range in tree-leaf units
+  // (final nodes; = r0/r1 without ET), used by the top BFS and the frontier.
+  uint32_t v, R;
+  uint64_t nr0, nr1;
   uint32_t nsy, nst;  // y-ring / T-ring depth (tc)
   uint32_t tmem_cols, y_stage_bytes, t_stage_bytes;
   uint64_t r0a, packed_rows;
@@ -682,11 +756,11 @@ bool pick_kernel(uint32_t Kt, uint32_t D, Plan &pl) {
 
 // Subtree depth m: the largest m (<= m_cap) that still gives >= 8 work items
 // per SM (measured: beyond that, deeper top BFS costs more than balance gains).
-uint32_t choose_m_target(const Plan &pl, uint32_t n, uint64_t r0, uint32_t m_min, uint32_t m_cap) {
+uint32_t choose_m_target(const Plan &pl, uint32_t n, uint32_t m_min, uint32_t m_cap) {
   const uint64_t target = 8ull * num_sms();
   uint32_t best = m_min;
   for (uint32_t m = std::min<uint32_t>(n, m_cap); m >= m_min; --m) {
-    const uint64_t F = ((pl.r1 - 1) >> m) - (r0 >> m) + 1;
+    const uint64_t F = ((pl.nr1 - 1) >> m) - (pl.nr0 >> m) + 1;
     const uint64_t items = uint64_t(pl.n_ktiles) * ((F + pl.Ft - 1) / pl.Ft);
     best = m;
     if (items >= target) break;
@@ -695,16 +769,23 @@ uint32_t choose_m_target(const Plan &pl, uint32_t n, uint64_t r0, uint32_t m_min
 }
 
 // Window / T-ring sizing for the IMAD kernel; false if SMEM does not fit.
+// Rows per window unit: a leaf pair, or one final node with early termination.
+inline uint32_t unit_rows(const Plan &pl) { return pl.v ? (1u << pl.v) : 2u; }
+
 bool set_windows(Plan &pl, uint32_t W, uint32_t D, size_t stack_bytes) {
   pl.W = W;
-  pl.y_stage_words = uint32_t(align_up(size_t(pl.Kt) * pl.Ft * 2 * W, 32));
+  pl.R = unit_rows(pl) * W;
+  pl.y_stage_words = uint32_t(align_up(size_t(pl.Kt) * pl.Ft * pl.R, 32));
   const uint32_t pad = 32u * pl.kc.CPL * pl.CG;  // lanes whose columns exceed D read past the last row
+  // A final node's 16 rows (early termination) cannot be split across
+  // entries: its entry may exceed the default size at large D.
+  const size_t budget = pl.v ? std::max<size_t>(kTEntryBytes, (size_t(pl.R) * D + pad) * 4) : kTEntryBytes;
   uint32_t CN = pl.Ft;
-  while (CN > 1 && (size_t(CN) * 2 * W * D + pad) * 4 > kTEntryBytes) CN >>= 1;
-  if ((size_t(CN) * 2 * W * D + pad) * 4 > kTEntryBytes) return false;
+  while (CN > 1 && (size_t(CN) * pl.R * D + pad) * 4 > budget) CN >>= 1;
+  if ((size_t(CN) * pl.R * D + pad) * 4 > budget) return false;
   pl.CN = CN;
   pl.n_chunks = (pl.Ft + CN - 1) / CN;
-  pl.t_stage_words = uint32_t(align_up(size_t(CN) * 2 * W * D + pad, 32));
+  pl.t_stage_words = uint32_t(align_up(size_t(CN) * pl.R * D + pad, 32));
   const size_t fixed = 128 + 4 * 2 * size_t(pl.y_stage_words) + stack_bytes;
   if (fixed + 2 * 4 * size_t(pl.t_stage_words) > 227 * 1024) return false;
   pl.NST = uint32_t(std::min<size_t>(8, (227 * 1024 - fixed) / (4 * size_t(pl.t_stage_words))));
@@ -712,11 +793,29 @@ bool set_windows(Plan &pl, uint32_t W, uint32_t D, size_t stack_bytes) {
   return true;
 }
 
-int make_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl) {
-  std::memset(&pl, 0, sizeof pl);
-  pl.n = n;
+// Row range -> tree-leaf (final node) range for the top BFS and frontier.
+void set_ranges(Plan &pl, uint32_t log_n, uint64_t r0, uint64_t rows, bool et) {
+  pl.v = et ? 4u : 0u;
+  pl.n = log_n - pl.v;
   pl.r0 = r0;
   pl.r1 = r0 + rows;
+  pl.nr0 = r0 >> pl.v;
+  pl.nr1 = ((pl.r1 - 1) >> pl.v) + 1;
+}
+
+// PRF blocks: top levels (nodes intersecting the range) + fused subtrees
+// (2^m - 1 internal nodes, + 2^m Convert blocks with early termination).
+uint64_t count_blocks(const Plan &pl, uint32_t B) {
+  uint64_t top = 0;
+  for (uint32_t k = 0; k < pl.f; ++k) top += ((pl.nr1 - 1) >> (pl.n - k)) - (pl.nr0 >> (pl.n - k)) + 1;
+  const uint64_t per = ((1ull << pl.m) - 1) + (pl.v ? (1ull << pl.m) : 0);
+  return uint64_t(B) * top + uint64_t(pl.n_items) * pl.tasks * per;
+}
+
+int make_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et = false) {
+  std::memset(&pl, 0, sizeof pl);
+  set_ranges(pl, log_n, r0, rows, et);
+  const uint32_t n = pl.n;
   // Key tile: lanes <-> keys (Kt <= 32), remaining lanes <-> frontier nodes.
   pl.Kt = std::min<uint32_t>(32, pow2ceil(B));
   while (pl.Kt * D > 8192 && pl.Kt > 1) pl.Kt >>= 1;  // accumulator budget: Kt*D <= 8192 words/CTA
@@ -730,23 +829,25 @@ int make_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Pl
   // Subtree depth m (frontier depth f = n - m) from a cost model; the SMEM
   // DFS stack (m x 16 B per producer thread) is capped at 64 KB.
   const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((64 * 1024) / (32 * NP * 16)));
-  pl.m = choose_m_target(pl, n, r0, 1, m_cap);
+  pl.m = choose_m_target(pl, n, 1, m_cap);
   if (const char *e = getenv("DPF_FORCE_M")) {  // tuning override
     const uint32_t fm = uint32_t(atoi(e));
     if (fm >= 1 && fm <= std::min<uint32_t>(n, m_cap)) pl.m = fm;
   }
   pl.f = n - pl.m;
-  pl.lo_f = r0 >> pl.m;
-  pl.F = ((pl.r1 - 1) >> pl.m) - pl.lo_f + 1;
+  pl.lo_f = pl.nr0 >> pl.m;
+  pl.F = ((pl.nr1 - 1) >> pl.m) - pl.lo_f + 1;
   pl.cap = pl.F;
   const uint64_t items = uint64_t(pl.n_ktiles) * ((pl.F + pl.Ft - 1) / pl.Ft);
   if (items > 0x7FFFFFFFull) return DPF_EINVAL;
   pl.n_items = uint32_t(items);
-  // Window: W leaf pairs per thread (y stage = Kt*Ft*2W words <= 16 KB); T
-  // ring entries of CN nodes x 2W rows (<= 32 KB), NST of them.
-  const uint32_t nq = 1u << (pl.m - 1);
+  // Window: W units per thread (y stage = Kt*Ft*R words <= 16 KB, 32 KB with
+  // early termination, whose shallower subtrees leave SMEM to spare); T ring
+  // entries of CN nodes x R rows (<= 32 KB), NST of them.
+  const uint32_t nq = et ? (1u << pl.m) : (1u << (pl.m - 1));
+  const uint64_t ybudget = et ? 32 * 1024 : 16 * 1024;
   uint32_t W = std::min<uint32_t>(8, nq);
-  while (W > 1 && uint64_t(pl.Kt) * pl.Ft * 2 * W * 4 > 16 * 1024) W >>= 1;
+  while (W > 1 && uint64_t(pl.Kt) * pl.Ft * unit_rows(pl) * W * 4 > ybudget) W >>= 1;
   const size_t stack_bytes = size_t(pl.m) * 32 * NP * 16;
   for (;; W >>= 1) {
     if (set_windows(pl, W, D, stack_bytes)) break;
@@ -754,10 +855,7 @@ int make_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Pl
   }
   pl.nwin = nq / pl.W;
   pl.grid = std::min<uint32_t>(pl.n_items, uint32_t(num_sms()));
-  // PRF blocks: top levels (nodes intersecting the range) + fused subtrees.
-  uint64_t top = 0;
-  for (uint32_t k = 0; k < pl.f; ++k) top += ((pl.r1 - 1) >> (n - k)) - (r0 >> (n - k)) + 1;
-  pl.prf_blocks = uint64_t(B) * top + uint64_t(pl.n_items) * pl.tasks * ((1ull << pl.m) - 1);
+  pl.prf_blocks = count_blocks(pl, B);
   return DPF_OK;
 }
 
@@ -771,13 +869,12 @@ inline uint32_t tc_t_stages(uint32_t) { return 4u; }
 // Kt = MMA N = 64/32/16 keys so that 4 limb accumulators x D/128 tiles x Kt
 // columns fit the 512 TMEM columns; Ft = 512/Kt frontier nodes per item;
 // W = 4 leaf pairs per node per window (one 8-row packed block).
-int make_tc_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl) {
+int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et = false) {
   std::memset(&pl, 0, sizeof pl);
-  if (D % 128 || D > 1024 || n < 3) return DPF_EINVAL;
+  if (D % 128 || D > 1024 || log_n < 3) return DPF_EINVAL;
   pl.tc = true;
-  pl.n = n;
-  pl.r0 = r0;
-  pl.r1 = r0 + rows;
+  set_ranges(pl, log_n, r0, rows, et);
+  const uint32_t n = pl.n;
   pl.r0a = r0 & ~7ull;
   pl.packed_rows = ((pl.r1 + 7) & ~7ull) - pl.r0a;
   pl.Kt = D <= 256 ? 64 : D <= 512 ? 32 : 16;
@@ -785,33 +882,35 @@ int make_tc_plan(uint32_t B, uint32_t n, uint64_t r0, uint64_t rows, uint32_t D,
   pl.Ft = 32 * kTcNP / pl.Kt;
   pl.tasks = pl.Kt * pl.Ft;
   pl.n_ktiles = (B + pl.Kt - 1) / pl.Kt;
-  const uint32_t W = 4;
-  const uint32_t Kw = pl.Ft * 2 * W;
+  // W units per node per window: 4 leaf pairs (one 8-row packed block), or
+  // one final node (16 rows) with early termination.
+  const uint32_t W = et ? 1 : 4;
+  pl.R = unit_rows(pl) * W;
+  const uint32_t Kw = pl.Ft * pl.R;
   pl.y_stage_bytes = 4 * pl.Kt * Kw;
   // SMEM: T ring + y ring + the DFS stack (16 B per producer thread per level)
   pl.nst = tc_t_stages(D);
   const size_t fixed = 1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(kTcNSY) * pl.y_stage_bytes;
   const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / (32 * kTcNP * 16)));
-  if (m_cap < 3) return DPF_EINVAL;
-  pl.m = choose_m_target(pl, n, r0, 3, m_cap);
+  const uint32_t m_min = et ? 1 : 3;
+  if (m_cap < m_min || n < m_min) return DPF_EINVAL;
+  pl.m = choose_m_target(pl, n, m_min, m_cap);
   pl.f = n - pl.m;
-  pl.lo_f = r0 >> pl.m;
-  pl.F = ((pl.r1 - 1) >> pl.m) - pl.lo_f + 1;
+  pl.lo_f = pl.nr0 >> pl.m;
+  pl.F = ((pl.nr1 - 1) >> pl.m) - pl.lo_f + 1;
   pl.cap = pl.F;
   const uint64_t items = uint64_t(pl.n_ktiles) * ((pl.F + pl.Ft - 1) / pl.Ft);
   if (items > 0x7FFFFFFFull) return DPF_EINVAL;
   pl.n_items = uint32_t(items);
   pl.W = W;
-  pl.nwin = (1u << (pl.m - 1)) / W;
+  pl.nwin = (et ? (1u << pl.m) : (1u << (pl.m - 1))) / W;
   const uint32_t cols = (D / 128) * 4 * pl.Kt;
   pl.tmem_cols = 32;
   while (pl.tmem_cols < cols) pl.tmem_cols <<= 1;
   pl.smem_bytes = fixed + size_t(pl.m) * 32 * kTcNP * 16;  // stack slots 1..m-1 (slot 0 unused)
   if (pl.smem_bytes > 227 * 1024) return DPF_EINVAL;
   pl.grid = std::min<uint32_t>(pl.n_items, uint32_t(num_sms()));
-  uint64_t top = 0;
-  for (uint32_t k = 0; k < pl.f; ++k) top += ((pl.r1 - 1) >> (n - k)) - (r0 >> (n - k)) + 1;
-  pl.prf_blocks = uint64_t(B) * top + uint64_t(pl.n_items) * pl.tasks * ((1ull << pl.m) - 1);
+  pl.prf_blocks = count_blocks(pl, B);
   return DPF_OK;
 }
 
@@ -872,26 +971,28 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
     dev::copy_roots_kernel<<<(B + 127) / 128, 128, 0, st>>>(keys_dev, kstride, B, ws.front[0], pl.cap);
     ++nk;
   }
+  // The top of the tree works on tree-leaf (final node) ranges [nr0, nr1):
+  // with early termination (R20) the levels are Eq. 3 ChaCha20 levels.
   const uint32_t a = std::min(pl.f, dev::kTopSmemLevels);
   if (a >= 1) {
     if (pl.prf == DPF_PRF_AES128)
-      dev::expand_top_smem_kernel<dev::PrfAesBs><<<B, 256, 0, st>>>(keys_dev, kstride, pl.n, a, pl.r0, pl.r1,
+      dev::expand_top_smem_kernel<dev::PrfAesBs><<<B, 256, 0, st>>>(keys_dev, kstride, pl.n, a, pl.nr0, pl.nr1,
                                                                    ws.front[(pl.f - a) & 1], pl.cap);
     else
-      dev::expand_top_smem_kernel<dev::PrfChacha><<<B, 256, 0, st>>>(keys_dev, kstride, pl.n, a, pl.r0, pl.r1,
+      dev::expand_top_smem_kernel<dev::PrfChacha><<<B, 256, 0, st>>>(keys_dev, kstride, pl.n, a, pl.nr0, pl.nr1,
                                                                     ws.front[(pl.f - a) & 1], pl.cap);
     ++nk;
   }
   for (uint32_t k = a + 1; k <= pl.f; ++k) {
-    const uint64_t np = ((pl.r1 - 1) >> (pl.n - (k - 1))) - (pl.r0 >> (pl.n - (k - 1))) + 1;
+    const uint64_t np = ((pl.nr1 - 1) >> (pl.n - (k - 1))) - (pl.nr0 >> (pl.n - (k - 1))) + 1;
     const uint64_t total = np * B;
     const uint32_t grid = uint32_t(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
     if (pl.prf == DPF_PRF_AES128)
-      dev::expand_level_kernel<dev::PrfAesBs><<<grid, 256, 0, st>>>(keys_dev, kstride, B, pl.n, k, pl.r0, pl.r1,
+      dev::expand_level_kernel<dev::PrfAesBs><<<grid, 256, 0, st>>>(keys_dev, kstride, B, pl.n, k, pl.nr0, pl.nr1,
                                                                    ws.front[(pl.f - k + 1) & 1],
                                                                    ws.front[(pl.f - k) & 1], pl.cap);
     else
-      dev::expand_level_kernel<dev::PrfChacha><<<grid, 256, 0, st>>>(keys_dev, kstride, B, pl.n, k, pl.r0, pl.r1,
+      dev::expand_level_kernel<dev::PrfChacha><<<grid, 256, 0, st>>>(keys_dev, kstride, B, pl.n, k, pl.nr0, pl.nr1,
                                                                     ws.front[(pl.f - k + 1) & 1],
                                                                     ws.front[(pl.f - k) & 1], pl.cap);
     ++nk;
@@ -927,6 +1028,7 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
   p.Ft = pl.Ft;
   p.tasks = pl.tasks;
   p.W = pl.W;
+  p.R = pl.R;
   p.CG = pl.CG;
   p.KG = pl.KG;
   p.SG = pl.SG;
@@ -940,8 +1042,9 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
     tp.f = p;
     tp.y_stage_bytes = pl.y_stage_bytes;
     tp.tmem_cols = pl.tmem_cols;
-    auto fn = pl.prf == DPF_PRF_AES128 ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4>
-                                       : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4>;
+    auto fn = pl.prf == DPF_PRF_AES128        ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4>
+              : pl.prf == DPF_PRF_CHACHA20_ET ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSY, 4>
+                                              : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4>;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
       return DPF_ECUDA;
     if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
@@ -952,7 +1055,7 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
     if (kernels) *kernels = nk;
     return DPF_OK;
   }
-  auto kfn = pl.prf == DPF_PRF_AES128 ? pl.kc.fn_aes : pl.kc.fn;
+  auto kfn = pl.kc.get(pl.prf);
   if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
     return DPF_ECUDA;
   if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
@@ -965,9 +1068,9 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
 }
 
 int check_common(uint32_t B, const uint32_t *table, uint64_t row_begin, uint64_t rows, uint32_t D,
-                 const uint32_t *out, void *ws, uint32_t n) {
+                 const uint32_t *out, void *ws, uint32_t n, uint32_t prf) {
   if (B == 0 || !table || !out || !ws || D == 0 || D > 1024 || (D & 3)) return DPF_EINVAL;
-  if (n < 1 || n > DPF_MAX_LOG_N) return DPF_EKEY;
+  if (n < (prf == DPF_PRF_CHACHA20_ET ? DPF_ET_BITS + 1 : 1) || n > DPF_MAX_LOG_N) return DPF_EKEY;
   if (rows == 0) return DPF_EINVAL;
   const uint64_t dom = n >= 64 ? ~0ull : (1ull << n);
   if (row_begin >= dom || rows > dom - row_begin) return DPF_EINVAL;
@@ -984,7 +1087,7 @@ int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uin
     if (B == 0) return DPF_EINVAL;
     prf = keys[0].prf;
   }
-  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128) return DPF_EUNSUPPORTED;
+  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128 && prf != DPF_PRF_CHACHA20_ET) return DPF_EUNSUPPORTED;
   if (keys) {
     if (B == 0) return DPF_EINVAL;
     n = keys[0].log_n;
@@ -993,13 +1096,14 @@ int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uin
       if (keys[b].log_n != n || keys[b].prf != keys[0].prf) return DPF_EKEY;
     }
   }
-  int rc = check_common(B, table, row_begin, rows, D, out, workspace, n);
+  int rc = check_common(B, table, row_begin, rows, D, out, workspace, n, prf);
   if (rc) return rc;
   Plan pl;
-  rc = packed ? make_tc_plan(B, n, row_begin, rows, D, pl) : make_plan(B, n, row_begin, rows, D, pl);
+  const bool et = prf == DPF_PRF_CHACHA20_ET;
+  rc = packed ? make_tc_plan(B, n, row_begin, rows, D, pl, et) : make_plan(B, n, row_begin, rows, D, pl, et);
   if (rc) return rc;
   pl.prf = prf;
-  const uint32_t kstride = uint32_t(dpf_key_wire_size(n));
+  const uint32_t kstride = uint32_t(dpf_key_wire_size_prf(n, prf));
   Workspace ws;
   const size_t need = layout(pl, B, kstride, &ws, workspace);
   if (ws_bytes < need) return DPF_ENOMEM;
@@ -1065,15 +1169,46 @@ extern "C" size_t dpf_eval_workspace_bytes(uint32_t B, uint32_t log_n, uint64_t 
   Plan pl;
   if (make_plan(B, log_n, 0, row_count, D, pl) != DPF_OK) return 0;
   // The frontier size depends on the alignment of row_begin; size for the
-  // worst case (one extra node per key).
+  // worst case (one extra node per key).  Covers every scheme and both
+  // contraction paths (IMAD, tcgen05).
   pl.cap += 1;
   size_t bytes = layout(pl, B, dpf_key_wire_size(log_n), nullptr, nullptr);
-  Plan tc;
-  if (make_tc_plan(B, log_n, 0, row_count, D, tc) == DPF_OK) {
-    tc.cap += 1;
-    bytes = std::max(bytes, layout(tc, B, dpf_key_wire_size(log_n), nullptr, nullptr));
+  for (int et = 0; et < 2; ++et) {
+    if (et && log_n <= DPF_ET_BITS) break;
+    const size_t kst = et ? dpf_key_wire_size_prf(log_n, DPF_PRF_CHACHA20_ET) : dpf_key_wire_size(log_n);
+    Plan q;
+    if (et && make_plan(B, log_n, 0, row_count, D, q, true) == DPF_OK) {
+      q.cap += 1;
+      bytes = std::max(bytes, layout(q, B, kst, nullptr, nullptr));
+    }
+    if (make_tc_plan(B, log_n, 0, row_count, D, q, et != 0) == DPF_OK) {
+      q.cap += 1;
+      bytes = std::max(bytes, layout(q, B, kst, nullptr, nullptr));
+    }
   }
   return bytes;
+}
+
+extern "C" int dpf_eval_plan(uint32_t B, uint32_t log_n, uint32_t prf, uint64_t row_begin, uint64_t row_count,
+                             uint32_t D, int packed, dpf_eval_stats *out) {
+  if (!out || B == 0 || D == 0 || D > 1024 || (D & 3) || row_count == 0) return DPF_EINVAL;
+  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128 && prf != DPF_PRF_CHACHA20_ET) return DPF_EUNSUPPORTED;
+  const bool et = prf == DPF_PRF_CHACHA20_ET;
+  if (log_n < (et ? DPF_ET_BITS + 1 : 1) || log_n > DPF_MAX_LOG_N) return DPF_EINVAL;
+  const uint64_t dom = 1ull << log_n;
+  if (row_begin >= dom || row_count > dom - row_begin) return DPF_EINVAL;
+  Plan pl;
+  const int rc = packed ? make_tc_plan(B, log_n, row_begin, row_count, D, pl, et)
+                        : make_plan(B, log_n, row_begin, row_count, D, pl, et);
+  if (rc) return rc;
+  out->prf_blocks = pl.prf_blocks;
+  out->kernels = 0;
+  out->frontier_depth = pl.f;
+  out->keys_per_tile = pl.Kt;
+  out->nodes_per_tile = pl.Ft;
+  out->work_items = pl.n_items;
+  out->grid = pl.grid;
+  return DPF_OK;
 }
 
 extern "C" size_t dpf_table_packed_bytes(uint64_t row_begin, uint64_t row_count, uint32_t D) {
@@ -1159,7 +1294,7 @@ extern "C" int dpf_eval_leaves(const dpf_key *keys, uint32_t B, uint32_t *leaves
   for (uint32_t b = 0; b < B; ++b)
     if (!host_key_valid(keys[b]) || keys[b].log_n != n || keys[b].prf != keys[0].prf) return DPF_EKEY;
   if (n > 20) return DPF_EINVAL;
-  const uint32_t kstride = uint32_t(dpf_key_wire_size(n));
+  const uint32_t kstride = uint32_t(dpf_key_wire_size_prf(n, keys[0].prf));
   if (workspace_bytes < size_t(B) * kstride) return DPF_ENOMEM;
   std::vector<uint8_t> staged(size_t(B) * kstride);
   for (uint32_t b = 0; b < B; ++b) dpf_key_serialize(&keys[b], staged.data() + size_t(b) * kstride, kstride, nullptr);
@@ -1172,6 +1307,8 @@ extern "C" int dpf_eval_leaves(const dpf_key *keys, uint32_t B, uint32_t *leaves
   if (keys[0].prf == DPF_PRF_AES128) {
     dev::aes_bitslice_keys_kernel<<<uint32_t((B * (1 + 4 * n) + 255) / 256), 256, 0, st>>>(kd, kstride, B, n);
     dev::eval_leaves_kernel<dev::PrfAesBs><<<grid, 256, 0, st>>>(kd, kstride, B, n, leaves);
+  } else if (keys[0].prf == DPF_PRF_CHACHA20_ET) {
+    dev::eval_leaves_kernel<dev::PrfChachaEt><<<grid, 256, 0, st>>>(kd, kstride, B, n, leaves);
   } else {
     dev::eval_leaves_kernel<dev::PrfChacha><<<grid, 256, 0, st>>>(kd, kstride, B, n, leaves);
   }
@@ -1228,6 +1365,7 @@ struct GroupedPlan {
 // items ordered by subtree size so the static round-robin stays balanced.
 int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t prf, GroupedPlan &gp) {
   if (!gs || G == 0 || D == 0 || D > 1024 || (D & 3)) return DPF_EINVAL;
+  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128) return DPF_EUNSUPPORTED;
   uint32_t Bmax = 0;
   for (uint32_t i = 0; i < G; ++i) {
     const dpf_eval_group &g = gs[i];
@@ -1341,7 +1479,7 @@ extern "C" size_t dpf_eval_grouped_workspace_bytes(const dpf_eval_group *groups,
 
 extern "C" int dpf_eval_grouped(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D, uint32_t prf,
                                 void *workspace, size_t workspace_bytes, void *stream) {
-  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128) return DPF_EUNSUPPORTED;
+  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128) return DPF_EUNSUPPORTED;  // ET: not grouped (yet)
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & (kAlign - 1))) return DPF_EINVAL;
   GroupedPlan gp;
   int rc = make_grouped_plan(groups, n_groups, D, prf, gp);
@@ -1427,6 +1565,7 @@ extern "C" int dpf_eval_grouped(const dpf_eval_group *groups, uint32_t n_groups,
   p.Ft = pl.Ft;
   p.tasks = pl.tasks;
   p.W = pl.W;
+  p.R = pl.R;
   p.CG = pl.CG;
   p.KG = pl.KG;
   p.SG = pl.SG;
@@ -1435,7 +1574,7 @@ extern "C" int dpf_eval_grouped(const dpf_eval_group *groups, uint32_t n_groups,
   p.CN = pl.CN;
   p.n_chunks = pl.n_chunks;
   p.NST = pl.NST;
-  auto kfn = prf == DPF_PRF_AES128 ? pl.kc.fn_aes : pl.kc.fn;
+  auto kfn = pl.kc.get(prf);
   if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
     return DPF_ECUDA;
   const bool timed = g_timer.on && 2 * g_timer.used + 1 < g_timer.ev.size();

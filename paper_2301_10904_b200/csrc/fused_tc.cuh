@@ -95,6 +95,27 @@ __device__ __forceinline__ void put_leaf_pair(uint8_t *yb, uint32_t ybplane, uin
   *reinterpret_cast<uint16_t *>(yb + 3 * ybplane + off) = uint16_t(p23 >> 16);
 }
 
+// R20 (early termination): the 16 leaves kk..kk+15 (kk % 16 == 0) of key kl
+// from one final node -> one 16-byte row of core matrix (kk/16, kl/8) in each
+// limb plane: a 4x4 byte transpose per 4 leaves (8 PRMT), one STS.128 per plane.
+__device__ __forceinline__ void put_leaf16(uint8_t *yb, uint32_t ybplane, uint32_t Kt, uint32_t kl, uint32_t kk,
+                                           const uint32_t (&y)[16]) {
+  const uint32_t off = ((kk >> 4) * (Kt >> 3) + (kl >> 3)) * 128u + (kl & 7u) * 16u;
+  uint32_t pl[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t a = __byte_perm(y[4 * i], y[4 * i + 1], 0x5140), b = __byte_perm(y[4 * i + 2], y[4 * i + 3], 0x5140);
+    const uint32_t c = __byte_perm(y[4 * i], y[4 * i + 1], 0x7362), d = __byte_perm(y[4 * i + 2], y[4 * i + 3], 0x7362);
+    pl[0][i] = __byte_perm(a, b, 0x5410);
+    pl[1][i] = __byte_perm(a, b, 0x7632);
+    pl[2][i] = __byte_perm(c, d, 0x5410);
+    pl[3][i] = __byte_perm(c, d, 0x7632);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    *reinterpret_cast<uint4 *>(yb + k * ybplane + off) = make_uint4(pl[k][0], pl[k][1], pl[k][2], pl[k][3]);
+}
+
 // NP producer warps, NSY-deep y ring, NST-deep T ring of (K-chunk, d-tile)
 // entries.  Named barriers: 1..NSY = y stage FULL (producers arrive, the MMA
 // warp syncs); NSY+1 = epilogue.
@@ -135,8 +156,9 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const uint32_t W2 = 2 * p.W;         // leaves per node per window (multiple of 8)
+  const uint32_t W2 = p.R;             // leaves per node per window (multiple of 8)
   const uint32_t Kw = p.Ft * W2;       // leaves per window (multiple of 32)
+  constexpr uint32_t V = Prf::kEt ? 4u : 0u;  // log2(rows per subtree leaf), R20
   const uint32_t ybplane = p.Kt * Kw;  // bytes per y limb plane
   const uint32_t D = p.D;
 
@@ -161,9 +183,55 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
       const uint8_t *key = g.keys + uint64_t(valid ? b : 0) * g.kstride;
       const uint32_t cw_out = key_cw_out(key);
       uint4 cur = valid ? g.frontier[uint64_t(b) * g.cap + node] : make_uint4(0, 0, 0, 0);
-      const uint64_t row_base = (g.lo_f + node) << g.m;
-      const bool inside = valid && row_base >= g.r0 && row_base + (1ull << g.m) <= g.r1;
+      const uint64_t row_base = (g.lo_f + node) << (g.m + V);
+      const bool inside = valid && row_base >= g.r0 && row_base + (1ull << (g.m + V)) <= g.r1;
       uint32_t dep = 0;
+      if constexpr (Prf::kEt) {
+        // R20: one final node (16 leaves) per unit; even units expand the
+        // leaf-parent, odd units convert the right child kept from it.
+        uint32_t cwl[16];
+        load_cwl(key_cw(key, g.n + 1), cwl);
+        uint4 pend = make_uint4(0, 0, 0, 0);
+        const uint32_t npairs = 1u << (g.m - 1);
+        for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
+          const uint32_t ys = wseq % NSY, yuse = wseq / NSY;
+          if (yuse > 0) mbar_wait(&yempty[ys], (yuse - 1) & 1);
+          uint8_t *yb = ybuf + ys * tp.y_stage_bytes;
+          for (uint32_t qi = 0; qi < p.W; ++qi) {
+            const uint32_t q = win * p.W + qi;
+            uint4 sf;
+            if ((q & 1) == 0) {
+              while (dep + 1 < g.m) {
+                uint4 c0, c1;
+                node_children<Prf>(cur, key_cw(key, g.n - g.m + dep + 1), c0, c1);
+                stack[(dep + 1) * (32 * NP) + tix] = c1;
+                cur = c0;
+                ++dep;
+              }
+              node_children<Prf>(cur, key_cw(key, g.n), sf, pend);
+            } else {
+              sf = pend;
+            }
+            uint32_t y[16];
+            leaf_values16(sf, cwl, y);
+            if (!inside) {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) {
+                const uint64_t row = row_base + 16ull * q + c;
+                y[c] = (valid && row >= g.r0 && row < g.r1) ? y[c] : 0u;
+              }
+            }
+            put_leaf16(yb, ybplane, p.Kt, kl, nl * W2 + 16 * qi, y);
+            if ((q & 1) && (q >> 1) + 1 < npairs) {
+              const uint32_t k = g.m - 1 - (__ffs((q >> 1) + 1) - 1);
+              cur = stack[k * (32 * NP) + tix];
+              dep = k;
+            }
+          }
+          fence_proxy_async_smem();
+          named_arrive(1 + ys, 32 * (NP + 1));
+        }
+      } else {
       for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
         const uint32_t ys = wseq % NSY, yuse = wseq / NSY;
         if (yuse > 0) mbar_wait(&yempty[ys], (yuse - 1) & 1);
@@ -195,6 +263,7 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
         fence_proxy_async_smem();  // generic-proxy STS -> visible to the tensor core (async proxy)
         named_arrive(1 + ys, 32 * (NP + 1));  // the MMA warp sleeps in bar.sync until all producers arrive
       }
+      }  // !kEt
     }
   } else if (warp < NP + NC) {
     // ------------------------------------------------ MMA issuer + epilogue
@@ -289,9 +358,11 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
       const uint32_t ng = (item - g.item_base) / g.n_ktiles;
       for (uint32_t win = 0; win < g.nwin; ++win) {
         for (uint32_t cc = 0; cc < n_cc; ++cc) {
-          // lane j < 4: node 4cc + j, rows [s0, s0 + 8) (one packed block)
-          const uint64_t node = uint64_t(ng) * p.Ft + 4 * cc + (lane & 3);
-          const uint64_t s0 = ((g.lo_f + node) << g.m) + uint64_t(W2) * win;
+          // lane j < 4: window leaves [32cc + 8j, +8) = rows [s0, s0 + 8) of
+          // one node (one packed block): node (32cc + 8j) / W2, offset % W2
+          const uint32_t kw0 = 32 * cc + 8 * (lane & 3);
+          const uint64_t node = uint64_t(ng) * p.Ft + kw0 / W2;
+          const uint64_t s0 = ((g.lo_f + node) << (g.m + V)) + uint64_t(W2) * win + kw0 % W2;
           const bool ok = lane < 4 && node < g.F && s0 >= g.r0a && s0 < pend;
           const uint32_t total = __popc(__ballot_sync(0xFFFFFFFFu, ok)) * 4096u;
           for (uint32_t dt = 0; dt < n_dt; ++dt, ++tseq) {

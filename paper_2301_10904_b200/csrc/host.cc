@@ -158,11 +158,17 @@ class KeystreamDrbg {
   int pos_ = 16;
 };
 
+// Tree depth: log_n levels, or h = log_n - 4 with early-terminated leaves (R20).
+inline uint32_t tree_levels(uint32_t prf, uint32_t log_n) {
+  return prf == DPF_PRF_CHACHA20_ET ? log_n - DPF_ET_BITS : log_n;
+}
+
 bool key_ok(const dpf_key &k) {
+  const bool et = k.prf == DPF_PRF_CHACHA20_ET;
   return k.magic == DPF_KEY_MAGIC && k.version == DPF_KEY_VERSION &&
-         (k.prf == DPF_PRF_CHACHA20 || k.prf == DPF_PRF_AES128) &&
-         k.party <= 1 && k.log_n >= 1 && k.log_n <= DPF_MAX_LOG_N && (k.root[0] & 1u) == k.party &&
-         k.reserved == 0;
+         (k.prf == DPF_PRF_CHACHA20 || k.prf == DPF_PRF_AES128 || et) && k.party <= 1 &&
+         k.log_n >= (et ? DPF_ET_BITS + 1 : 1) && k.log_n <= DPF_MAX_LOG_N && (k.root[0] & 1u) == k.party &&
+         k.reserved == 0 && (!et || k.cw_out == 0);
 }
 
 }  // namespace
@@ -174,7 +180,10 @@ extern "C" int dpf_gen(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t p
                        dpf_key *k0, dpf_key *k1) {
   if (!k0 || !k1 || log_n < 1 || log_n > DPF_MAX_LOG_N) return DPF_EINVAL;
   if (alpha >> log_n) return DPF_EINVAL;
-  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128) return DPF_EUNSUPPORTED;
+  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128 && prf != DPF_PRF_CHACHA20_ET) return DPF_EUNSUPPORTED;
+  const bool et = prf == DPF_PRF_CHACHA20_ET;
+  if (et && log_n <= DPF_ET_BITS) return DPF_EINVAL;
+  const uint32_t h = tree_levels(prf, log_n);
   uint8_t seed[32];
   if (rng_seed) {
     std::memcpy(seed, rng_seed, 32);
@@ -202,7 +211,7 @@ extern "C" int dpf_gen(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t p
     k.log_n = uint8_t(log_n);
     to_bytes(s[p], k.root);
   }
-  for (uint32_t d = 1; d <= log_n; ++d) {
+  for (uint32_t d = 1; d <= h; ++d) {
     const unsigned keep = unsigned(alpha >> (log_n - d)) & 1u, lose = keep ^ 1u;
     Words4 P[2][2];  // P[party][child]
     prf_pair(prf, s[0], P[0][0], P[0][1]);
@@ -225,6 +234,25 @@ extern "C" int dpf_gen(uint32_t log_n, uint64_t alpha, uint32_t beta, uint32_t p
       }
     for (int p = 0; p < 2; ++p) s[p] = xor4(P[p][keep], C[s[p][0] & 1u][keep]);
   }
+  if (et) {
+    // R20: leaf codeword over the 16 words of Convert(s) = ChaCha20 block 1:
+    // y0 + y1 = beta at alpha's word, 0 at the other 15.
+    uint32_t W[2][16];
+    for (int p = 0; p < 2; ++p) {
+      const uint32_t key[8] = {s[p][0], s[p][1], s[p][2], s[p][3], 0, 0, 0, 0};
+      const uint32_t nonce[3] = {0, 0, 0};
+      chacha20_words(key, 1, nonce, W[p]);
+    }
+    const uint32_t a = uint32_t(alpha & ((1u << DPF_ET_BITS) - 1));
+    for (uint32_t c = 0; c < (1u << DPF_ET_BITS); ++c) {
+      const uint32_t v = (c == a ? beta : 0u) - W[0][c] + W[1][c];
+      const uint32_t cw = (s[1][0] & 1u) ? 0u - v : v;
+      st32(k0->cw[h][0][0] + 4 * c, cw);
+      st32(k1->cw[h][0][0] + 4 * c, cw);
+    }
+    k0->cw_out = k1->cw_out = 0;
+    return DPF_OK;
+  }
   // Final Z_2^32 correction (R7): y0 + y1 = beta at alpha.
   const uint32_t v = beta - s[0][1] + s[1][1];
   const uint32_t cw_out = (s[1][0] & 1u) ? 0u - v : v;
@@ -237,10 +265,16 @@ extern "C" size_t dpf_key_wire_size(uint32_t log_n) {
   return 32u + 64u * size_t(log_n);
 }
 
+extern "C" size_t dpf_key_wire_size_prf(uint32_t log_n, uint32_t prf) {
+  if (prf == DPF_PRF_CHACHA20 || prf == DPF_PRF_AES128) return dpf_key_wire_size(log_n);
+  if (prf != DPF_PRF_CHACHA20_ET || log_n <= DPF_ET_BITS || log_n > DPF_MAX_LOG_N) return 0;
+  return 32u + 64u * size_t(log_n - DPF_ET_BITS) + 64u;  // h columns + CWL
+}
+
 extern "C" int dpf_key_serialize(const dpf_key *k, uint8_t *out, size_t cap, size_t *written) {
   if (!k || !out) return DPF_EINVAL;
   if (!key_ok(*k)) return DPF_EKEY;
-  const size_t need = dpf_key_wire_size(k->log_n);
+  const size_t need = dpf_key_wire_size_prf(k->log_n, k->prf);
   if (cap < need) return DPF_EINVAL;
   st32(out, k->magic);
   out[4] = k->version; out[5] = k->prf; out[6] = k->party; out[7] = k->log_n;
@@ -248,7 +282,7 @@ extern "C" int dpf_key_serialize(const dpf_key *k, uint8_t *out, size_t cap, siz
   st32(out + 12, 0);
   std::memcpy(out + 16, k->root, 16);
   // cw[d-1][t][c] is already laid out level-major, t, c: 64 bytes per level.
-  std::memcpy(out + 32, k->cw, 64u * k->log_n);
+  std::memcpy(out + 32, k->cw, need - 32);  // ET: h columns, then CWL in column h
   if (written) *written = need;
   return DPF_OK;
 }
@@ -263,8 +297,8 @@ extern "C" int dpf_key_deserialize(const uint8_t *in, size_t len, dpf_key *k) {
   t.cw_out = ld32(in + 8);
   t.reserved = ld32(in + 12);
   std::memcpy(t.root, in + 16, 16);
-  if (!key_ok(t) || len != dpf_key_wire_size(t.log_n)) return DPF_EKEY;
-  std::memcpy(t.cw, in + 32, 64u * t.log_n);
+  if (!key_ok(t) || len != dpf_key_wire_size_prf(t.log_n, t.prf)) return DPF_EKEY;
+  std::memcpy(t.cw, in + 32, len - 32);
   *k = t;
   return DPF_OK;
 }
@@ -287,7 +321,7 @@ extern "C" const char *dpf_strerror(int code) {
   }
 }
 
-extern "C" const char *dpf_version(void) { return "libdpfpir 0.1 (sm_100a, ChaCha20 GGM DPF, Z_2^32 shares)"; }
+extern "C" const char *dpf_version(void) { return "libdpfpir 0.2 (sm_100a, ChaCha20 / AES-128 / early-terminated ChaCha20 GGM DPF, Z_2^32 shares)"; }
 
 // Shared with eval.cu: key validation for the device path.
 namespace dpfpir {

@@ -25,6 +25,8 @@ LIB_PATH = os.environ.get("DPFPIR_LIB") or os.path.join(_PKG, "libdpfpir.so")
 DPF_MAX_LOG_N = 32
 DPF_PRF_CHACHA20 = 1
 DPF_PRF_AES128 = 2
+DPF_PRF_CHACHA20_ET = 3  # early-terminated leaves (R20), log_n >= 5
+DPF_ET_BITS = 4
 DPF_OK, DPF_EINVAL, DPF_EKEY, DPF_ENOMEM, DPF_ECUDA, DPF_EUNSUPPORTED = 0, -1, -2, -3, -4, -6
 
 
@@ -72,6 +74,8 @@ def lib() -> ctypes.CDLL:
     L.dpf_gen.argtypes = [u32, u64, u32, u32, vp, vp, vp]
     L.dpf_key_wire_size.argtypes = [u32]
     L.dpf_key_wire_size.restype = sz
+    L.dpf_key_wire_size_prf.argtypes = [u32, u32]
+    L.dpf_key_wire_size_prf.restype = sz
     L.dpf_key_serialize.argtypes = [vp, vp, sz, ctypes.POINTER(sz)]
     L.dpf_key_deserialize.argtypes = [vp, sz, vp]
     L.dpf_reconstruct.argtypes = [vp, vp, sz, vp]
@@ -91,6 +95,7 @@ def lib() -> ctypes.CDLL:
     L.dpf_eval_grouped_workspace_bytes.restype = sz
     L.dpf_eval_grouped.argtypes = [vp, u32, u32, u32, vp, sz, vp]
     L.dpf_last_eval_stats.argtypes = [vp]
+    L.dpf_eval_plan.argtypes = [u32, u32, u32, u64, u64, u32, ctypes.c_int, vp]
     L.dpf_kernel_timer_begin.argtypes = [u32]
     L.dpf_kernel_timer_read.argtypes = [vp, u32, vp]
     L.dpf_strerror.argtypes = [ctypes.c_int]
@@ -101,9 +106,9 @@ def lib() -> ctypes.CDLL:
     return L
 
 
-EXPORTED_SYMBOLS = ("dpf_gen", "dpf_key_wire_size", "dpf_key_serialize", "dpf_key_deserialize", "dpf_reconstruct",
+EXPORTED_SYMBOLS = ("dpf_gen", "dpf_key_wire_size", "dpf_key_wire_size_prf", "dpf_key_serialize", "dpf_key_deserialize", "dpf_reconstruct",
                     "dpf_eval_workspace_bytes", "dpf_eval_batch", "dpf_eval_batch_shard", "dpf_eval_batch_wire",
-                    "dpf_serve_batch", "dpf_eval_leaves", "dpf_last_eval_stats", "dpf_kernel_timer_begin",
+                    "dpf_serve_batch", "dpf_eval_leaves", "dpf_last_eval_stats", "dpf_eval_plan", "dpf_kernel_timer_begin",
                     "dpf_table_packed_bytes", "dpf_table_pack", "dpf_eval_batch_packed", "dpf_eval_batch_wire_packed",
                     "dpf_eval_grouped_workspace_bytes", "dpf_eval_grouped",
                     "dpf_kernel_timer_read", "dpf_strerror", "dpf_version")
@@ -177,12 +182,12 @@ def gen(log_n: int, alpha: int, beta: int = 1, rng_seed: Optional[bytes] = None,
     return k0, k1
 
 
-def key_wire_size(log_n: int) -> int:
-    return lib().dpf_key_wire_size(log_n)
+def key_wire_size(log_n: int, prf: int = DPF_PRF_CHACHA20) -> int:
+    return lib().dpf_key_wire_size_prf(log_n, prf)
 
 
 def key_serialize(k: DpfKey) -> bytes:
-    n = key_wire_size(k.log_n)
+    n = key_wire_size(k.log_n, k.prf)
     buf = ctypes.create_string_buffer(max(n, 1))
     written = ctypes.c_size_t(0)
     _check(lib().dpf_key_serialize(ctypes.byref(k), buf, n, ctypes.byref(written)), "dpf_key_serialize")
@@ -265,9 +270,9 @@ def eval_batch(keys, table, out=None, workspace=None, stream=None):
 
 
 def keys_to_wire(keys) -> np.ndarray:
-    """Serialize a key batch into consecutive wire records (uint8 [B, 32+64n])."""
+    """Serialize a key batch into consecutive wire records (uint8 [B, key_wire_size(n, prf)])."""
     kb = _as_batch(keys)
-    w = key_wire_size(kb.log_n)
+    w = key_wire_size(kb.log_n, kb.prf)
     out = np.zeros((len(kb), w), np.uint8)
     written = ctypes.c_size_t(0)
     for i in range(len(kb)):
@@ -414,7 +419,7 @@ def eval_leaves(keys, device="cuda", stream=None):
     kb = _as_batch(keys)
     B, n = len(kb), kb.log_n
     out = torch.empty((B, 1 << n), dtype=torch.int32, device=device)
-    ws = _workspace(B * key_wire_size(n) + 256, out.device)
+    ws = _workspace(B * key_wire_size(n, kb.prf) + 256, out.device)
     _check(lib().dpf_eval_leaves(kb.ptr, B, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
            "dpf_eval_leaves")
     return out
@@ -423,6 +428,14 @@ def eval_leaves(keys, device="cuda", stream=None):
 def last_eval_stats() -> dict:
     s = DpfEvalStats()
     _check(lib().dpf_last_eval_stats(ctypes.byref(s)), "dpf_last_eval_stats")
+    return {f: getattr(s, f) for f, _ in DpfEvalStats._fields_}
+
+
+def eval_plan(B: int, log_n: int, rows: int, D: int, prf: int = DPF_PRF_CHACHA20, row_begin: int = 0,
+              packed: bool = False) -> dict:
+    """dpf_eval_plan: the launch plan (host only, no device calls)."""
+    s = DpfEvalStats()
+    _check(lib().dpf_eval_plan(B, log_n, prf, row_begin, rows, D, int(packed), ctypes.byref(s)), "dpf_eval_plan")
     return {f: getattr(s, f) for f, _ in DpfEvalStats._fields_}
 
 

@@ -156,3 +156,73 @@ def test_planner_accepts_every_valid_shape(lib):
                 if dpfpir.eval_workspace_bytes(B, n, rows, D) == 0:
                     bad.append((D, B, n, rows))
     assert not bad, bad[:10]
+
+
+# ---------------------------------------------------------------- early termination (row f4, R20)
+
+def test_gen_et_equals_oracle_gen(lib, oracle):
+    r = np.random.default_rng(44)
+    for n in (5, 6, 10, 17, 20, 32):
+        alpha = int(r.integers(0, 1 << n))
+        beta = int(r.integers(0, 1 << 32))
+        seed = bytes(r.integers(0, 256, 32, dtype=np.uint8))
+        k0, k1 = dpfpir.gen(n, alpha, beta, seed, prf=dpfpir.DPF_PRF_CHACHA20_ET)
+        o0, o1 = oracle.gen(n, alpha, beta, seed, prf=oracle.PRF_CHACHA20_ET)
+        assert dpfpir.key_serialize(k0) == oracle.key_to_wire(o0)
+        assert dpfpir.key_serialize(k1) == oracle.key_to_wire(o1)
+
+
+def test_et_key_codec_and_errors(lib):
+    ET = dpfpir.DPF_PRF_CHACHA20_ET
+    assert dpfpir.key_wire_size(20, ET) == 32 + 64 * 17
+    assert dpfpir.key_wire_size(4, ET) == 0 and dpfpir.key_wire_size(33, ET) == 0
+    assert dpfpir.key_wire_size(20, 9) == 0
+    k0, k1 = dpfpir.gen(20, 777, 1, bytes(range(32)), prf=ET)
+    w = dpfpir.key_serialize(k1)
+    assert len(w) == 32 + 64 * 17 and w[5] == ET
+    assert dpfpir.key_serialize(dpfpir.key_deserialize(w)) == w
+    with pytest.raises(dpfpir.DpfError):
+        dpfpir.key_deserialize(w + bytes(64))  # a standard-length payload is not an ET key
+    bad = bytearray(w)
+    bad[8] = 1  # ET keys carry cw_out = 0
+    with pytest.raises(dpfpir.DpfError) as e:
+        dpfpir.key_deserialize(bytes(bad))
+    assert e.value.code == dpfpir.DPF_EKEY
+    with pytest.raises(dpfpir.DpfError) as e:
+        dpfpir.gen(4, 3, prf=ET)  # needs h = log_n - 4 >= 1
+    assert e.value.code == dpfpir.DPF_EINVAL
+
+
+def test_et_gen_keys_satisfy_contract(lib, oracle):
+    for alpha in (0, 17, 255, 200):
+        k0, k1 = dpfpir.gen(8, alpha, 9, bytes(32), prf=dpfpir.DPF_PRF_CHACHA20_ET)
+        y = oracle.eval_full(oracle.key_from_wire(dpfpir.key_serialize(k0))) + \
+            oracle.eval_full(oracle.key_from_wire(dpfpir.key_serialize(k1)))
+        want = np.zeros(256, np.uint32)
+        want[alpha] = 9
+        np.testing.assert_array_equal(y, want)
+
+
+def test_planner_all_schemes_and_paths(lib):
+    """dpf_eval_plan (host only) finds a plan for every shape each path
+    accepts, and its block count is the closed form: N - 1 per key (R9) or
+    N/8 - 1 with early termination (R20) over a full power-of-two domain."""
+    ET = dpfpir.DPF_PRF_CHACHA20_ET
+    bad = []
+    for prf in (1, 2, ET):
+        for packed in (False, True):
+            Ds = range(128, 1025, 128) if packed else range(4, 1025, 28)
+            for D in Ds:
+                for B in (1, 17, 64, 256, 1000):
+                    for n, r0, rows in ((5, 0, 32), (6, 3, 50), (10, 0, 1000), (20, 0, 1 << 20), (24, 5, 1 << 23),
+                                        (32, (1 << 32) - 4096, 4096)):
+                        if packed and n < 3:
+                            continue
+                        try:
+                            dpfpir.eval_plan(B, n, rows, D, prf, r0, packed)
+                        except dpfpir.DpfError:
+                            bad.append((prf, packed, D, B, n, rows))
+    assert not bad, bad[:10]
+    for prf, per in ((1, (1 << 20) - 1), (ET, (1 << 17) - 1)):
+        for packed in (False, True):
+            assert dpfpir.eval_plan(256, 20, 1 << 20, 256, prf, 0, packed)["prf_blocks"] == 256 * per

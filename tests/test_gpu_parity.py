@@ -310,3 +310,98 @@ def test_deep_domains_small_shards(dp, oracle):
         ok = oracle.key_from_wire(dp.key_serialize(pairs[0][0]))
         y = np.array([oracle.eval_point(ok, r0 + j) for j in range(rows)], np.uint32)
         np.testing.assert_array_equal(s0[0], oracle.contract(y, T))
+
+
+# ---------------------------------------------------------------- early-terminated leaves (row f4, R20)
+
+ET = 3
+
+
+def make_et_keys(dp, oracle, n, alphas, seed, betas=None):
+    keys, okeys = [], []
+    for i, (a, s) in enumerate(zip(alphas, synth.gen_seeds(len(alphas), seed))):
+        beta = 1 if betas is None else int(betas[i])
+        k = dp.gen(n, int(a), beta, s, prf=ET)[i % 2]
+        keys.append(k)
+        okeys.append(oracle.key_from_wire(dp.key_serialize(k)))
+    return keys, okeys
+
+
+def test_et_leaves_match_oracle(dp, oracle):
+    for n, B in ((5, 2), (6, 3), (12, 2), (16, 1)):
+        keys, okeys = make_et_keys(dp, oracle, n, synth.alphas(B, 1 << n, n), 70 + n)
+        got = dp.as_u32(dp.eval_leaves(keys))
+        for b in range(B):
+            np.testing.assert_array_equal(got[b], oracle.eval_full(okeys[b]))
+
+
+@pytest.mark.parametrize("n,N,D,B", [
+    (5, 32, 4, 1), (6, 50, 16, 3), (9, 512, 64, 33), (12, 4096, 64, 37), (13, 5000, 32, 64), (10, 1000, 12, 7),
+    (14, 1 << 14, 256, 100), (15, 20000, 128, 40), (8, 256, 1024, 9), (16, 1 << 16, 64, 64), (11, 2047, 8, 2),
+])
+def test_et_parity_imad(dp, oracle, n, N, D, B):
+    T = synth.table(N, D, 4000 + n + D)
+    keys, okeys = make_et_keys(dp, oracle, n, synth.alphas(B, N, 4000 + n), 4000 + n + B,
+                               betas=synth.betas(B, n, random=True))
+    got = dp.as_u32(dp.eval_batch(keys, to_dev(T)))
+    np.testing.assert_array_equal(got, oracle.answer_batch(okeys, T, threads=8))
+
+
+@pytest.mark.parametrize("n,N,D,B", [
+    (12, 4096, 256, 32), (13, 8000, 128, 40), (14, 1 << 14, 256, 64), (10, 1000, 128, 5), (5, 32, 256, 1),
+    (11, 2047, 256, 100), (16, 1 << 16, 128, 33), (12, 3000, 384, 40), (11, 2048, 512, 70), (10, 1024, 1024, 20),
+    (6, 64, 128, 3),
+])
+def test_et_parity_tc(dp, oracle, n, N, D, B):
+    T = synth.table(N, D, 5000 + n + D)
+    keys, okeys = make_et_keys(dp, oracle, n, synth.alphas(B, N, 5000 + n), 5000 + n + B)
+    Td = to_dev(T)
+    got = dp.as_u32(dp.eval_batch_packed(keys, dp.table_pack(Td)))
+    want = oracle.answer_batch(okeys, T, threads=8)
+    np.testing.assert_array_equal(got, want)
+    np.testing.assert_array_equal(dp.as_u32(dp.eval_batch(keys, Td)), want)
+
+
+def test_et_shards_wire_and_reconstruct(dp, oracle):
+    n, N, D, B = 14, 12345, 128, 40
+    T = synth.table(N, D, 88)
+    al = synth.alphas(B, N, 88)
+    pairs = [dp.gen(n, int(a), 1, s, prf=ET) for a, s in zip(al, synth.gen_seeds(B, 88))]
+    Td = to_dev(T)
+    k0, k1 = [p[0] for p in pairs], [p[1] for p in pairs]
+    whole = dp.as_u32(dp.eval_batch(k0, Td))
+    ok = [oracle.key_from_wire(dp.key_serialize(k)) for k in k0[:8]]
+    np.testing.assert_array_equal(whole[:8], oracle.answer_batch(ok, T, threads=8))
+    wire = torch.from_numpy(dp.keys_to_wire(k0)).cuda()
+    np.testing.assert_array_equal(dp.as_u32(dp.eval_batch_wire(wire, n, Td, prf=ET)), whole)
+    pk = dp.table_pack(Td)
+    np.testing.assert_array_equal(dp.as_u32(dp.eval_batch_wire_packed(wire, n, pk, prf=ET)), whole)
+    for cuts in ([0, 4096, 8192, N], [0, 1, 777, 5000, 12000, N], [0, 7, 9, N]):  # cuts inside final nodes
+        acc = np.zeros_like(whole)
+        acc_tc = np.zeros_like(whole)
+        for lo, hi in zip(cuts[:-1], cuts[1:]):
+            acc += dp.as_u32(dp.eval_batch_shard(k0, to_dev(T[lo:hi]), lo))
+            acc_tc += dp.as_u32(dp.eval_batch_packed(k0, dp.table_pack(to_dev(T[lo:hi]), lo)))
+        np.testing.assert_array_equal(acc, whole)
+        np.testing.assert_array_equal(acc_tc, whole)
+    sh1 = dp.as_u32(dp.eval_batch(k1, Td))
+    np.testing.assert_array_equal(dp.reconstruct(whole, sh1), T[al.astype(np.int64)])
+
+
+def test_et_c3_full_size_sampled(dp, oracle):
+    """Config c3's shape (2^20 x 256, B = 256) with ET keys in the bench's launch
+    configuration (tcgen05 path); every query reconstructs, sampled keys equal
+    the oracle, and the device computes N/8 - 1 blocks per key."""
+    w = synth.CONFIGS["c3"]
+    T = synth.table(w.N, w.D, w.seed)
+    al = synth.alphas(w.B, w.N, w.seed)
+    pairs = [dp.gen(w.log_n, int(a), 1, s, prf=ET) for a, s in zip(al, synth.gen_seeds(w.B, w.seed))]
+    pk = dp.table_pack(to_dev(T))
+    sh0 = dp.as_u32(dp.eval_batch_packed([p[0] for p in pairs], pk))
+    assert dp.last_eval_stats()["prf_blocks"] == w.B * (w.N // 8 - 1)
+    sh1 = dp.as_u32(dp.eval_batch_packed([p[1] for p in pairs], pk))
+    np.testing.assert_array_equal(dp.reconstruct(sh0, sh1), T[al.astype(np.int64)])
+    sample = [0, 77, 255]
+    want = oracle.answer_batch([oracle.key_from_wire(dp.key_serialize(pairs[b][0])) for b in sample], T, threads=3)
+    for i, b in enumerate(sample):
+        np.testing.assert_array_equal(sh0[b], want[i])
