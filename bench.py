@@ -45,7 +45,15 @@ import synth  # noqa: E402
 # (bitsliced, table-free) = the compiled ALU instructions of one node's two
 # encryptions + key schedule in this formulation (9 x 411 + 336 + 40 setup;
 # Boyar-Peralta S-box = 95 LOP3): a better circuit would lower it.
-ALU_OPS_PER_BLOCK = {"chacha20": 640, "aes128": 4075}
+ALU_OPS_PER_BLOCK = {"chacha20": 640, "aes128": 4075, "chacha20_et": 640}
+# leaf rows per tree leaf: early termination (R20) ends the tree at final
+# nodes of 16 rows, each converted by one more ChaCha20 block (counter 1).
+ET_BITS = {"chacha20": 0, "aes128": 0, "chacha20_et": 4}
+
+
+def prf_code(dpfpir, name):
+    return {"chacha20": dpfpir.DPF_PRF_CHACHA20, "aes128": dpfpir.DPF_PRF_AES128,
+            "chacha20_et": dpfpir.DPF_PRF_CHACHA20_ET}[name]
 METRIC = "DPF-PIR queries/sec"
 UNIT = "queries/s"
 
@@ -149,7 +157,7 @@ def run_reference(args, rank, world):
     from paper_2301_10904_b200 import build as pbuild
     from paper_2301_10904_b200 import dpfpir
     pbuild.build()  # host-side Gen only (client work, outside the timed region)
-    prf = dpfpir.DPF_PRF_AES128 if args.prf == "aes128" else dpfpir.DPF_PRF_CHACHA20
+    prf = prf_code(dpfpir, args.prf)
     _, pairs = make_keys(w, dpfpir, prf)
     wire = dpfpir.keys_to_wire([p[0] for p in pairs])
     T = synth.table(w.N, w.D, w.seed)
@@ -188,8 +196,9 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--prf", default="chacha20", choices=["chacha20", "aes128"],
-                    help="tree PRF (chacha20 = the paper's fastest standard PRF, Table 5; aes128 = its baseline)")
+    ap.add_argument("--prf", default="chacha20", choices=["chacha20", "aes128", "chacha20_et"],
+                    help="tree PRF (chacha20 = the paper's fastest standard PRF, Table 5; aes128 = its baseline; "
+                         "chacha20_et = ChaCha20 with early-terminated 16-row leaves, DESIGN.md R20)")
     ap.add_argument("--table", default="auto", choices=["auto", "packed", "rowmajor"],
                     help="packed = limb-packed table + tcgen05 contraction (D % 128 == 0); rowmajor = IMAD path")
     ap.add_argument("--e2e-steps", type=int, default=None)
@@ -222,7 +231,7 @@ def main():
     # server state: the table is re-laid-out once into u8 limb planes (outside every timed region)
     Tp = dpfpir.table_pack(T, r0) if use_packed else None
     torch.cuda.synchronize()
-    prf = dpfpir.DPF_PRF_AES128 if args.prf == "aes128" else dpfpir.DPF_PRF_CHACHA20
+    prf = prf_code(dpfpir, args.prf)
     al, pairs = make_keys(w, dpfpir, prf)
     keys0 = dpfpir.KeyBatch.from_keys([p[0] for p in pairs])
     wire_host = dpfpir.keys_to_wire(keys0)
@@ -319,21 +328,25 @@ def main():
 
     # ---- roofline of the dominant kernel (fused eval), live CUDA-event time
     pk = peaks()
-    m = w.log_n - stats["frontier_depth"]
-    fused_blocks = w.B * (rows >> m) * ((1 << m) - 1)  # algorithmic blocks per launch (no padding)
+    v = ET_BITS[args.prf]
+    m = w.log_n - v - stats["frontier_depth"]
+    # algorithmic blocks per launch (no padding): the subtrees' internal nodes,
+    # plus one Convert block per final node with early termination
+    fused_blocks = w.B * ((rows >> v) >> m) * ((1 << m) - 1 + ((1 << m) if v else 0))
     kern_avg_ms = sum(kernel_ms) / len(kernel_ms)
     alu_peak = 148 * 64 * pk["sm_max_mhz"] * 1e6  # ALU-pipe lane-ops/s
     ops_per_block = ALU_OPS_PER_BLOCK[args.prf]
     achieved = ops_per_block * fused_blocks / (kern_avg_ms * 1e-3)
-    qps_roof = alu_peak / (ops_per_block * (rows - 1 + g))
+    tree_blocks = (rows - 1 + g) if not v else (2 * (rows >> v) - 1 + g)
+    qps_roof = alu_peak / (ops_per_block * tree_blocks)
     hbm_qps_roof = G * pk["hbm_gbs"] * 1e9 * w.B / (4.0 * w.N * w.D)
-    traffic = _ncu_traffic(w.name)
+    traffic = _ncu_traffic(w.name if args.prf == "chacha20" else "%s_%s" % (w.name, args.prf))
     roofline = {
         "bound": "alu", "achieved": achieved * 1e-12, "peak": alu_peak * 1e-12, "unit": "Tops/s",
         "frac": achieved / alu_peak, "traffic": traffic,
         "kernel": "fused_eval_tc_kernel" if use_packed else "fused_eval_kernel", "kernel_ms": kern_avg_ms,
         "kernel_share_of_step": kern_avg_ms / ms_per_step,
-        "ops": ("640 ALU-pipe int32 ops (LOP3 xor + SHF rotate) per ChaCha20 block" if args.prf == "chacha20" else
+        "ops": ("640 ALU-pipe int32 ops (LOP3 xor + SHF rotate) per ChaCha20 block" if args.prf != "aes128" else
                 "4075 ALU-pipe ops per bitsliced AES-128 node (2 blocks + key schedule)") +
                " x %d blocks per launch" % fused_blocks,
         "peak_basis": "148 SMs x 64 ALU lanes/clk x %.0f MHz (%s)" % (pk["sm_max_mhz"], pk["source"]),

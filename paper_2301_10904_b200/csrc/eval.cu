@@ -236,6 +236,19 @@ __device__ __forceinline__ GroupDesc group_of(const FusedParams &p, uint32_t ite
   return p.groups[lo];
 }
 
+// A CTA runs items item, item + gridDim.x, ...; consecutive ones of the same
+// group and key tile add into the same answers, so their partial sums stay in
+// the accumulators (registers / TMEM) and are flushed once at the end of the
+// run (the host picks a grid that is a multiple of the key-tile count when
+// that is free, which makes a CTA's key tile constant).  Exact for any
+// grouping: Z_2^32 addition is associative.
+__device__ __forceinline__ bool run_continues(const FusedParams &p, const GroupDesc &g, uint32_t kt, uint32_t next) {
+  if (next >= p.n_items) return false;
+  if (p.n_groups <= 1) return (next - g.item_base) % g.n_ktiles == kt;
+  const GroupDesc h = group_of(p, next);
+  return h.item_base == g.item_base && (next - h.item_base) % h.n_ktiles == kt;
+}
+
 template <int NP, int NC>
 struct Smem {
   static constexpr int kThreads = 32 * (NP + NC + 1);
@@ -445,8 +458,8 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
         }
         if (wseq + 2 < total_w) named_arrive(3 + stage, kEmptyThreads);
       }
-      // a6/a7: flush this item's partial answers, party sign applied once.
-      if (active) {
+      // a6/a7: flush the run's partial answers, party sign applied once.
+      if (active && !run_continues(p, g, kt, item + gridDim.x)) {
 #pragma unroll
         for (int k = 0; k < KPW; ++k) {
           const uint32_t b = kt * p.Kt + key0 + k;
@@ -768,6 +781,23 @@ uint32_t choose_m_target(const Plan &pl, uint32_t n, uint32_t m_min, uint32_t m_
   return best;
 }
 
+// Persistent grid: one CTA per SM.  When the key-tile count divides a grid
+// of (almost) every SM, each CTA keeps one key tile for all its items, so
+// its accumulators are flushed once instead of once per item (run_continues).
+// DPF_GRID_ALIGN=1 forces the aligned grid even when it idles SMs, =0 never.
+uint32_t choose_grid(uint32_t n_items, uint32_t n_ktiles) {
+  const uint32_t sms = uint32_t(num_sms());
+  if (n_items <= sms) return n_items;
+  static const int force = [] {
+    const char *e = getenv("DPF_GRID_ALIGN");
+    return e ? atoi(e) : -1;
+  }();
+  const uint32_t aligned = n_ktiles <= sms ? (sms / n_ktiles) * n_ktiles : sms;
+  if (force == 0) return sms;
+  if (force == 1 || aligned == sms) return aligned;
+  return sms;
+}
+
 // Window / T-ring sizing for the IMAD kernel; false if SMEM does not fit.
 // Rows per window unit: a leaf pair, or one final node with early termination.
 inline uint32_t unit_rows(const Plan &pl) { return pl.v ? (1u << pl.v) : 2u; }
@@ -854,16 +884,35 @@ int make_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D
     if (W == 1) return DPF_EINVAL;
   }
   pl.nwin = nq / pl.W;
-  pl.grid = std::min<uint32_t>(pl.n_items, uint32_t(num_sms()));
+  pl.grid = choose_grid(pl.n_items, pl.n_ktiles);
   pl.prf_blocks = count_blocks(pl, B);
   return DPF_OK;
 }
 
 constexpr uint32_t kTcNP = 16;   // producer warps (4 per SMSP)
 constexpr uint32_t kTcNSY = 2;   // y-ring depth
+// Early termination (R20) fills a y stage with ~2 ChaCha20 blocks per thread
+// instead of ~8, so the MMA side (80 UMMAs per stage) needs more slack: a
+// 3-deep y ring (measured at c3: 0.58 -> 0.61 of the ALU roofline).
+// DPF_TC_NSY=2 restores 2 (tuning).
+inline uint32_t tc_y_stages(bool et) {
+  static const uint32_t v = [] {
+    const char *e = getenv("DPF_TC_NSY");
+    return (e && atoi(e) == 2) ? 2u : 3u;
+  }();
+  return et ? v : kTcNSY;
+}
 // T-ring depth (16 KB entries).  8 entries measured no faster than 4 at
 // D = 512/1024, so the SMEM goes to the DFS stack instead.
-inline uint32_t tc_t_stages(uint32_t) { return 4u; }
+// DPF_TC_NST=8 selects an 8-deep ring (tuning).
+inline uint32_t tc_t_stages(uint32_t) {
+  static const uint32_t v = [] {
+    const char *e = getenv("DPF_TC_NST");
+    const int n = e ? atoi(e) : 4;
+    return (n == 6 || n == 8) ? uint32_t(n) : 4u;
+  }();
+  return v;
+}
 
 // tcgen05 plan (limb-packed table), D a multiple of 128 up to 1024:
 // Kt = MMA N = 64/32/16 keys so that 4 limb accumulators x D/128 tiles x Kt
@@ -878,7 +927,7 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
   pl.r0a = r0 & ~7ull;
   pl.packed_rows = ((pl.r1 + 7) & ~7ull) - pl.r0a;
   pl.Kt = D <= 256 ? 64 : D <= 512 ? 32 : 16;
-  pl.nsy = kTcNSY;
+  pl.nsy = tc_y_stages(et);
   pl.Ft = 32 * kTcNP / pl.Kt;
   pl.tasks = pl.Kt * pl.Ft;
   pl.n_ktiles = (B + pl.Kt - 1) / pl.Kt;
@@ -890,7 +939,7 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
   pl.y_stage_bytes = 4 * pl.Kt * Kw;
   // SMEM: T ring + y ring + the DFS stack (16 B per producer thread per level)
   pl.nst = tc_t_stages(D);
-  const size_t fixed = 1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(kTcNSY) * pl.y_stage_bytes;
+  const size_t fixed = 1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(pl.nsy) * pl.y_stage_bytes;
   const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / (32 * kTcNP * 16)));
   const uint32_t m_min = et ? 1 : 3;
   if (m_cap < m_min || n < m_min) return DPF_EINVAL;
@@ -909,7 +958,7 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
   while (pl.tmem_cols < cols) pl.tmem_cols <<= 1;
   pl.smem_bytes = fixed + size_t(pl.m) * 32 * kTcNP * 16;  // stack slots 1..m-1 (slot 0 unused)
   if (pl.smem_bytes > 227 * 1024) return DPF_EINVAL;
-  pl.grid = std::min<uint32_t>(pl.n_items, uint32_t(num_sms()));
+  pl.grid = choose_grid(pl.n_items, pl.n_ktiles);
   pl.prf_blocks = count_blocks(pl, B);
   return DPF_OK;
 }
@@ -1042,9 +1091,26 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
     tp.f = p;
     tp.y_stage_bytes = pl.y_stage_bytes;
     tp.tmem_cols = pl.tmem_cols;
-    auto fn = pl.prf == DPF_PRF_AES128        ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4>
-              : pl.prf == DPF_PRF_CHACHA20_ET ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSY, 4>
-                                              : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4>;
+    static const uint32_t spin = [] {
+      const char *e = getenv("DPF_LOADER_SPIN");
+      return uint32_t(e && atoi(e) == 1);
+    }();
+    tp.loader_spin = spin;
+    static const uint32_t nomma = [] {
+      const char *e = getenv("DPF_DEBUG_NOMMA");
+      return uint32_t(e && atoi(e) == 1);
+    }();
+    tp.debug_nomma = nomma;
+    using TcFn = void (*)(const dev::TcParams);
+    TcFn fn;
+    if (pl.prf == DPF_PRF_AES128) fn = &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4>;
+    else if (pl.prf == DPF_PRF_CHACHA20_ET)
+      fn = pl.nsy == 3 ? (pl.nst == 6 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 3, 6>
+                                      : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 3, 4>)
+                       : (pl.nst == 8 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSY, 8>
+                                      : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSY, 4>);
+    else fn = pl.nst == 8 ? &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 8>
+                          : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4>;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
       return DPF_ECUDA;
     if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);

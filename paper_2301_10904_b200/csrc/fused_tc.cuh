@@ -30,6 +30,8 @@ namespace dev {
 struct TcParams {
   FusedParams f;  // groups: T = the limb-packed rows [r0a, r0a + packed_rows)
   uint32_t y_stage_bytes, tmem_cols;
+  uint32_t loader_spin;  // T loader waits by polling (try_wait) instead of sleeping back-off
+  uint32_t debug_nomma;  // tuning only: skip the MMAs (wrong answers; isolates the producer rate)
 };
 
 constexpr uint32_t kTcTStageBytes = 16384;  // 32 leaves x 128 columns x 4 limbs
@@ -272,12 +274,16 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
     const uint32_t idesc = umma_idesc_u8(p.Kt);
     const uint32_t b_lbo = (p.Kt >> 3) * 128u;
     const uint32_t ybase = smem_u32(ybuf), tbase = smem_u32(tbuf);
-    uint32_t wseq = 0, tseq = 0, it = 0;
-    for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+    // nf = accumulator flushes so far; fresh = this item starts a run (the
+    // first MMA of the run overwrites TMEM, later ones accumulate)
+    uint32_t wseq = 0, tseq = 0, nf = 0;
+    bool fresh = true;
+    for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       const GroupDesc g = group_of(p, item);
       const uint32_t kt = (item - g.item_base) % g.n_ktiles;
+      const bool last = !run_continues(p, g, kt, item + gridDim.x);
       if (q == 0) {
-        if (it > 0) mbar_wait(accempty, (it - 1) & 1);  // epilogue drained the accumulators
+        if (fresh && nf > 0) mbar_wait(accempty, (nf - 1) & 1);  // epilogue drained the accumulators
         for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
           const uint32_t ys = wseq % NSY;
           named_sync(1 + ys, 32 * (NP + 1));
@@ -288,7 +294,7 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
               const uint32_t ts = tseq % NST, tuse = tseq / NST;
               mbar_wait(&tfull[ts], tuse & 1);
               tc_fence_after();
-              if (lane == 0) {
+              if (lane == 0 && !tp.debug_nomma) {
                 const uint32_t tb = tbase + ts * kTcTStageBytes;
 #pragma unroll
                 for (uint32_t s = 0; s < 4; ++s) {
@@ -297,25 +303,28 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
                     const uint32_t k = s - i;
                     const uint64_t ad = umma_desc(tb + k * 1024u, 4096u, 128u);
                     const uint64_t bd = umma_desc(yb + i * ybplane + cc * 2u * b_lbo, b_lbo, 128u);
-                    const uint32_t acc = (win == 0 && cc == 0 && i == 0) ? 0u : 1u;
+                    const uint32_t acc = (fresh && win == 0 && cc == 0 && i == 0) ? 0u : 1u;
                     umma_u8(tmem_base + (dt * 4 + s) * p.Kt, ad, bd, idesc, acc);
                   }
                 }
-                umma_commit(&tempty[ts]);  // T entry reusable once these MMAs finish
               }
+              if (lane == 0) umma_commit(&tempty[ts]);  // T entry reusable once these MMAs finish
               __syncwarp();
             }
           }
           if (lane == 0) {
             umma_commit(&yempty[ys]);                     // y stage reusable
-            if (win + 1 == g.nwin) umma_commit(accfull);  // item's accumulators complete
+            if (last && win + 1 == g.nwin) umma_commit(accfull);  // run's accumulators complete
           }
           __syncwarp();
         }
       }
+      fresh = last;
+      if (!last) continue;
       // epilogue: all NC warps, TMEM lanes 32q..32q+31 = columns d.  Only the
       // MMA warp polls the commit barrier; the others sleep in bar.sync.
-      if (q == 0) mbar_wait(accfull, it & 1);
+      if (q == 0) mbar_wait(accfull, nf & 1);
+      ++nf;
       named_sync(NSY + 1, 32 * NC);
       tc_fence_after();
       for (uint32_t dt = 0; dt < n_dt; ++dt) {
@@ -367,7 +376,10 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
           const uint32_t total = __popc(__ballot_sync(0xFFFFFFFFu, ok)) * 4096u;
           for (uint32_t dt = 0; dt < n_dt; ++dt, ++tseq) {
             const uint32_t ts = tseq % NST, tuse = tseq / NST;
-            if (tuse > 0) mbar_wait_backoff(&tempty[ts], (tuse - 1) & 1);
+            if (tuse > 0) {
+              if (tp.loader_spin) mbar_wait(&tempty[ts], (tuse - 1) & 1);
+              else mbar_wait_backoff(&tempty[ts], (tuse - 1) & 1);
+            }
             if (lane == 0) mbar_arrive_expect_tx(&tfull[ts], total);
             __syncwarp();
             if (ok)

@@ -405,3 +405,28 @@ def test_et_c3_full_size_sampled(dp, oracle):
     want = oracle.answer_batch([oracle.key_from_wire(dp.key_serialize(pairs[b][0])) for b in sample], T, threads=3)
     for i, b in enumerate(sample):
         np.testing.assert_array_equal(sh0[b], want[i])
+
+
+@pytest.mark.parametrize("n,N,D,B,prf,packed", [
+    (14, 1 << 14, 64, 37 * 32, 1, False),   # IMAD: 37 key tiles, aligned grid of 148
+    (14, (1 << 14) - 5, 128, 256, 1, True),   # tcgen05: 4 key tiles, ragged N
+    (16, 60000, 256, 256, 3, True),         # early termination, tcgen05
+    (18, 250000, 64, 64, 3, False),         # early termination, IMAD: 2 key tiles, ragged N
+])
+def test_accumulator_runs_across_items(dp, oracle, n, N, D, B, prf, packed):
+    """A CTA keeps its accumulators across consecutive items of one key tile
+    and flushes once per run (run_continues): many items per CTA, exact."""
+    plan = dp.eval_plan(B, n, N, D, prf=prf, packed=packed)
+    assert plan["work_items"] > plan["grid"]
+    n_kt = -(-B // plan["keys_per_tile"])
+    assert plan["grid"] % n_kt == 0  # every CTA stays on one key tile
+    T = synth.table(N, D, 9100 + n)
+    al = synth.alphas(B, N, 9100 + n)
+    if prf == 3:
+        keys, okeys = make_et_keys(dp, oracle, n, al, 9200 + n)
+    else:
+        keys, okeys = make_keys(dp, oracle, n, al, 9200 + n)
+    Td = to_dev(T)
+    got = dp.as_u32(dp.eval_batch_packed(keys, dp.table_pack(Td)) if packed else dp.eval_batch(keys, Td))
+    assert dp.last_eval_stats()["grid"] == plan["grid"]
+    np.testing.assert_array_equal(got, oracle.answer_batch(okeys, T, threads=16))
