@@ -227,7 +227,7 @@ def main():
 
     T_host = synth.table_rows(w.N, w.D, w.seed, r0, r0 + rows)
     T = torch.from_numpy(T_host.view(np.int32)).to(dev)
-    use_packed = args.table == "packed" or (args.table == "auto" and w.D % 128 == 0 and w.D <= 1024 and w.B >= 32)
+    use_packed = args.table == "packed" or (args.table == "auto" and w.D <= 1024 and w.B >= 32)
     # server state: the table is re-laid-out once into u8 limb planes (outside every timed region)
     Tp = dpfpir.table_pack(T, r0) if use_packed else None
     torch.cuda.synchronize()

@@ -180,16 +180,18 @@ int dpf_eval_batch_wire(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n
  * y*t mod 2^32 = sum_{s<4} 2^(8s) sum_{i+k=s} y_i t_k (DESIGN.md
  * "tcgen05 contraction").  The table must first be re-laid-out once (server
  * state) by dpf_table_pack into blocks of 8 rows:
- *   block b (rows 8b'..8b'+7 with b' = row_begin/8 + b), 32*D bytes,
- *   [d-tile t < D/128][limb k < 4][chunk c < 8][row r < 8][16 bytes: byte k
+ *   block b (rows 8b'..8b'+7 with b' = row_begin/8 + b), 32*Dp bytes,
+ *   [d-tile t < Dp/128][limb k < 4][chunk c < 8][row r < 8][16 bytes: byte k
  *   of T[row][128t + 16c .. 128t + 16c + 15]]
- * Rows of the 8-row blocks outside [row_begin, row_begin+row_count) are
- * zero.  Requirements: D a multiple of 128, D <= 1024, log_n >= 3.  The
- * kernel tiles 64 keys per work item (32 for D <= 512, 16 above), so
- * batches of that many keys use it fully. */
+ * with Dp = D rounded up to a multiple of 128.  Rows of the 8-row blocks
+ * outside [row_begin, row_begin+row_count) and columns >= D are zero.
+ * Requirements: D % 4 == 0, D <= 1024, log_n >= 3.  The kernel tiles Kt keys
+ * per work item, Kt = 128 / 64 / 32 / 16 for Dp = 128 / 256 / 384-512 /
+ * 640-1024 (4 limb accumulators x Dp/128 tiles x Kt columns <= 512 TMEM
+ * columns), so batches of Kt keys use it fully. */
 
 /* Bytes of the packed copy of rows [row_begin, row_begin+row_count) (8-row
- * aligned), 0 if D % 128 != 0 or row_count == 0. */
+ * aligned, 4*Dp bytes per row), 0 if D % 4 != 0, D > 1024 or row_count == 0. */
 size_t dpf_table_packed_bytes(uint64_t row_begin, uint64_t row_count, uint32_t D);
 
 /* Pack a row-major DEVICE table shard (row_count x D uint32, pointing at row
@@ -200,7 +202,7 @@ int dpf_table_pack(const uint32_t *table_shard, uint64_t row_begin, uint64_t row
 
 /* As dpf_eval_batch_shard / dpf_eval_batch_wire, reading the packed table
  * (`packed` from dpf_table_pack with the same row_begin, row_count, D).
- * Same ownership and errors; DPF_EINVAL if D % 128 != 0 or D > 1024. */
+ * Same ownership and errors; DPF_EINVAL if D % 4 != 0 or D > 1024. */
 int dpf_eval_batch_packed(const dpf_key *keys, uint32_t B, const void *packed, uint64_t row_begin,
                           uint64_t row_count, uint32_t D, uint32_t *partial_shares, void *workspace,
                           size_t workspace_bytes, void *stream);

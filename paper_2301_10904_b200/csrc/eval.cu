@@ -920,13 +920,20 @@ inline uint32_t tc_t_stages(uint32_t) {
 // W = 4 leaf pairs per node per window (one 8-row packed block).
 int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et = false) {
   std::memset(&pl, 0, sizeof pl);
-  if (D % 128 || D > 1024 || log_n < 3) return DPF_EINVAL;
+  if (D == 0 || D % 4 || D > 1024 || log_n < 3) return DPF_EINVAL;
   pl.tc = true;
   set_ranges(pl, log_n, r0, rows, et);
   const uint32_t n = pl.n;
   pl.r0a = r0 & ~7ull;
   pl.packed_rows = ((pl.r1 + 7) & ~7ull) - pl.r0a;
-  pl.Kt = D <= 256 ? 64 : D <= 512 ? 32 : 16;
+  // Kt = MMA N: the largest power of two <= 128 whose 4 limb accumulators x
+  // n_dt d-tiles x Kt columns fit the 512 TMEM columns (D <= 128: 128 keys,
+  // 256: 64, 512: 32, 1024: 16).  D is padded to whole 128-column d-tiles.
+  const uint32_t n_dt = (D + 127) / 128;
+  pl.Kt = 128;
+  while (4 * n_dt * pl.Kt > 512) pl.Kt >>= 1;
+  // small batches: no wider than the batch (MMA N >= 16)
+  while (pl.Kt > 16 && pl.Kt / 2 >= B) pl.Kt >>= 1;
   pl.nsy = tc_y_stages(et);
   pl.Ft = 32 * kTcNP / pl.Kt;
   pl.tasks = pl.Kt * pl.Ft;
@@ -953,7 +960,7 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
   pl.n_items = uint32_t(items);
   pl.W = W;
   pl.nwin = (et ? (1u << pl.m) : (1u << (pl.m - 1))) / W;
-  const uint32_t cols = (D / 128) * 4 * pl.Kt;
+  const uint32_t cols = n_dt * 4 * pl.Kt;
   pl.tmem_cols = 32;
   while (pl.tmem_cols < cols) pl.tmem_cols <<= 1;
   pl.smem_bytes = fixed + size_t(pl.m) * 32 * kTcNP * 16;  // stack slots 1..m-1 (slot 0 unused)
@@ -1277,23 +1284,26 @@ extern "C" int dpf_eval_plan(uint32_t B, uint32_t log_n, uint32_t prf, uint64_t 
   return DPF_OK;
 }
 
+// Packed width: D padded to whole 128-column d-tiles (padding columns are zero).
+inline uint32_t packed_width(uint32_t D) { return (D + 127) & ~127u; }
+
 extern "C" size_t dpf_table_packed_bytes(uint64_t row_begin, uint64_t row_count, uint32_t D) {
-  if (row_count == 0 || D == 0 || D % 128) return 0;
+  if (row_count == 0 || D == 0 || D % 4 || D > 1024) return 0;
   const uint64_t r0a = row_begin & ~7ull, r1a = (row_begin + row_count + 7) & ~7ull;
-  return size_t((r1a - r0a) * 4ull * D);
+  return size_t((r1a - r0a) * 4ull * packed_width(D));
 }
 
 extern "C" int dpf_table_pack(const uint32_t *table_shard, uint64_t row_begin, uint64_t row_count, uint32_t D,
                               void *packed, void *stream) {
-  if (!table_shard || !packed || row_count == 0 || D == 0 || D % 128) return DPF_EINVAL;
+  if (!table_shard || !packed || row_count == 0 || D == 0 || D % 4 || D > 1024) return DPF_EINVAL;
   if ((reinterpret_cast<uintptr_t>(table_shard) & 15) || (reinterpret_cast<uintptr_t>(packed) & 15))
     return DPF_EINVAL;
   const uint64_t r0a = row_begin & ~7ull, r1a = (row_begin + row_count + 7) & ~7ull;
   const uint64_t nblocks = (r1a - r0a) / 8;
-  const uint64_t total = nblocks * 8 * (D / 16);
+  const uint64_t total = nblocks * 8 * (packed_width(D) / 16);
   const uint32_t grid = uint32_t(std::min<uint64_t>((total + 255) / 256, 148ull * 32));
   dev::table_pack_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
-      table_shard, row_begin, row_begin + row_count, r0a, nblocks, D, static_cast<uint8_t *>(packed));
+      table_shard, row_begin, row_begin + row_count, r0a, nblocks, D, packed_width(D), static_cast<uint8_t *>(packed));
   return cudaGetLastError() == cudaSuccess ? DPF_OK : DPF_ECUDA;
 }
 

@@ -163,6 +163,7 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
   constexpr uint32_t V = Prf::kEt ? 4u : 0u;  // log2(rows per subtree leaf), R20
   const uint32_t ybplane = p.Kt * Kw;  // bytes per y limb plane
   const uint32_t D = p.D;
+  const uint32_t Dp = (D + 127) & ~127u;  // packed width: whole 128-column d-tiles
 
   if (warp < NP) {
     // ------------------------------------------------------------ producers
@@ -270,7 +271,7 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
   } else if (warp < NP + NC) {
     // ------------------------------------------------ MMA issuer + epilogue
     const uint32_t q = warp - NP;  // TMEM lane quarter
-    const uint32_t n_dt = D / 128, n_cc = Kw / 32;
+    const uint32_t n_dt = Dp / 128, n_cc = Kw / 32;
     const uint32_t idesc = umma_idesc_u8(p.Kt);
     const uint32_t b_lbo = (p.Kt >> 3) * 128u;
     const uint32_t ybase = smem_u32(ybuf), tbase = smem_u32(tbuf);
@@ -359,7 +360,7 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
     // ------------------------------------------------------------ T loader
     // Per (window, 32-leaf chunk, d-tile): 4 nodes x one 4 KB packed block.
     uint32_t tseq = 0;
-    const uint32_t n_dt = D / 128, n_cc = Kw / 32;
+    const uint32_t n_dt = Dp / 128, n_cc = Kw / 32;
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       const GroupDesc g = group_of(p, item);
       const uint64_t pend = g.r0a + g.packed_rows;
@@ -384,7 +385,7 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
             __syncwarp();
             if (ok)
               bulk_g2s(tbuf + ts * kTcTStageBytes + lane * 4096u,
-                       packed + ((s0 - g.r0a) >> 3) * (32ull * D) + dt * 4096ull, 4096u, &tfull[ts]);
+                       packed + ((s0 - g.r0a) >> 3) * (32ull * Dp) + dt * 4096ull, 4096u, &tfull[ts]);
           }
         }
       }
@@ -400,12 +401,12 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
 }
 
 // Limb-pack rows [r0a, r1a) of a shard (8-row aligned; rows outside
-// [r0, r1) are zero): block b = rows r0a+8b..+8 (32 D bytes), laid out
-// [d-tile dt][limb k][chunk cl][row rr][16 bytes: byte k of
-// T[row][128 dt + 16 cl .. + 15]].
+// [r0, r1) and columns >= D are zero): block b = rows r0a+8b..+8 (32 Dp
+// bytes, Dp = D padded to a multiple of 128), laid out [d-tile dt][limb k]
+// [chunk cl][row rr][16 bytes: byte k of T[row][128 dt + 16 cl .. + 15]].
 __global__ void table_pack_kernel(const uint32_t *__restrict__ T, uint64_t r0, uint64_t r1, uint64_t r0a,
-                                  uint64_t nblocks, uint32_t D, uint8_t *__restrict__ out) {
-  const uint32_t nchunk = D / 16;
+                                  uint64_t nblocks, uint32_t D, uint32_t Dp, uint8_t *__restrict__ out) {
+  const uint32_t nchunk = Dp / 16;
   const uint64_t total = nblocks * 8 * nchunk;  // one thread per (block, row, chunk): 16 words in, 4 x 16 B out
   for (uint64_t t = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; t < total;
        t += uint64_t(gridDim.x) * blockDim.x) {
@@ -414,18 +415,14 @@ __global__ void table_pack_kernel(const uint32_t *__restrict__ T, uint64_t r0, u
     const uint64_t blk = t / (8ull * nchunk);
     const uint64_t row = r0a + blk * 8 + rr;
     uint32_t w[16];
-    if (row >= r0 && row < r1) {
-      const uint4 *src = reinterpret_cast<const uint4 *>(T + (row - r0) * D + 16ull * c);
+    const bool row_in = row >= r0 && row < r1;
+    const uint4 *src = reinterpret_cast<const uint4 *>(T + (row - r0) * D + 16ull * c);
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const uint4 x = __ldg(src + v);
-        w[4 * v] = x.x; w[4 * v + 1] = x.y; w[4 * v + 2] = x.z; w[4 * v + 3] = x.w;
-      }
-    } else {
-#pragma unroll
-      for (int v = 0; v < 16; ++v) w[v] = 0;
+    for (int v = 0; v < 4; ++v) {
+      const uint4 x = (row_in && 16 * c + 4 * v < D) ? __ldg(src + v) : make_uint4(0, 0, 0, 0);
+      w[4 * v] = x.x; w[4 * v + 1] = x.y; w[4 * v + 2] = x.z; w[4 * v + 3] = x.w;
     }
-    uint8_t *blk_out = out + blk * 32ull * D;
+    uint8_t *blk_out = out + blk * 32ull * Dp;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       uint32_t o[4];

@@ -430,3 +430,26 @@ def test_accumulator_runs_across_items(dp, oracle, n, N, D, B, prf, packed):
     got = dp.as_u32(dp.eval_batch_packed(keys, dp.table_pack(Td)) if packed else dp.eval_batch(keys, Td))
     assert dp.last_eval_stats()["grid"] == plan["grid"]
     np.testing.assert_array_equal(got, oracle.answer_batch(okeys, T, threads=16))
+
+
+@pytest.mark.parametrize("n,N,D,B,prf", [
+    (12, 4096, 64, 130, 1), (11, 2000, 4, 3, 1), (12, 4000, 100, 70, 1), (10, 1024, 192, 40, 1),
+    (11, 2047, 1000, 17, 1), (13, 1 << 13, 64, 128, 3), (12, 3001, 36, 129, 3), (10, 1000, 320, 33, 2),
+])
+def test_packed_tc_padded_columns(dp, oracle, n, N, D, B, prf):
+    """tcgen05 path for D not a multiple of 128: the packed table is padded
+    with zero columns to whole 128-column d-tiles (Kt = 128 keys at D <= 128)."""
+    T = synth.table(N, D, 9300 + D)
+    al = synth.alphas(B, N, 9300 + n)
+    if prf == 3:
+        keys, okeys = make_et_keys(dp, oracle, n, al, 9400 + n)
+    else:
+        seeds = synth.gen_seeds(B, 9400 + n)
+        keys, okeys = [], []
+        for i, (a, s) in enumerate(zip(al, seeds)):
+            k = dp.gen(n, int(a), 1, s, prf=prf)[i % 2]
+            keys.append(k)
+            okeys.append(oracle.key_from_wire(dp.key_serialize(k)))
+    Tp = dp.table_pack(to_dev(T))
+    got = dp.as_u32(dp.eval_batch_packed(keys, Tp))
+    np.testing.assert_array_equal(got, oracle.answer_batch(okeys, T, threads=16))

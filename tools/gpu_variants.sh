@@ -1,5 +1,6 @@
 #!/bin/bash
-for v in "DPF_TC_NSY=3" "DPF_TC_NSY=3 DPF_TC_NST=6" "DPF_TC_NSY=3 DPF_TC_NST=6 DPF_LOADER_SPIN=1" "DPF_TC_NSY=3 DPF_LOADER_SPIN=1"; do
-  echo "== $v"
-  env $v bash tools/bench_brief.sh c3 --prf chacha20_et --steps 20 2>&1 | tail -1 | cut -c1-200
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 > gpurun_out/pytest_gpu.txt 2>&1; tail -3 gpurun_out/pytest_gpu.txt
+for a in "c3 --prf chacha20_et" "t5 --prf chacha20_et --table packed" "t5 --prf chacha20_et --table rowmajor" "t5 --table packed" "c2 --prf chacha20_et --table packed" "c2 --table packed" "c4 --prf chacha20_et --table packed --steps 5"; do
+  echo "== $a"
+  bash tools/bench_brief.sh $a --steps 10 2>&1 | tail -1 | cut -c1-230
 done
