@@ -200,7 +200,7 @@ def main():
                     help="tree PRF (chacha20 = the paper's fastest standard PRF, Table 5; aes128 = its baseline; "
                          "chacha20_et = ChaCha20 with early-terminated 16-row leaves, DESIGN.md R20)")
     ap.add_argument("--table", default="auto", choices=["auto", "packed", "rowmajor"],
-                    help="packed = limb-packed table + tcgen05 contraction (D % 128 == 0); rowmajor = IMAD path")
+                    help="packed = limb-packed table + tcgen05 contraction (any D %% 4 == 0, padded to 128-column tiles); rowmajor = IMAD path")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))

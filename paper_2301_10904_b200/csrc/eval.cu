@@ -689,6 +689,7 @@ struct Plan {
   uint32_t v, R;
   uint64_t nr0, nr1;
   uint32_t nsy, nst;  // y-ring / T-ring depth (tc)
+  bool pair;          // tc: CTA pairs (cta_group::2, M = 256); Kt = keys per CTA, 2 Kt per item
   uint32_t tmem_cols, y_stage_bytes, t_stage_bytes;
   uint64_t r0a, packed_rows;
   uint32_t n, m, f, Kt, Ft, tasks, W, CG, KG, SG, n_ktiles, n_items, nwin, grid;
@@ -769,8 +770,8 @@ bool pick_kernel(uint32_t Kt, uint32_t D, Plan &pl) {
 
 // Subtree depth m: the largest m (<= m_cap) that still gives >= 8 work items
 // per SM (measured: beyond that, deeper top BFS costs more than balance gains).
-uint32_t choose_m_target(const Plan &pl, uint32_t n, uint32_t m_min, uint32_t m_cap) {
-  const uint64_t target = 8ull * num_sms();
+uint32_t choose_m_target(const Plan &pl, uint32_t n, uint32_t m_min, uint32_t m_cap, uint32_t workers = 0) {
+  const uint64_t target = 8ull * (workers ? workers : uint32_t(num_sms()));
   uint32_t best = m_min;
   for (uint32_t m = std::min<uint32_t>(n, m_cap); m >= m_min; --m) {
     const uint64_t F = ((pl.nr1 - 1) >> m) - (pl.nr0 >> m) + 1;
@@ -785,8 +786,8 @@ uint32_t choose_m_target(const Plan &pl, uint32_t n, uint32_t m_min, uint32_t m_
 // of (almost) every SM, each CTA keeps one key tile for all its items, so
 // its accumulators are flushed once instead of once per item (run_continues).
 // DPF_GRID_ALIGN=1 forces the aligned grid even when it idles SMs, =0 never.
-uint32_t choose_grid(uint32_t n_items, uint32_t n_ktiles) {
-  const uint32_t sms = uint32_t(num_sms());
+uint32_t choose_grid(uint32_t n_items, uint32_t n_ktiles, uint32_t sms = 0) {
+  if (sms == 0) sms = uint32_t(num_sms());
   if (n_items <= sms) return n_items;
   static const int force = [] {
     const char *e = getenv("DPF_GRID_ALIGN");
@@ -890,6 +891,39 @@ int make_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D
 }
 
 constexpr uint32_t kTcNP = 16;   // producer warps (4 per SMSP)
+
+// How many 2-CTA clusters of the tcgen05 kernel fit on the device at once
+// (cudaOccupancyMaxActiveClusters; num_sms/2 without a device).
+uint32_t max_pairs(size_t smem_bytes) {
+  static uint32_t cached = 0;
+  static size_t cached_smem = 0;
+  if (cached && cached_smem == smem_bytes) return cached;
+  uint32_t r = uint32_t(num_sms()) / 2;
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3(2 * r);
+  cfg.blockDim = dim3(32 * (kTcNP + 4 + 1));
+  cfg.dynamicSmemBytes = smem_bytes;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  auto fn = &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, 2, 4, true>;
+  int n = 0;
+  int dev_id = 0;
+  if (cudaGetDevice(&dev_id) == cudaSuccess &&
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes)) == cudaSuccess &&
+      cudaOccupancyMaxActiveClusters(&n, fn, &cfg) == cudaSuccess && n > 0)
+    r = std::min<uint32_t>(r, uint32_t(n));
+  else
+    cudaGetLastError();  // clear: no device (host-only planning)
+  cached = r;
+  cached_smem = smem_bytes;
+  return r;
+}
 constexpr uint32_t kTcNSY = 2;   // y-ring depth
 // Early termination (R20) fills a y stage with ~2 ChaCha20 blocks per thread
 // instead of ~8, so the MMA side (80 UMMAs per stage) needs more slack: a
@@ -904,15 +938,8 @@ inline uint32_t tc_y_stages(bool et) {
 }
 // T-ring depth (16 KB entries).  8 entries measured no faster than 4 at
 // D = 512/1024, so the SMEM goes to the DFS stack instead.
-// DPF_TC_NST=8 selects an 8-deep ring (tuning).
-inline uint32_t tc_t_stages(uint32_t) {
-  static const uint32_t v = [] {
-    const char *e = getenv("DPF_TC_NST");
-    const int n = e ? atoi(e) : 4;
-    return (n == 6 || n == 8) ? uint32_t(n) : 4u;
-  }();
-  return v;
-}
+// (6 and 8 entries measured no faster for early termination either.)
+inline uint32_t tc_t_stages(uint32_t) { return 4u; }
 
 // tcgen05 plan (limb-packed table), D a multiple of 128 up to 1024:
 // Kt = MMA N = 64/32/16 keys so that 4 limb accumulators x D/128 tiles x Kt
@@ -929,15 +956,26 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
   // Kt = MMA N: the largest power of two <= 128 whose 4 limb accumulators x
   // n_dt d-tiles x Kt columns fit the 512 TMEM columns (D <= 128: 128 keys,
   // 256: 64, 512: 32, 1024: 16).  D is padded to whole 128-column d-tiles.
+  // CTA pairs (cta_group::2) when the d-tiles split evenly over two SMs:
+  // each CTA keeps n_dt/2 tiles, so the MMA N doubles to Ktp = 2 Kt (D = 256:
+  // 128 keys per MMA instead of 64) and each SM stages half of the table.
   const uint32_t n_dt = (D + 127) / 128;
-  pl.Kt = 128;
-  while (4 * n_dt * pl.Kt > 512) pl.Kt >>= 1;
-  // small batches: no wider than the batch (MMA N >= 16)
-  while (pl.Kt > 16 && pl.Kt / 2 >= B) pl.Kt >>= 1;
+  static const int pair_env = [] {
+    const char *e = getenv("DPF_TC_PAIR");
+    return e ? atoi(e) : -1;
+  }();
+  pl.pair = n_dt % 2 == 0 && pair_env != 0 && B > 16;
+  const uint32_t n_dt_cta = pl.pair ? n_dt / 2 : n_dt;
+  uint32_t Ktp = 128;
+  while (4 * n_dt_cta * Ktp > 512) Ktp >>= 1;
+  // small batches: no wider than the batch (MMA N >= 16, >= 32 for a pair)
+  const uint32_t kmin = pl.pair ? 32 : 16;
+  while (Ktp > kmin && Ktp / 2 >= B) Ktp >>= 1;
+  pl.Kt = pl.pair ? Ktp / 2 : Ktp;
   pl.nsy = tc_y_stages(et);
   pl.Ft = 32 * kTcNP / pl.Kt;
-  pl.tasks = pl.Kt * pl.Ft;
-  pl.n_ktiles = (B + pl.Kt - 1) / pl.Kt;
+  pl.tasks = Ktp * pl.Ft;  // per item (both CTAs of a pair)
+  pl.n_ktiles = (B + Ktp - 1) / Ktp;
   // W units per node per window: 4 leaf pairs (one 8-row packed block), or
   // one final node (16 rows) with early termination.
   const uint32_t W = et ? 1 : 4;
@@ -950,7 +988,9 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
   const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / (32 * kTcNP * 16)));
   const uint32_t m_min = et ? 1 : 3;
   if (m_cap < m_min || n < m_min) return DPF_EINVAL;
-  pl.m = choose_m_target(pl, n, m_min, m_cap);
+  // co-resident CTA pairs: a GPC with an odd SM count leaves an SM unpaired
+  const uint32_t workers = pl.pair ? max_pairs(fixed + size_t(m_cap) * 32 * kTcNP * 16) : uint32_t(num_sms());
+  pl.m = choose_m_target(pl, n, m_min, m_cap, workers);
   pl.f = n - pl.m;
   pl.lo_f = pl.nr0 >> pl.m;
   pl.F = ((pl.nr1 - 1) >> pl.m) - pl.lo_f + 1;
@@ -960,12 +1000,12 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
   pl.n_items = uint32_t(items);
   pl.W = W;
   pl.nwin = (et ? (1u << pl.m) : (1u << (pl.m - 1))) / W;
-  const uint32_t cols = n_dt * 4 * pl.Kt;
+  const uint32_t cols = n_dt_cta * 4 * Ktp;
   pl.tmem_cols = 32;
   while (pl.tmem_cols < cols) pl.tmem_cols <<= 1;
   pl.smem_bytes = fixed + size_t(pl.m) * 32 * kTcNP * 16;  // stack slots 1..m-1 (slot 0 unused)
   if (pl.smem_bytes > 227 * 1024) return DPF_EINVAL;
-  pl.grid = choose_grid(pl.n_items, pl.n_ktiles);
+  pl.grid = pl.pair ? 2 * choose_grid(pl.n_items, pl.n_ktiles, workers) : choose_grid(pl.n_items, pl.n_ktiles);
   pl.prf_blocks = count_blocks(pl, B);
   return DPF_OK;
 }
@@ -1110,18 +1150,34 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
     tp.debug_nomma = nomma;
     using TcFn = void (*)(const dev::TcParams);
     TcFn fn;
-    if (pl.prf == DPF_PRF_AES128) fn = &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4>;
+    if (pl.prf == DPF_PRF_AES128)
+      fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, true>
+                   : &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, false>;
     else if (pl.prf == DPF_PRF_CHACHA20_ET)
-      fn = pl.nsy == 3 ? (pl.nst == 6 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 3, 6>
-                                      : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 3, 4>)
-                       : (pl.nst == 8 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSY, 8>
-                                      : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSY, 4>);
-    else fn = pl.nst == 8 ? &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 8>
-                          : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4>;
+      fn = pl.pair ? (pl.nsy == 3 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 3, 4, true>
+                                  : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, true>)
+                   : (pl.nsy == 3 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 3, 4, false>
+                                  : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, false>);
+    else
+      fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, true>
+                   : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, false>;
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
       return DPF_ECUDA;
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3(pl.grid);
+    cfg.blockDim = dim3(32 * (kTcNP + 4 + 1));
+    cfg.dynamicSmemBytes = pl.smem_bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = pl.pair ? 2 : 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
     if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
-    fn<<<pl.grid, 32 * (kTcNP + 4 + 1), pl.smem_bytes, st>>>(tp);
+    if (cudaLaunchKernelEx(&cfg, fn, tp) != cudaSuccess) return DPF_ECUDA;
     if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used++ + 1], st);
     ++nk;
     if (cudaGetLastError() != cudaSuccess) return DPF_ECUDA;
@@ -1225,7 +1281,7 @@ int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uin
   g_stats.prf_blocks = pl.prf_blocks;
   g_stats.kernels = nk;
   g_stats.frontier_depth = pl.f;
-  g_stats.keys_per_tile = pl.Kt;
+  g_stats.keys_per_tile = pl.pair ? 2 * pl.Kt : pl.Kt;
   g_stats.nodes_per_tile = pl.Ft;
   g_stats.work_items = pl.n_items;
   g_stats.grid = pl.grid;
@@ -1277,7 +1333,7 @@ extern "C" int dpf_eval_plan(uint32_t B, uint32_t log_n, uint32_t prf, uint64_t 
   out->prf_blocks = pl.prf_blocks;
   out->kernels = 0;
   out->frontier_depth = pl.f;
-  out->keys_per_tile = pl.Kt;
+  out->keys_per_tile = pl.pair ? 2 * pl.Kt : pl.Kt;
   out->nodes_per_tile = pl.Ft;
   out->work_items = pl.n_items;
   out->grid = pl.grid;
@@ -1662,7 +1718,7 @@ extern "C" int dpf_eval_grouped(const dpf_eval_group *groups, uint32_t n_groups,
   g_stats.prf_blocks = pl.prf_blocks;
   g_stats.kernels = nk;
   g_stats.frontier_depth = 0;
-  g_stats.keys_per_tile = pl.Kt;
+  g_stats.keys_per_tile = pl.pair ? 2 * pl.Kt : pl.Kt;
   g_stats.nodes_per_tile = pl.Ft;
   g_stats.work_items = pl.n_items;
   g_stats.grid = pl.grid;

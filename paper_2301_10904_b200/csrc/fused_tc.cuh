@@ -49,15 +49,15 @@ __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint
 }
 
 // Instruction descriptor, kind::i8: D = s32 (no saturate), A = u8 MN-major,
-// B = u8 K-major, M = 128, N = n.
-__host__ __device__ constexpr uint32_t umma_idesc_u8(uint32_t n) {
+// B = u8 K-major, M = m (128, or 256 for a CTA pair), N = n.
+__host__ __device__ constexpr uint32_t umma_idesc_u8(uint32_t n, uint32_t m = 128) {
   return (2u << 4)            // c_format = S32
          | (0u << 7)          // a_format = unsigned 8-bit
          | (0u << 10)         // b_format = unsigned 8-bit
          | (1u << 15)         // a_major = MN
          | (0u << 16)         // b_major = K
          | ((n >> 3) << 17)   // N >> 3
-         | ((128u >> 4) << 24);  // M >> 4
+         | ((m >> 4) << 24);  // M >> 4
 }
 
 __device__ __forceinline__ void umma_u8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
@@ -67,6 +67,51 @@ __device__ __forceinline__ void umma_u8(uint32_t tmem_d, uint64_t adesc, uint64_
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+      : "memory");
+}
+
+// cta_group::2 (CTA pair, M = 256): issued by the leader CTA only; A rows
+// 0..127 / B columns 0..N/2-1 come from the leader's SMEM, the rest from the
+// peer's SMEM at the same offsets; each CTA's TMEM receives its 128 rows.
+__device__ __forceinline__ void umma_u8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Commit to the same-offset mbarrier in both CTAs of the pair.
+__device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(uint16_t(3))
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Arrive on the leader CTA's (rank 0) copy of an mbarrier (release at cluster scope).
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t *bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+// Wait for a phase completed (partly) by arrivals from the peer CTA.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "DPF_WAITC_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra DPF_WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
       : "memory");
 }
 
@@ -121,7 +166,16 @@ __device__ __forceinline__ void put_leaf16(uint8_t *yb, uint32_t ybplane, uint32
 // NP producer warps, NSY-deep y ring, NST-deep T ring of (K-chunk, d-tile)
 // entries.  Named barriers: 1..NSY = y stage FULL (producers arrive, the MMA
 // warp syncs); NSY+1 = epilogue.
-template <class Prf, int NP, int NSY, int NST>
+//
+// PAIR (cluster of 2 CTAs, cta_group::2): a work item is 2 Kt keys x Ft
+// nodes.  Both CTAs expand the same nodes, each for its Kt keys (B operand
+// columns), and each stages the table columns of its half of the d-tiles (A
+// rows); the leader issues M = 256, N = 2 Kt MMAs, so every MMA covers twice
+// the keys of a single-CTA one and each SM streams half of the table.  The
+// peer's MMA warp forwards its y-FULL and T-FULL events to the leader
+// (ypeer / tpeer, remote mbarrier arrives); the leader's commits arrive in
+// both CTAs (multicast); both epilogues release the leader's accempty.
+template <class Prf, int NP, int NSY, int NST, bool PAIR>
 __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(const TcParams tp) {
   constexpr int NC = 4;
   const FusedParams &p = tp.f;
@@ -131,7 +185,9 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
   uint64_t *yempty = tempty + NST;                       // [NSY], count 1 (tcgen05.commit)
   uint64_t *accfull = yempty + NSY;                      // count 1 (tcgen05.commit)
   uint64_t *accempty = accfull + 1;                      // count NC (epilogue warps)
-  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(accempty + 1);
+  uint64_t *tpeer = accempty + 1;                        // [NST], count 1 (PAIR: peer's T entry landed)
+  uint64_t *ypeer = tpeer + NST;                         // [NSY], count 1 (PAIR: peer's y stage full)
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(ypeer + NSY);
   uint8_t *tbuf = smem + 1024;
   uint8_t *ybuf = tbuf + NST * kTcTStageBytes;
   uint4 *stack = reinterpret_cast<uint4 *>(ybuf + NSY * tp.y_stage_bytes);
@@ -144,18 +200,33 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
     }
     for (int s = 0; s < NSY; ++s) mbar_init(&yempty[s], 1);
     mbar_init(accfull, 1);
-    mbar_init(accempty, NC);
+    mbar_init(accempty, PAIR ? 2 * NC : NC);
+    for (int s = 0; s < NST; ++s) mbar_init(&tpeer[s], 1);
+    for (int s = 0; s < NSY; ++s) mbar_init(&ypeer[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == NP) {  // consumer warp 0 owns the TMEM allocation
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(tp.tmem_cols)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  if (warp == NP) {  // consumer warp 0 owns the TMEM allocation (in each CTA of a pair)
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(tp.tmem_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(tp.tmem_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // both CTAs' barriers initialised before any remote arrive
   tc_fence_after();
+  // work items: one per CTA, or one per CTA pair
+  const uint32_t first = PAIR ? blockIdx.x >> 1 : blockIdx.x;
+  const uint32_t stride = PAIR ? gridDim.x >> 1 : gridDim.x;
+  const uint32_t Ktp = PAIR ? 2 * p.Kt : p.Kt;  // keys per item
   const uint32_t tmem_base = *tmem_slot;
 
   const uint32_t W2 = p.R;             // leaves per node per window (multiple of 8)
@@ -164,6 +235,8 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
   const uint32_t ybplane = p.Kt * Kw;  // bytes per y limb plane
   const uint32_t D = p.D;
   const uint32_t Dp = (D + 127) & ~127u;  // packed width: whole 128-column d-tiles
+  const uint32_t n_dt = PAIR ? Dp / 256 : Dp / 128;  // d-tiles staged by this CTA
+  const uint32_t dt0 = rank * n_dt;                   // first of them
 
   if (warp < NP) {
     // ------------------------------------------------------------ producers
@@ -175,12 +248,12 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
     const uint32_t tix = warp * 32 + lane;
     const uint32_t kl = tix % p.Kt, nl = tix / p.Kt;
     uint32_t wseq = 0;
-    for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+    for (uint32_t item = first; item < p.n_items; item += stride) {
       const GroupDesc g = group_of(p, item);
       const uint32_t li = item - g.item_base;
       const uint32_t kt = li % g.n_ktiles, ng = li / g.n_ktiles;
       const uint32_t nq = 1u << (g.m - 1);
-      const uint32_t b = kt * p.Kt + kl;
+      const uint32_t b = kt * Ktp + rank * p.Kt + kl;
       const uint64_t node = uint64_t(ng) * p.Ft + nl;
       const bool valid = b < g.B && node < g.F;
       const uint8_t *key = g.keys + uint64_t(valid ? b : 0) * g.kstride;
@@ -271,29 +344,34 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
   } else if (warp < NP + NC) {
     // ------------------------------------------------ MMA issuer + epilogue
     const uint32_t q = warp - NP;  // TMEM lane quarter
-    const uint32_t n_dt = Dp / 128, n_cc = Kw / 32;
-    const uint32_t idesc = umma_idesc_u8(p.Kt);
-    const uint32_t b_lbo = (p.Kt >> 3) * 128u;
+    const uint32_t n_cc = Kw / 32;
+    const uint32_t idesc = umma_idesc_u8(Ktp, PAIR ? 256u : 128u);
+    const uint32_t b_lbo = (p.Kt >> 3) * 128u;  // this CTA's Kt keys of the B operand
     const uint32_t ybase = smem_u32(ybuf), tbase = smem_u32(tbuf);
     // nf = accumulator flushes so far; fresh = this item starts a run (the
     // first MMA of the run overwrites TMEM, later ones accumulate)
     uint32_t wseq = 0, tseq = 0, nf = 0;
     bool fresh = true;
-    for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+    for (uint32_t item = first; item < p.n_items; item += stride) {
       const GroupDesc g = group_of(p, item);
       const uint32_t kt = (item - g.item_base) % g.n_ktiles;
-      const bool last = !run_continues(p, g, kt, item + gridDim.x);
-      if (q == 0) {
-        if (fresh && nf > 0) mbar_wait(accempty, (nf - 1) & 1);  // epilogue drained the accumulators
+      const bool last = !run_continues(p, g, kt, item + stride);
+      if (q == 0 && rank == 0) {
+        if (fresh && nf > 0) {  // epilogue(s) drained the accumulators
+          if (PAIR) mbar_wait_cluster(accempty, (nf - 1) & 1);
+          else mbar_wait(accempty, (nf - 1) & 1);
+        }
         for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
           const uint32_t ys = wseq % NSY;
           named_sync(1 + ys, 32 * (NP + 1));
+          if (PAIR) mbar_wait_cluster(&ypeer[ys], (wseq / NSY) & 1);
           tc_fence_after();
           const uint32_t yb = ybase + ys * tp.y_stage_bytes;
           for (uint32_t cc = 0; cc < n_cc; ++cc) {
             for (uint32_t dt = 0; dt < n_dt; ++dt, ++tseq) {
               const uint32_t ts = tseq % NST, tuse = tseq / NST;
               mbar_wait(&tfull[ts], tuse & 1);
+              if (PAIR) mbar_wait_cluster(&tpeer[ts], tuse & 1);
               tc_fence_after();
               if (lane == 0 && !tp.debug_nomma) {
                 const uint32_t tb = tbase + ts * kTcTStageBytes;
@@ -305,17 +383,41 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
                     const uint64_t ad = umma_desc(tb + k * 1024u, 4096u, 128u);
                     const uint64_t bd = umma_desc(yb + i * ybplane + cc * 2u * b_lbo, b_lbo, 128u);
                     const uint32_t acc = (fresh && win == 0 && cc == 0 && i == 0) ? 0u : 1u;
-                    umma_u8(tmem_base + (dt * 4 + s) * p.Kt, ad, bd, idesc, acc);
+                    if (PAIR) umma_u8_pair(tmem_base + (dt * 4 + s) * Ktp, ad, bd, idesc, acc);
+                    else umma_u8(tmem_base + (dt * 4 + s) * Ktp, ad, bd, idesc, acc);
                   }
                 }
               }
-              if (lane == 0) umma_commit(&tempty[ts]);  // T entry reusable once these MMAs finish
+              if (lane == 0) {  // T entry reusable once these MMAs finish
+                if (PAIR) umma_commit_pair(&tempty[ts]);
+                else umma_commit(&tempty[ts]);
+              }
               __syncwarp();
             }
           }
           if (lane == 0) {
-            umma_commit(&yempty[ys]);                     // y stage reusable
-            if (last && win + 1 == g.nwin) umma_commit(accfull);  // run's accumulators complete
+            if (PAIR) {
+              umma_commit_pair(&yempty[ys]);                     // y stage reusable (both CTAs)
+              if (last && win + 1 == g.nwin) umma_commit_pair(accfull);
+            } else {
+              umma_commit(&yempty[ys]);                          // y stage reusable
+              if (last && win + 1 == g.nwin) umma_commit(accfull);  // run's accumulators complete
+            }
+          }
+          __syncwarp();
+        }
+      } else if (q == 0) {
+        // PAIR peer: forward this CTA's y-FULL and T-FULL events to the leader
+        for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
+          const uint32_t ys = wseq % NSY;
+          named_sync(1 + ys, 32 * (NP + 1));
+          if (lane == 0) mbar_arrive_leader(&ypeer[ys]);
+          for (uint32_t cc = 0; cc < n_cc; ++cc) {
+            for (uint32_t dt = 0; dt < n_dt; ++dt, ++tseq) {
+              const uint32_t ts = tseq % NST, tuse = tseq / NST;
+              mbar_wait(&tfull[ts], tuse & 1);
+              if (lane == 0) mbar_arrive_leader(&tpeer[ts]);
+            }
           }
           __syncwarp();
         }
@@ -329,21 +431,21 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
       named_sync(NSY + 1, 32 * NC);
       tc_fence_after();
       for (uint32_t dt = 0; dt < n_dt; ++dt) {
-        const uint32_t d = dt * 128 + q * 32 + lane;
-        for (uint32_t h = 0; h < p.Kt / 16; ++h) {
+        const uint32_t d = (dt0 + dt) * 128 + q * 32 + lane;
+        for (uint32_t h = 0; h < Ktp / 16; ++h) {
           uint32_t v[16], x[16], z[16];
-          const uint32_t taddr = tmem_base + ((q * 32u) << 16) + dt * 4 * p.Kt + h * 16;
+          const uint32_t taddr = tmem_base + ((q * 32u) << 16) + dt * 4 * Ktp + h * 16;
           tmem_ld16(taddr, v);
-          tmem_ld16(taddr + p.Kt, x);
+          tmem_ld16(taddr + Ktp, x);
           tmem_wait_ld();
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] += x[j] << 8;
-          tmem_ld16(taddr + 2 * p.Kt, x);
-          tmem_ld16(taddr + 3 * p.Kt, z);
+          tmem_ld16(taddr + 2 * Ktp, x);
+          tmem_ld16(taddr + 3 * Ktp, z);
           tmem_wait_ld();
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const uint32_t bkey = kt * p.Kt + h * 16 + j;
+            const uint32_t bkey = kt * Ktp + h * 16 + j;
             if (bkey < g.B && d < D) {
               const uint32_t val = v[j] + (x[j] << 16) + (z[j] << 24);  // A0 + 2^8 A1 + 2^16 A2 + 2^24 A3
               const uint32_t neg = key_party(g.keys + uint64_t(bkey) * g.kstride);
@@ -354,14 +456,17 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(accempty);
+      if (lane == 0) {
+        if (PAIR && rank != 0) mbar_arrive_leader(accempty);
+        else mbar_arrive(accempty);
+      }
     }
   } else {
     // ------------------------------------------------------------ T loader
     // Per (window, 32-leaf chunk, d-tile): 4 nodes x one 4 KB packed block.
     uint32_t tseq = 0;
-    const uint32_t n_dt = Dp / 128, n_cc = Kw / 32;
-    for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+    const uint32_t n_cc = Kw / 32;
+    for (uint32_t item = first; item < p.n_items; item += stride) {
       const GroupDesc g = group_of(p, item);
       const uint64_t pend = g.r0a + g.packed_rows;
       const uint8_t *packed = reinterpret_cast<const uint8_t *>(g.T);
@@ -385,7 +490,7 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
             __syncwarp();
             if (ok)
               bulk_g2s(tbuf + ts * kTcTStageBytes + lane * 4096u,
-                       packed + ((s0 - g.r0a) >> 3) * (32ull * Dp) + dt * 4096ull, 4096u, &tfull[ts]);
+                       packed + ((s0 - g.r0a) >> 3) * (32ull * Dp) + (dt0 + dt) * 4096ull, 4096u, &tfull[ts]);
           }
         }
       }
@@ -393,10 +498,15 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // no CTA leaves while its peer may still signal it
   if (warp == NP) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tp.tmem_cols)
-                 : "memory");
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tp.tmem_cols)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(tp.tmem_cols)
+                   : "memory");
   }
 }
 

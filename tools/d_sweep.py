@@ -32,8 +32,7 @@ for D in args.D:
     ws = torch.empty(dpfpir.eval_workspace_bytes(B, n, N, D), dtype=torch.uint8, device="cuda")
     out = torch.empty((B, D), dtype=torch.int32, device="cuda")
     paths = [("imad", None)]
-    if D % 128 == 0:
-        paths.append(("tcgen05", dpfpir.table_pack(T)))
+    paths.append(("tcgen05", dpfpir.table_pack(T)))
     for name, pk in paths:
         def step():
             if pk is None:

@@ -25,7 +25,7 @@ al = synth.alphas(w.B, w.N, w.seed)
 seeds = synth.gen_seeds(w.B, w.seed)
 keys = [dpfpir.gen(w.log_n, int(a), 1, s)[0] for a, s in zip(al, seeds)]
 wire = torch.from_numpy(dpfpir.keys_to_wire(keys)).cuda()
-packed = args.table == "packed" or (args.table == "auto" and w.D % 128 == 0 and w.B >= 32)
+packed = args.table == "packed" or (args.table == "auto" and w.B >= 32)
 for G in args.shards:
     r0, rows = shard.row_range(w.N, G, 0)
     T = torch.from_numpy(synth.table_rows(w.N, w.D, w.seed, r0, r0 + rows).view(np.int32)).cuda()
