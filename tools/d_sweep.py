@@ -20,11 +20,14 @@ ap.add_argument("--B", type=int, default=256)
 ap.add_argument("--log-n", type=int, default=20)
 ap.add_argument("--D", type=int, nargs="+", default=[16, 32, 64, 128, 256, 512, 1024])
 ap.add_argument("--steps", type=int, default=5)
+ap.add_argument("--prf", default="chacha20", choices=["chacha20", "chacha20_et"])
 args = ap.parse_args()
+prf = dpfpir.DPF_PRF_CHACHA20_ET if args.prf == "chacha20_et" else dpfpir.DPF_PRF_CHACHA20
 n, B = args.log_n, args.B
 N = 1 << n
 al = synth.alphas(B, N, 99)
-keys = [dpfpir.gen(n, int(a), 1, s)[0] for a, s in zip(al, synth.gen_seeds(B, 99))]
+keys = [dpfpir.gen(n, int(a), 1, s, prf=prf)[0] for a, s in zip(al, synth.gen_seeds(B, 99))]
+blocks_per_key = (N - 1) if prf == dpfpir.DPF_PRF_CHACHA20 else (N // 8 - 1)  # R9 / R20
 wire = torch.from_numpy(dpfpir.keys_to_wire(keys)).cuda()
 peak = 148 * 64 * 1965e6
 for D in args.D:
@@ -36,9 +39,9 @@ for D in args.D:
     for name, pk in paths:
         def step():
             if pk is None:
-                dpfpir.eval_batch_wire(wire, n, T, 0, out=out, workspace=ws)
+                dpfpir.eval_batch_wire(wire, n, T, 0, out=out, workspace=ws, prf=prf)
             else:
-                dpfpir.eval_batch_wire_packed(wire, n, pk, out=out, workspace=ws)
+                dpfpir.eval_batch_wire_packed(wire, n, pk, out=out, workspace=ws, prf=prf)
         for _ in range(2):
             step()
         torch.cuda.synchronize()
@@ -51,6 +54,7 @@ for D in args.D:
         ms = e0.elapsed_time(e1) / args.steps
         st = dpfpir.last_eval_stats()
         print(json.dumps({"D": D, "entry_bytes": 4 * D, "path": name, "B": B, "log_n": n, "ms": round(ms, 3),
-                          "qps": round(B / (ms * 1e-3)), "step_frac_alu": round(640 * B * (N - 1) / (ms * 1e-3) / peak, 3),
+                          "qps": round(B / (ms * 1e-3)), "prf": args.prf,
+                          "step_frac_alu": round(640 * B * blocks_per_key / (ms * 1e-3) / peak, 3),
                           "keys_per_tile": st["keys_per_tile"], "frontier_depth": st["frontier_depth"]}), flush=True)
     del T, ws
