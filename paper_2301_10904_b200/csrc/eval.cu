@@ -1531,7 +1531,30 @@ int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t
   pl.prf = prf;
   (void)Bmax;
   const uint32_t NP = uint32_t(pl.kc.NP);
-  const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((64 * 1024) / (32 * NP * 16)));
+  uint32_t m_cap = std::min<uint32_t>(14, uint32_t((64 * 1024) / (32 * NP * 16)));
+  // Balance: a common cap on the subtree depth so that the items of all
+  // groups number >= 8 per SM (one item per key tile and group starves most
+  // SMs when one big table dominates).  Streaming regime (Kt <= 2: every
+  // table row serves <= 2 keys, so the table streams at the PRF rate): cap m
+  // so that one window covers whole subtrees, which makes each T-ring entry
+  // one contiguous bulk copy instead of one small copy per node.
+  // m_floor: no group's subtrees shallower than one full window (the shared
+  // window W must divide every group's 2^(m-1); tiny groups would drag it
+  // down to one leaf pair per node and make every T copy tiny).
+  uint32_t m_floor = 1;
+  {
+    double units = 0;
+    for (uint32_t i = 0; i < G; ++i) units += double((gs[i].B + pl.Kt - 1) / pl.Kt) * double(gs[i].row_count);
+    const double per_item = units / (double(pl.Ft) * 8.0 * num_sms());
+    uint32_t m_bal = 1;
+    while (m_bal < 14 && double(2u << m_bal) <= per_item) ++m_bal;
+    m_cap = std::min(m_cap, m_bal);
+    uint32_t Wmax = 8;
+    while (Wmax > 1 && uint64_t(pl.Kt) * pl.Ft * 2 * Wmax * 4 > 16 * 1024) Wmax >>= 1;
+    while ((1u << m_floor) < 2 * Wmax) ++m_floor;  // 2^(m-1) = W_max: one window per subtree
+    if (pl.Kt <= 2) m_cap = std::min(m_cap, m_floor);
+    m_floor = std::min(m_floor, m_cap);
+  }
   gp.desc.assign(G, dev::GroupDesc{});
   uint32_t m_min_all = 32;
   for (uint32_t i = 0; i < G; ++i) {
@@ -1543,7 +1566,7 @@ int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t
     uint32_t lg_ft = 0;
     while ((2u << lg_ft) <= pl.Ft) ++lg_ft;
     uint32_t m = lg_rows > lg_ft ? lg_rows - lg_ft : 1;
-    m = std::max(1u, std::min(std::min(m, n), m_cap));
+    m = std::max(1u, std::min(std::min(std::max(m, m_floor), n), m_cap));
     d.n = n;
     d.m = m;
     d.r0 = g.row_begin;

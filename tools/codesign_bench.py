@@ -84,6 +84,7 @@ for Binf in a.batches:
         res[name] = e0.elapsed_time(e1) / a.steps
     # correctness: second server, reconstruct the first inferences' real queries
     grouped()
+    plan = dpfpir.last_eval_stats()
     dpfpir.eval_grouped(groups1, D)
     torch.cuda.synchronize()
     ok = True
@@ -103,4 +104,4 @@ for Binf in a.batches:
                       "dropped_rows": dropped, "ms_grouped": round(ms, 4), "ms_separate": round(res["separate"], 4),
                       "inferences_per_s": round(Binf / (ms * 1e-3), 1), "dpf_queries_per_s": round(n_keys / (ms * 1e-3)),
                       "alu_frac": round(640 * blocks / (ms * 1e-3) / (148 * 64 * 1965e6), 3),
-                      "rows_reconstructed_ok": ok}), flush=True)
+                      "rows_reconstructed_ok": ok, "plan": plan}), flush=True)
