@@ -453,3 +453,27 @@ def test_packed_tc_padded_columns(dp, oracle, n, N, D, B, prf):
     Tp = dp.table_pack(to_dev(T))
     got = dp.as_u32(dp.eval_batch_packed(keys, Tp))
     np.testing.assert_array_equal(got, oracle.answer_batch(okeys, T, threads=16))
+
+
+@pytest.mark.parametrize("D", [32, 64])
+def test_grouped_small_batches_streaming(dp, oracle, D):
+    """Co-design at inference batch 1 (row f2): 1-2 keys per group (shared key
+    tile 1 -> streaming regime, one window per subtree), tiny and ragged hot
+    tables next to large full ones, deep frontiers (> 10 top levels)."""
+    shapes = [(18, 1 << 18, 0, 1 << 18, 1), (15, 26215, 0, 26215, 2), (12, 409, 0, 409, 2), (16, 1 << 16, 0, 1 << 16, 1),
+              (9, 300, 0, 300, 1), (17, 100000, 3, 99990, 2)]
+    groups, expect = [], []
+    for i, (n, N, r0, rows, B) in enumerate(shapes):
+        T = synth.table(N, D, 950 + i)
+        al = synth.alphas(B, N, 950 + i)
+        keys = [dp.gen(n, int(a), 1, s)[(j + i) % 2] for j, (a, s) in enumerate(zip(al, synth.gen_seeds(B, 950 + i)))]
+        okeys = [oracle.key_from_wire(dp.key_serialize(k)) for k in keys]
+        Tsh = T[r0:r0 + rows]
+        wire = torch.from_numpy(dp.keys_to_wire(keys)).cuda()
+        out = torch.empty((B, D), dtype=torch.int32, device="cuda")
+        groups.append((wire, n, to_dev(Tsh), r0, out))
+        expect.append(oracle.answer_batch(okeys, Tsh, row_begin=r0, threads=8))
+    dp.eval_grouped(groups, D)
+    torch.cuda.synchronize()
+    for (wire, n, Td, r0, out), want in zip(groups, expect):
+        np.testing.assert_array_equal(dp.as_u32(out), want)
