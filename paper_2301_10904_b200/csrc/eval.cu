@@ -211,6 +211,7 @@ struct GroupDesc {
   uint32_t item_base;       // first work item of this group
   uint32_t key_base;        // first key of this group (grouped top BFS)
   uint4 *frontier_alt;      // grouped top BFS ping-pong buffer (f > kTopSmemLevels)
+  uint64_t nr0, nr1;        // grouped top BFS: the row range in tree-leaf units (R20: final nodes)
 };
 
 struct FusedParams {
@@ -569,7 +570,7 @@ __global__ void __launch_bounds__(256) expand_top_grouped_kernel(const GroupDesc
   const uint32_t b = blockIdx.x - g.key_base;
   const uint8_t *key = g.keys + uint64_t(b) * g.kstride;
   const uint32_t n = g.n, f = g.n - g.m, a = f < kTopSmemLevels ? f : kTopSmemLevels;
-  const uint64_t r0 = g.r0, r1 = g.r1;
+  const uint64_t r0 = g.nr0, r1 = g.nr1;
   // level a lands where the remaining levels' ping-pong ends on `frontier`
   uint4 *out = (((f - a) & 1) ? g.frontier_alt : const_cast<uint4 *>(g.frontier)) + uint64_t(b) * g.cap;
   if (threadIdx.x == 0) buf[0][0] = key_root(key);
@@ -598,8 +599,8 @@ __global__ void expand_level_grouped_kernel(const GroupDesc *__restrict__ groups
   const GroupDesc &g = groups[blockIdx.y];
   const uint32_t n = g.n, f = g.n - g.m;
   if (k > f) return;
-  const uint64_t plo = g.r0 >> (n - (k - 1)), phi = (g.r1 - 1) >> (n - (k - 1));
-  const uint64_t lo = g.r0 >> (n - k), hi = (g.r1 - 1) >> (n - k);
+  const uint64_t plo = g.nr0 >> (n - (k - 1)), phi = (g.nr1 - 1) >> (n - (k - 1));
+  const uint64_t lo = g.nr0 >> (n - k), hi = (g.nr1 - 1) >> (n - k);
   const uint64_t np = phi - plo + 1, total = np * g.B;
   const uint4 *in = ((f - k + 1) & 1) ? g.frontier_alt : g.frontier;
   uint4 *out = ((f - k) & 1) ? g.frontier_alt : const_cast<uint4 *>(g.frontier);
@@ -1106,6 +1107,8 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
   g.lo_f = pl.lo_f;
   g.r0 = pl.r0;
   g.r1 = pl.r1;
+  g.nr0 = pl.nr0;
+  g.nr1 = pl.nr1;
   g.r0a = pl.r0a;
   g.packed_rows = pl.packed_rows;
   g.kstride = kstride;
@@ -1497,11 +1500,13 @@ struct GroupedPlan {
 // items ordered by subtree size so the static round-robin stays balanced.
 int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t prf, GroupedPlan &gp) {
   if (!gs || G == 0 || D == 0 || D > 1024 || (D & 3)) return DPF_EINVAL;
-  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128) return DPF_EUNSUPPORTED;
+  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128 && prf != DPF_PRF_CHACHA20_ET) return DPF_EUNSUPPORTED;
+  const bool et = prf == DPF_PRF_CHACHA20_ET;
+  const uint32_t v = et ? DPF_ET_BITS : 0u;  // log2(rows per tree leaf)
   uint32_t Bmax = 0;
   for (uint32_t i = 0; i < G; ++i) {
     const dpf_eval_group &g = gs[i];
-    if (!g.keys_wire || !g.table || !g.shares || g.B == 0 || g.log_n < 1 || g.log_n > DPF_MAX_LOG_N ||
+    if (!g.keys_wire || !g.table || !g.shares || g.B == 0 || g.log_n < 1 + v || g.log_n > DPF_MAX_LOG_N ||
         g.row_count == 0)
       return DPF_EINVAL;
     const uint64_t dom = 1ull << g.log_n;
@@ -1526,7 +1531,7 @@ int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t
     }
   }
   // reuse the single-group planner for the shared part (tile, Ft, SMEM rules)
-  int rc = make_plan(best_kt, 20, 0, 1u << 20, D, pl);
+  int rc = make_plan(best_kt, 20, 0, 1u << 20, D, pl, et);
   if (rc) return rc;
   pl.prf = prf;
   (void)Bmax;
@@ -1544,14 +1549,17 @@ int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t
   uint32_t m_floor = 1;
   {
     double units = 0;
-    for (uint32_t i = 0; i < G; ++i) units += double((gs[i].B + pl.Kt - 1) / pl.Kt) * double(gs[i].row_count);
+    for (uint32_t i = 0; i < G; ++i)
+      units += double((gs[i].B + pl.Kt - 1) / pl.Kt) * double(gs[i].row_count >> v);
     const double per_item = units / (double(pl.Ft) * 8.0 * num_sms());
     uint32_t m_bal = 1;
     while (m_bal < 14 && double(2u << m_bal) <= per_item) ++m_bal;
     m_cap = std::min(m_cap, m_bal);
+    // window units per subtree: 2^(m-1) leaf pairs, or 2^m final nodes (R20)
+    const uint64_t ybudget = et ? 32 * 1024 : 16 * 1024;
     uint32_t Wmax = 8;
-    while (Wmax > 1 && uint64_t(pl.Kt) * pl.Ft * 2 * Wmax * 4 > 16 * 1024) Wmax >>= 1;
-    while ((1u << m_floor) < 2 * Wmax) ++m_floor;  // 2^(m-1) = W_max: one window per subtree
+    while (Wmax > 1 && uint64_t(pl.Kt) * pl.Ft * unit_rows(pl) * Wmax * 4 > ybudget) Wmax >>= 1;
+    while ((et ? (1u << m_floor) : (1u << m_floor) / 2) < Wmax) ++m_floor;  // one window per subtree
     if (pl.Kt <= 2) m_cap = std::min(m_cap, m_floor);
     m_floor = std::min(m_floor, m_cap);
   }
@@ -1560,9 +1568,9 @@ int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t
   for (uint32_t i = 0; i < G; ++i) {
     const dpf_eval_group &g = gs[i];
     dev::GroupDesc &d = gp.desc[i];
-    const uint32_t n = g.log_n;
+    const uint32_t n = g.log_n - v;  // tree depth
     uint32_t lg_rows = 0;
-    while ((2ull << lg_rows) <= g.row_count) ++lg_rows;  // floor(log2(rows))
+    while ((2ull << lg_rows) <= (g.row_count >> v)) ++lg_rows;  // floor(log2(tree leaves))
     uint32_t lg_ft = 0;
     while ((2u << lg_ft) <= pl.Ft) ++lg_ft;
     uint32_t m = lg_rows > lg_ft ? lg_rows - lg_ft : 1;
@@ -1571,20 +1579,23 @@ int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t
     d.m = m;
     d.r0 = g.row_begin;
     d.r1 = g.row_begin + g.row_count;
-    d.lo_f = d.r0 >> m;
-    d.F = ((d.r1 - 1) >> m) - d.lo_f + 1;
+    d.nr0 = d.r0 >> v;
+    d.nr1 = ((d.r1 - 1) >> v) + 1;
+    d.lo_f = d.nr0 >> m;
+    d.F = ((d.nr1 - 1) >> m) - d.lo_f + 1;
     d.cap = d.F;
     d.B = g.B;
-    d.kstride = uint32_t(dpf_key_wire_size(n));
+    d.kstride = uint32_t(dpf_key_wire_size_prf(g.log_n, prf));
     d.n_ktiles = (g.B + pl.Kt - 1) / pl.Kt;
     d.T = g.table;
     d.shares = g.shares;
     m_min_all = std::min(m_min_all, m);
   }
-  // window: W leaf pairs must divide every group's 2^(m-1)
-  uint32_t W = std::min<uint32_t>(8, 1u << (m_min_all - 1));
+  // window: W units (leaf pairs / final nodes) must divide every group's
+  // 2^(m-1) (2^m with early termination)
+  uint32_t W = std::min<uint32_t>(8, et ? (1u << m_min_all) : (1u << (m_min_all - 1)));
   const size_t stack_bytes = size_t(m_cap) * 32 * NP * 16;
-  while (W > 1 && uint64_t(pl.Kt) * pl.Ft * 2 * W * 4 > 16 * 1024) W >>= 1;
+  while (W > 1 && uint64_t(pl.Kt) * pl.Ft * unit_rows(pl) * W * 4 > (et ? 32 * 1024 : 16 * 1024)) W >>= 1;
   for (;; W >>= 1) {
     if (set_windows(pl, W, D, stack_bytes)) break;
     if (W == 1) return DPF_EINVAL;
@@ -1600,7 +1611,7 @@ int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t
   uint64_t blocks = 0;
   for (uint32_t oi : gp.order) {
     dev::GroupDesc &d = gp.desc[oi];
-    d.nwin = (1u << (d.m - 1)) / W;
+    d.nwin = (et ? (1u << d.m) : (1u << (d.m - 1))) / W;
     d.item_base = uint32_t(items);
     d.key_base = uint32_t(keys);
     items += uint64_t(d.n_ktiles) * ((d.F + pl.Ft - 1) / pl.Ft);
@@ -1608,8 +1619,9 @@ int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t
     gp.front_bytes += 2 * align_up(size_t(d.B) * d.cap * 16, kAlign);
     gp.keys_bytes += align_up(size_t(d.B) * d.kstride, kAlign);
     uint64_t top = 0;
-    for (uint32_t k = 0; k < d.n - d.m; ++k) top += ((d.r1 - 1) >> (d.n - k)) - (d.r0 >> (d.n - k)) + 1;
-    blocks += uint64_t(d.B) * top + uint64_t(d.n_ktiles) * ((d.F + pl.Ft - 1) / pl.Ft) * pl.tasks * ((1ull << d.m) - 1);
+    for (uint32_t k = 0; k < d.n - d.m; ++k) top += ((d.nr1 - 1) >> (d.n - k)) - (d.nr0 >> (d.n - k)) + 1;
+    const uint64_t per = ((1ull << d.m) - 1) + (et ? (1ull << d.m) : 0);  // + Convert blocks (R20)
+    blocks += uint64_t(d.B) * top + uint64_t(d.n_ktiles) * ((d.F + pl.Ft - 1) / pl.Ft) * pl.tasks * per;
   }
   if (items > 0x7FFFFFFFull || keys > 0x7FFFFFFFull) return DPF_EINVAL;
   pl.n_items = uint32_t(items);
@@ -1634,7 +1646,7 @@ extern "C" size_t dpf_eval_grouped_workspace_bytes(const dpf_eval_group *groups,
 
 extern "C" int dpf_eval_grouped(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D, uint32_t prf,
                                 void *workspace, size_t workspace_bytes, void *stream) {
-  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128) return DPF_EUNSUPPORTED;  // ET: not grouped (yet)
+  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128 && prf != DPF_PRF_CHACHA20_ET) return DPF_EUNSUPPORTED;
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & (kAlign - 1))) return DPF_EINVAL;
   GroupedPlan gp;
   int rc = make_grouped_plan(groups, n_groups, D, prf, gp);

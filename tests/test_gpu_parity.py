@@ -477,3 +477,26 @@ def test_grouped_small_batches_streaming(dp, oracle, D):
     torch.cuda.synchronize()
     for (wire, n, Td, r0, out), want in zip(groups, expect):
         np.testing.assert_array_equal(dp.as_u32(out), want)
+
+
+@pytest.mark.parametrize("kt_keys", [1, 40])
+def test_grouped_early_termination(dp, oracle, kt_keys):
+    """Grouped launches with the early-terminated scheme (rows f2 x f4):
+    final-node ranges in the top BFS, ragged row ranges inside final nodes."""
+    D = 32
+    shapes = [(14, 1 << 14, 0, 1 << 14), (12, 3001, 0, 3001), (10, 1000, 37, 900), (16, 60000, 0, 60000),
+              (5, 32, 0, 32), (13, 5000, 4096, 904)]
+    groups, expect = [], []
+    for i, (n, N, r0, rows) in enumerate(shapes):
+        B = kt_keys if i % 2 == 0 else max(1, kt_keys // 3)
+        T = synth.table(N, D, 970 + i)
+        keys, okeys = make_et_keys(dp, oracle, n, synth.alphas(B, N, 970 + i), 980 + i)
+        Tsh = T[r0:r0 + rows]
+        wire = torch.from_numpy(dp.keys_to_wire(keys)).cuda()
+        out = torch.empty((B, D), dtype=torch.int32, device="cuda")
+        groups.append((wire, n, to_dev(Tsh), r0, out))
+        expect.append(oracle.answer_batch(okeys, Tsh, row_begin=r0, threads=8))
+    dp.eval_grouped(groups, D, prf=ET)
+    torch.cuda.synchronize()
+    for (wire, n, Td, r0, out), want in zip(groups, expect):
+        np.testing.assert_array_equal(dp.as_u32(out), want)

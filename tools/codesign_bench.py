@@ -29,7 +29,9 @@ ap.add_argument("--q-full", type=int, default=1)
 ap.add_argument("--need", type=int, default=3)
 ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--check", type=int, default=2, help="inferences whose rows are reconstructed and checked")
+ap.add_argument("--prf", default="chacha20", choices=["chacha20", "chacha20_et"])
 a = ap.parse_args()
+prf = dpfpir.DPF_PRF_CHACHA20_ET if a.prf == "chacha20_et" else dpfpir.DPF_PRF_CHACHA20
 D = synth.CODESIGN_D
 rng = np.random.default_rng(0)
 tables = []
@@ -54,21 +56,21 @@ for Binf in a.batches:
         for kind, tbl, n, idxs in (("hot", tb["Hd"], tb["nH"], [p.hot_idx for p in plans]),
                                    ("full", tb["Td"], tb["nF"], [p.full_idx for p in plans])):
             flat = np.concatenate(idxs)
-            pairs = [dpfpir.gen(n, int(i), 1, next(seed_iter)) for i in flat]
+            pairs = [dpfpir.gen(n, int(i), 1, next(seed_iter), prf=prf) for i in flat]
             for party, gl in ((0, groups0), (1, groups1)):
                 wire = torch.from_numpy(dpfpir.keys_to_wire([p[party] for p in pairs])).cuda()
                 out = torch.empty((len(flat), D), dtype=torch.int32, device="cuda")
                 gl.append((wire, n, tbl, 0, out))
             real.append((t, kind, plans))
     n_keys = sum(g[0].shape[0] for g in groups0)
-    ws = torch.empty(dpfpir.eval_grouped_workspace_bytes(groups0, D), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(dpfpir.eval_grouped_workspace_bytes(groups0, D, prf=prf), dtype=torch.uint8, device="cuda")
 
     def grouped():
-        dpfpir.eval_grouped(groups0, D, workspace=ws)
+        dpfpir.eval_grouped(groups0, D, prf=prf, workspace=ws)
 
     def separate():
         for (wire, n, tbl, r0, out) in groups0:
-            dpfpir.eval_batch_wire(wire, n, tbl, r0, out=out)
+            dpfpir.eval_batch_wire(wire, n, tbl, r0, out=out, prf=prf)
 
     res = {}
     for name, fn in (("grouped", grouped), ("separate", separate)):
@@ -85,7 +87,7 @@ for Binf in a.batches:
     # correctness: second server, reconstruct the first inferences' real queries
     grouped()
     plan = dpfpir.last_eval_stats()
-    dpfpir.eval_grouped(groups1, D)
+    dpfpir.eval_grouped(groups1, D, prf=prf)
     torch.cuda.synchronize()
     ok = True
     for gi, (t, kind, plans) in enumerate(real):
@@ -97,9 +99,11 @@ for Binf in a.batches:
             mask = p.hot_real if kind == "hot" else p.full_real
             for j in np.nonzero(mask)[0]:
                 ok &= bool(np.array_equal(ans[inf * q + j], tables[t]["T"][rows[j]]))
-    blocks = sum(g[0].shape[0] * (g[2].shape[0] - 1) for g in groups0)  # nodes over each table's rows
+    # blocks over each table's rows: N - 1 per key (R9), N/8 - 1 with early termination (R20)
+    blocks = sum(g[0].shape[0] * ((g[2].shape[0] - 1) if prf == dpfpir.DPF_PRF_CHACHA20 else max(1, g[2].shape[0] // 8 - 1))
+                 for g in groups0)
     ms = res["grouped"]
-    print(json.dumps({"workload": "c5 co-design", "inferences_per_batch": Binf, "keys_per_batch": n_keys,
+    print(json.dumps({"workload": "c5 co-design", "prf": a.prf, "inferences_per_batch": Binf, "keys_per_batch": n_keys,
                       "q_hot": a.q_hot, "q_full": a.q_full, "hot_fraction": a.hot, "need_per_table": a.need,
                       "dropped_rows": dropped, "ms_grouped": round(ms, 4), "ms_separate": round(res["separate"], 4),
                       "inferences_per_s": round(Binf / (ms * 1e-3), 1), "dpf_queries_per_s": round(n_keys / (ms * 1e-3)),
