@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
   if (threadIdx.x == 0) {
     for (uint32_t s = 0; s < p.NST; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], NC);
+      mbar_init(&tempty[s], 32 * NC);  // every consumer lane releases what it read
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -454,8 +454,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
           if (active)
             consume_window<KPW, CPL>(yb + n0 * seg * p.Kt, tbuf + ts * p.t_stage_words, nn * seg, p.Kt, p.D, key0,
                                      colbase, sg, p.SG, acc);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[ts]);
+          mbar_arrive(&tempty[ts]);  // one warp instruction; each lane orders its own reads
         }
         if (wseq + 2 < total_w) named_arrive(3 + stage, kEmptyThreads);
       }
