@@ -202,6 +202,9 @@ def main():
     ap.add_argument("--table", default="auto", choices=["auto", "packed", "rowmajor"],
                     help="packed = limb-packed table + tcgen05 contraction (any D %% 4 == 0, padded to 128-column tiles); rowmajor = IMAD path")
     ap.add_argument("--e2e-steps", type=int, default=None)
+    ap.add_argument("--reduce", default="nccl", choices=["nccl", "p2p"],
+                    help="N > 1: sum the row shards' partial answers with one NCCL reduce, or inside the fused "
+                         "kernels (every rank red.adds into rank 0's buffer over a CUDA IPC / NVLink mapping)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -239,8 +242,15 @@ def main():
     ws = torch.empty(dpfpir.serve_workspace_bytes(w.B, w.log_n, rows, w.D), dtype=torch.uint8, device=dev)
     out = torch.empty((w.B, w.D), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
+    peer = shard.PeerShareReducer(out, dst=0) if (G > 1 and args.reduce == "p2p") else None
 
     def step():
+        if peer is not None:  # fused reduction: accumulate into rank 0's answers
+            peer.begin()
+            dpfpir.eval_batch_wire_ex(wire, w.log_n, Tp if use_packed else T, r0, rows, w.D, peer.ptr,
+                                      dpfpir.DPF_EVAL_ACCUMULATE, ws, stream=stream, prf=prf, packed=use_packed)
+            peer.finish()
+            return
         if use_packed:
             dpfpir.eval_batch_wire_packed(wire, w.log_n, Tp, out=out, workspace=ws, stream=stream, prf=prf)
         else:
@@ -373,7 +383,8 @@ def main():
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": w.name + ": " + w.note, "log_n": w.log_n, "N": w.N, "D": w.D, "B": w.B,
                        "prf": args.prf,
-                       "parallelism": "row-shard x%d + NCCL reduce" % G if G > 1 else "1 GPU",
+                       "parallelism": ("row-shard x%d + %s" % (G, "NCCL reduce" if args.reduce == "nccl" else
+                                       "in-kernel red.add into rank 0 over NVLink (CUDA IPC)")) if G > 1 else "1 GPU",
                        "keys": "device-resident wire keys (dpf_eval_batch_wire%s)" % ("_packed" if use_packed else ""),
                        "table": "limb-packed (dpf_table_pack, tcgen05 kind::i8 contraction)" if use_packed
                        else "row-major int32 (IMAD contraction)",
@@ -391,6 +402,8 @@ def main():
             "plan": stats,
         }
         print(json.dumps(line), flush=True)
+    if peer is not None:
+        peer.close()
     if G > 1:
         dist.barrier(device_ids=[local_rank])
         dist.destroy_process_group()

@@ -174,6 +174,38 @@ int dpf_eval_batch_wire(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n
                         uint64_t row_begin, uint64_t row_count, uint32_t D, uint32_t *partial_shares,
                         void *workspace, size_t workspace_bytes, void *stream);
 
+/* ---- fused cross-GPU reduction (multi-GPU row sharding) ----
+ * The G row shards' partial answers sum to the answer (Z_2^32 is a group).
+ * Instead of a separate collective, each rank's fused kernel can add its
+ * partial shares straight into ONE rank's answer buffer over NVLink: the
+ * epilogue's red.global.add.u32 targets a peer-mapped pointer, so the
+ * reduction overlaps the evaluation tile by tile.
+ *
+ * dpf_eval_batch_wire_ex: dpf_eval_batch_wire (packed = 0, `table` = the
+ * row-major shard) or dpf_eval_batch_wire_packed (packed = 1, `table` = the
+ * packed shard) with flags:
+ *   DPF_EVAL_ACCUMULATE  add into `shares` (B x D u32) instead of zeroing and
+ *                        overwriting it; `shares` may be a peer GPU's buffer
+ *                        opened with dpf_ipc_open.  The buffer's owner zeroes
+ *                        it before any rank launches, and reads it after every
+ *                        rank's launch completed (caller-side barrier).
+ * Errors: as dpf_eval_batch_wire; DPF_EINVAL for unknown flag bits. */
+#define DPF_EVAL_ACCUMULATE 1u
+int dpf_eval_batch_wire_ex(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n, uint32_t prf,
+                           const void *table, int packed, uint64_t row_begin, uint64_t row_count, uint32_t D,
+                           uint32_t *shares, uint32_t flags, void *workspace, size_t workspace_bytes, void *stream);
+
+/* CUDA IPC for the answer buffer: dpf_ipc_export writes the handle of the
+ * DEVICE allocation containing dev_ptr (64 opaque bytes, sent to the other
+ * ranks by the caller) and dev_ptr's byte offset inside that allocation;
+ * dpf_ipc_open maps it in another process (same or peer GPU; peer access is
+ * enabled lazily) and returns the allocation base (the buffer is at base +
+ * offset); dpf_ipc_close unmaps a base.  Errors: DPF_EINVAL (null), DPF_ECUDA. */
+#define DPF_IPC_HANDLE_BYTES 64
+int dpf_ipc_export(const void *dev_ptr, uint8_t handle[DPF_IPC_HANDLE_BYTES], uint64_t *offset);
+int dpf_ipc_open(const uint8_t handle[DPF_IPC_HANDLE_BYTES], void **base);
+int dpf_ipc_close(void *base);
+
 /* ---- limb-packed tables: the tcgen05 (tensor-core) contraction path ----
  * The contraction sum_j y_j T[j][d] mod 2^32 is computed on the 5th-gen
  * tensor cores (tcgen05.mma kind::i8) by splitting y and T into u8 limbs:

@@ -1059,9 +1059,13 @@ struct Staging {
 thread_local Staging g_staging;
 
 int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint32_t B, const uint32_t *table,
-                uint32_t D, uint32_t *out, const Workspace &ws, cudaStream_t st, uint32_t *kernels) {
+                uint32_t D, uint32_t *out, const Workspace &ws, cudaStream_t st, uint32_t *kernels,
+                uint32_t flags = 0) {
   uint32_t nk = 0;
-  if (cudaMemsetAsync(out, 0, size_t(B) * D * 4, st) != cudaSuccess) return DPF_ECUDA;
+  // a7: answers start at zero, unless the caller accumulates (DPF_EVAL_ACCUMULATE:
+  // `out` may be another rank's buffer mapped over NVLink, zeroed by its owner)
+  if (!(flags & DPF_EVAL_ACCUMULATE) && cudaMemsetAsync(out, 0, size_t(B) * D * 4, st) != cudaSuccess)
+    return DPF_ECUDA;
   // a2: levels 1..f; level k lands in front[(f-k)&1] so level f is front[0].
   if (pl.f == 0) {
     dev::copy_roots_kernel<<<(B + 127) / 128, 128, 0, st>>>(keys_dev, kstride, B, ws.front[0], pl.cap);
@@ -1212,7 +1216,7 @@ int check_common(uint32_t B, const uint32_t *table, uint64_t row_begin, uint64_t
 
 int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uint32_t log_n, uint32_t prf,
               const uint32_t *table, uint64_t row_begin, uint64_t rows, uint32_t D, uint32_t *out, void *workspace,
-              size_t ws_bytes, cudaStream_t st, bool packed = false) {
+              size_t ws_bytes, cudaStream_t st, bool packed = false, uint32_t flags = 0) {
   uint32_t n = log_n;
   if (keys) {
     if (B == 0) return DPF_EINVAL;
@@ -1277,7 +1281,7 @@ int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uin
     prep = 1;
   }
   uint32_t nk = 0;
-  rc = launch_eval(pl, kd, kstride, B, table, D, out, ws, st, &nk);
+  rc = launch_eval(pl, kd, kstride, B, table, D, out, ws, st, &nk, flags);
   if (rc) return rc;
   nk += prep;
   g_stats.prf_blocks = pl.prf_blocks;
@@ -1400,6 +1404,57 @@ extern "C" int dpf_eval_batch_wire(const uint8_t *keys_wire_dev, uint32_t B, uin
   if (!keys_wire_dev || (reinterpret_cast<uintptr_t>(keys_wire_dev) & 15)) return DPF_EINVAL;
   return eval_impl(nullptr, B, keys_wire_dev, log_n, prf, table_shard, row_begin, row_count, D, partial, workspace,
                    workspace_bytes, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int dpf_eval_batch_wire_ex(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n, uint32_t prf,
+                                      const void *table, int packed, uint64_t row_begin, uint64_t row_count,
+                                      uint32_t D, uint32_t *shares, uint32_t flags, void *workspace,
+                                      size_t workspace_bytes, void *stream) {
+  if (!keys_wire_dev || (reinterpret_cast<uintptr_t>(keys_wire_dev) & 15)) return DPF_EINVAL;
+  if (flags & ~uint32_t(DPF_EVAL_ACCUMULATE)) return DPF_EINVAL;
+  return eval_impl(nullptr, B, keys_wire_dev, log_n, prf, static_cast<const uint32_t *>(table), row_begin, row_count,
+                   D, shares, workspace, workspace_bytes, static_cast<cudaStream_t>(stream), packed != 0, flags);
+}
+
+extern "C" int dpf_ipc_export(const void *dev_ptr, uint8_t handle[DPF_IPC_HANDLE_BYTES], uint64_t *offset) {
+  if (!dev_ptr || !handle || !offset) return DPF_EINVAL;
+  static_assert(sizeof(cudaIpcMemHandle_t) == DPF_IPC_HANDLE_BYTES, "IPC handle size");
+  // The handle names the whole allocation (a caching allocator sub-allocates
+  // tensors inside it): report dev_ptr's offset from the allocation base.
+  using GetRange = int (*)(unsigned long long *, size_t *, unsigned long long);
+  static GetRange get_range = [] {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return reinterpret_cast<GetRange>(fn);
+  }();
+  if (!get_range) return DPF_ECUDA;
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, reinterpret_cast<unsigned long long>(dev_ptr)) != 0) return DPF_ECUDA;
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, const_cast<void *>(dev_ptr)) != cudaSuccess) return DPF_ECUDA;
+  std::memcpy(handle, &h, sizeof h);
+  *offset = reinterpret_cast<unsigned long long>(dev_ptr) - base;
+  return DPF_OK;
+}
+
+extern "C" int dpf_ipc_open(const uint8_t handle[DPF_IPC_HANDLE_BYTES], void **dev_ptr) {
+  if (!handle || !dev_ptr) return DPF_EINVAL;
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof h);
+  if (cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    cudaGetLastError();
+    return DPF_ECUDA;
+  }
+  return DPF_OK;
+}
+
+extern "C" int dpf_ipc_close(void *dev_ptr) {
+  if (!dev_ptr) return DPF_EINVAL;
+  return cudaIpcCloseMemHandle(dev_ptr) == cudaSuccess ? DPF_OK : DPF_ECUDA;
 }
 
 extern "C" int dpf_serve_batch(const dpf_key *keys, uint32_t B, const uint32_t *table_shard, uint64_t row_begin,

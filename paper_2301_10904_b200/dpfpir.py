@@ -85,6 +85,10 @@ def lib() -> ctypes.CDLL:
     L.dpf_eval_batch_shard.argtypes = [vp, u32, vp, u64, u64, u32, vp, vp, sz, vp]
     L.dpf_eval_batch_wire.argtypes = [vp, u32, u32, u32, vp, u64, u64, u32, vp, vp, sz, vp]
     L.dpf_serve_batch.argtypes = [vp, u32, vp, u64, u64, u32, vp, vp, sz, vp]
+    L.dpf_eval_batch_wire_ex.argtypes = [vp, u32, u32, u32, vp, ctypes.c_int, u64, u64, u32, vp, u32, vp, sz, vp]
+    L.dpf_ipc_export.argtypes = [vp, vp, ctypes.POINTER(u64)]
+    L.dpf_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
+    L.dpf_ipc_close.argtypes = [vp]
     L.dpf_eval_leaves.argtypes = [vp, u32, vp, vp, sz, vp]
     L.dpf_table_packed_bytes.argtypes = [u64, u64, u32]
     L.dpf_table_packed_bytes.restype = sz
@@ -111,6 +115,7 @@ EXPORTED_SYMBOLS = ("dpf_gen", "dpf_key_wire_size", "dpf_key_wire_size_prf", "dp
                     "dpf_serve_batch", "dpf_eval_leaves", "dpf_last_eval_stats", "dpf_eval_plan", "dpf_kernel_timer_begin",
                     "dpf_table_packed_bytes", "dpf_table_pack", "dpf_eval_batch_packed", "dpf_eval_batch_wire_packed",
                     "dpf_eval_grouped_workspace_bytes", "dpf_eval_grouped",
+                    "dpf_eval_batch_wire_ex", "dpf_ipc_export", "dpf_ipc_open", "dpf_ipc_close",
                     "dpf_kernel_timer_read", "dpf_strerror", "dpf_version")
 
 
@@ -279,6 +284,44 @@ def keys_to_wire(keys) -> np.ndarray:
         _check(lib().dpf_key_serialize(kb.ptr + i * KEY_BYTES, out[i].ctypes.data, w, ctypes.byref(written)),
                "dpf_key_serialize")
     return out
+
+
+DPF_EVAL_ACCUMULATE = 1
+IPC_HANDLE_BYTES = 64
+
+
+def eval_batch_wire_ex(keys_wire_dev, log_n: int, table, row_begin: int, row_count: int, D: int, shares_ptr: int,
+                       flags: int, workspace, stream=None, prf: int = DPF_PRF_CHACHA20, packed: bool = False):
+    """dpf_eval_batch_wire_ex: `table` is a row-major CUDA shard or a PackedTable;
+    `shares_ptr` a device address (possibly a peer rank's buffer from ipc_open)."""
+    tptr = table.data.data_ptr() if packed else table.data_ptr()
+    _check(lib().dpf_eval_batch_wire_ex(keys_wire_dev.data_ptr(), keys_wire_dev.shape[0], log_n, prf, tptr,
+                                        int(packed), row_begin, row_count, D, shares_ptr, flags,
+                                        workspace.data_ptr(), workspace.numel() * workspace.element_size(),
+                                        _stream_ptr(stream)), "dpf_eval_batch_wire_ex")
+
+
+def ipc_export(tensor) -> tuple[bytes, int]:
+    """dpf_ipc_export: (64-byte CUDA IPC handle of the allocation holding a CUDA
+    tensor, the tensor's byte offset inside it)."""
+    h = (ctypes.c_uint8 * IPC_HANDLE_BYTES)()
+    off = ctypes.c_uint64()
+    _check(lib().dpf_ipc_export(tensor.data_ptr(), h, ctypes.byref(off)), "dpf_ipc_export")
+    return bytes(h), int(off.value)
+
+
+def ipc_open(handle: bytes) -> int:
+    """dpf_ipc_open: map another process's allocation; returns its base device address."""
+    if len(handle) != IPC_HANDLE_BYTES:
+        raise ValueError("IPC handle must be %d bytes" % IPC_HANDLE_BYTES)
+    p = ctypes.c_void_p()
+    _check(lib().dpf_ipc_open((ctypes.c_uint8 * IPC_HANDLE_BYTES).from_buffer_copy(handle), ctypes.byref(p)),
+           "dpf_ipc_open")
+    return int(p.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _check(lib().dpf_ipc_close(ptr), "dpf_ipc_close")
 
 
 def eval_batch_wire(keys_wire_dev, log_n: int, table_shard, row_begin: int = 0, out=None, workspace=None,
