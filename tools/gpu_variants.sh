@@ -1,3 +1,12 @@
 #!/bin/bash
-DPF_ET_W=2 timeout 300 python -m pytest tests -m gpu -q -x --timeout 120 -k "et" 2>&1 | tail -2
-for v in "" "DPF_ET_W=2"; do for c in c3 t5; do echo "== $v $c"; env $v bash tools/bench_brief.sh $c --prf chacha20_et --steps 10 | cut -c1-140; done; done
+timeout 600 python tools/shard_sim.py --config c3 > gpurun_out/shard_sim.jsonl 2>&1
+timeout 600 python tools/shard_sim.py --config c3 --prf chacha20_et >> gpurun_out/shard_sim.jsonl 2>&1
+timeout 900 python tools/shard_sim.py --config c4 --steps 3 >> gpurun_out/shard_sim.jsonl 2>&1
+timeout 600 python tools/shard_sim.py --config c4 --prf chacha20_et --steps 5 >> gpurun_out/shard_sim.jsonl 2>&1
+timeout 600 python tools/shard_sim.py --config c3 --rank -1 --shards 8 >> gpurun_out/shard_sim.jsonl 2>&1
+python -c "
+import json
+for l in open('gpurun_out/shard_sim.jsonl'):
+    try: d=json.loads(l)
+    except Exception: print(l[:200]); continue
+    print(d['config'], d['prf'], d['G'], d['rows'], d['ms_per_gpu'], d['kernel_frac'], d['step_frac'], d['projected_qps'])"
