@@ -129,59 +129,58 @@ __device__ __forceinline__ const uint4 *key_cw(const uint8_t *k, uint32_t d) {
 }
 
 // ----------------------------------------------------------------- a2: top BFS
-// One launch per level k = 1..f.  Level k's nodes intersecting the row range
-// [r0, r1) are [lo_k, hi_k], lo_k = r0 >> (n-k); stored at [i - lo_k].
-// Thread per (key, parent): both children by one block (R9), kept if in range.
-template <class Prf>
-__global__ void expand_level_kernel(const uint8_t *__restrict__ keys, uint32_t kstride, uint32_t B, uint32_t n,
-                                    uint32_t k, uint64_t r0, uint64_t r1, const uint4 *__restrict__ in,
-                                    uint4 *__restrict__ out, uint64_t cap) {
-  const uint64_t plo = r0 >> (n - (k - 1)), phi = (r1 - 1) >> (n - (k - 1));
-  const uint64_t lo = r0 >> (n - k), hi = (r1 - 1) >> (n - k);
-  const uint64_t np = phi - plo + 1;
-  const uint64_t total = np * B;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t b = uint32_t(i / np);
-    const uint64_t p = plo + (i % np);
-    const uint8_t *key = keys + uint64_t(b) * kstride;
-    const uint4 s = (k == 1) ? key_root(key) : in[uint64_t(b) * cap + (p - plo)];
-    uint4 c0, c1;
-    node_children<Prf>(s, key_cw(key, k), c0, c1);
-    const uint64_t j0 = 2 * p, j1 = 2 * p + 1;
-    if (j0 >= lo && j0 <= hi) out[uint64_t(b) * cap + (j0 - lo)] = c0;
-    if (j1 >= lo && j1 <= hi) out[uint64_t(b) * cap + (j1 - lo)] = c1;
-  }
-}
-
-// Levels 1..a (a <= kTopSmemLevels) of every key in one launch: one CTA per
-// key expands level by level in shared memory (ping-pong), then writes level a
-// to `out`.  Removes a-1 kernel boundaries from the top of the tree.
+// Levels 1..f of every key (P:428 level-by-level, only for the small top of
+// the tree).  Level k's nodes intersecting the row range [r0, r1) are
+// [lo_k, hi_k], lo_k = r0 >> (n-k); the frontier stores node i at [i - lo_f].
+// Each expanded parent yields both children from one block (R9).
 constexpr uint32_t kTopSmemLevels = 10;
+// a2 in ONE launch for any frontier depth f: CTA (key b, j) owns level-s
+// node p = lo_s + j of the range's level-s nodes; thread 0 walks the root
+// path to it (s blocks, Eq. 3 along the bits of p), then levels s+1..f of its
+// subtree (intersected with [r0, r1)) expand breadth-first in shared memory
+// (<= 2^kTopSmemLevels nodes per level) and level f goes to the frontier.
+// Replaces one launch per level below 2^10 nodes; s also spreads small
+// batches over the SMs (the s path blocks per CTA are redundant work:
+// B * 2^s * s blocks, << the B * 2^f of the frontier).
 template <class Prf>
-__global__ void __launch_bounds__(256) expand_top_smem_kernel(const uint8_t *__restrict__ keys, uint32_t kstride,
-                                                              uint32_t n, uint32_t a, uint64_t r0, uint64_t r1,
-                                                              uint4 *__restrict__ out, uint64_t cap) {
+__global__ void __launch_bounds__(256) expand_top_split_kernel(const uint8_t *__restrict__ keys, uint32_t kstride,
+                                                               uint32_t n, uint32_t s, uint32_t f, uint64_t r0,
+                                                               uint64_t r1, uint4 *__restrict__ out, uint64_t cap) {
   __shared__ uint4 buf[2][1u << kTopSmemLevels];
-  const uint32_t b = blockIdx.x;
+  const uint64_t lo_s = r0 >> (n - s), cnt_s = ((r1 - 1) >> (n - s)) - lo_s + 1;
+  const uint32_t b = uint32_t(blockIdx.x / cnt_s);
+  const uint64_t ps = lo_s + blockIdx.x % cnt_s;  // this CTA's level-s node
   const uint8_t *key = keys + uint64_t(b) * kstride;
-  if (threadIdx.x == 0) buf[0][0] = key_root(key);
+  if (threadIdx.x == 0) {
+    uint4 x = key_root(key);
+    for (uint32_t d = 1; d <= s; ++d) {
+      uint4 c0, c1;
+      node_children<Prf>(x, key_cw(key, d), c0, c1);
+      x = ((ps >> (s - d)) & 1) ? c1 : c0;
+    }
+    buf[s & 1][0] = x;
+  }
   __syncthreads();
-  for (uint32_t k = 1; k <= a; ++k) {
-    const uint64_t plo = r0 >> (n - (k - 1)), phi = (r1 - 1) >> (n - (k - 1));
-    const uint64_t lo = r0 >> (n - k), hi = (r1 - 1) >> (n - k);
+  // level k of the subtree: [ps << (k-s), ((ps+1) << (k-s)) - 1] intersected with the range
+  uint64_t plo = ps, phi = ps;
+  for (uint32_t k = s + 1; k <= f; ++k) {
+    const uint64_t lo = max(ps << (k - s), r0 >> (n - k));
+    const uint64_t hi = min(((ps + 1) << (k - s)) - 1, (r1 - 1) >> (n - k));
     const uint4 *in = buf[(k - 1) & 1];
     uint4 *o = buf[k & 1];
     for (uint64_t p = plo + threadIdx.x; p <= phi; p += blockDim.x) {
       uint4 c0, c1;
       node_children<Prf>(in[p - plo], key_cw(key, k), c0, c1);
-      if (2 * p >= lo) o[2 * p - lo] = c0;
-      if (2 * p + 1 <= hi) o[2 * p + 1 - lo] = c1;
+      if (2 * p >= lo && 2 * p <= hi) o[2 * p - lo] = c0;
+      if (2 * p + 1 >= lo && 2 * p + 1 <= hi) o[2 * p + 1 - lo] = c1;
     }
     __syncthreads();
+    plo = lo;
+    phi = hi;
   }
-  const uint64_t cnt = ((r1 - 1) >> (n - a)) - (r0 >> (n - a)) + 1;
-  for (uint64_t i = threadIdx.x; i < cnt; i += blockDim.x) out[uint64_t(b) * cap + i] = buf[a & 1][i];
+  const uint64_t lo_f = r0 >> (n - f);
+  for (uint64_t i = threadIdx.x; i <= phi - plo; i += blockDim.x)
+    out[uint64_t(b) * cap + (plo - lo_f) + i] = buf[f & 1][i];
 }
 
 // f == 0: the frontier is the root itself.
@@ -991,6 +990,10 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
   // co-resident CTA pairs: a GPC with an odd SM count leaves an SM unpaired
   const uint32_t workers = pl.pair ? max_pairs(fixed + size_t(m_cap) * 32 * kTcNP * 16) : uint32_t(num_sms());
   pl.m = choose_m_target(pl, n, m_min, m_cap, workers);
+  if (const char *e = getenv("DPF_FORCE_M")) {  // tuning override
+    const uint32_t fm = uint32_t(atoi(e));
+    if (fm >= m_min && fm <= std::min<uint32_t>(n, m_cap)) pl.m = fm;
+  }
   pl.f = n - pl.m;
   pl.lo_f = pl.nr0 >> pl.m;
   pl.F = ((pl.nr1 - 1) >> pl.m) - pl.lo_f + 1;
@@ -1073,28 +1076,19 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
   }
   // The top of the tree works on tree-leaf (final node) ranges [nr0, nr1):
   // with early termination (R20) the levels are Eq. 3 ChaCha20 levels.
-  const uint32_t a = std::min(pl.f, dev::kTopSmemLevels);
-  if (a >= 1) {
+  // One launch: split depth s keeps <= 2^10 nodes per CTA and >= 2 CTAs per SM.
+  if (pl.f >= 1) {
+    uint32_t s = pl.f > dev::kTopSmemLevels ? pl.f - dev::kTopSmemLevels : 0;
+    while (s < pl.f && (uint64_t(B) << s) < 2ull * num_sms()) ++s;
+    const uint64_t cnt_s = ((pl.nr1 - 1) >> (pl.n - s)) - (pl.nr0 >> (pl.n - s)) + 1;
+    const uint64_t grid = uint64_t(B) * cnt_s;
+    if (grid > 0x7FFFFFFFull) return DPF_EINVAL;
     if (pl.prf == DPF_PRF_AES128)
-      dev::expand_top_smem_kernel<dev::PrfAesBs><<<B, 256, 0, st>>>(keys_dev, kstride, pl.n, a, pl.nr0, pl.nr1,
-                                                                   ws.front[(pl.f - a) & 1], pl.cap);
+      dev::expand_top_split_kernel<dev::PrfAesBs><<<uint32_t(grid), 256, 0, st>>>(
+          keys_dev, kstride, pl.n, s, pl.f, pl.nr0, pl.nr1, ws.front[0], pl.cap);
     else
-      dev::expand_top_smem_kernel<dev::PrfChacha><<<B, 256, 0, st>>>(keys_dev, kstride, pl.n, a, pl.nr0, pl.nr1,
-                                                                    ws.front[(pl.f - a) & 1], pl.cap);
-    ++nk;
-  }
-  for (uint32_t k = a + 1; k <= pl.f; ++k) {
-    const uint64_t np = ((pl.nr1 - 1) >> (pl.n - (k - 1))) - (pl.nr0 >> (pl.n - (k - 1))) + 1;
-    const uint64_t total = np * B;
-    const uint32_t grid = uint32_t(std::min<uint64_t>((total + 255) / 256, 148ull * 16));
-    if (pl.prf == DPF_PRF_AES128)
-      dev::expand_level_kernel<dev::PrfAesBs><<<grid, 256, 0, st>>>(keys_dev, kstride, B, pl.n, k, pl.nr0, pl.nr1,
-                                                                   ws.front[(pl.f - k + 1) & 1],
-                                                                   ws.front[(pl.f - k) & 1], pl.cap);
-    else
-      dev::expand_level_kernel<dev::PrfChacha><<<grid, 256, 0, st>>>(keys_dev, kstride, B, pl.n, k, pl.nr0, pl.nr1,
-                                                                    ws.front[(pl.f - k + 1) & 1],
-                                                                    ws.front[(pl.f - k) & 1], pl.cap);
+      dev::expand_top_split_kernel<dev::PrfChacha><<<uint32_t(grid), 256, 0, st>>>(
+          keys_dev, kstride, pl.n, s, pl.f, pl.nr0, pl.nr1, ws.front[0], pl.cap);
     ++nk;
   }
   const bool timed = g_timer.on && 2 * g_timer.used + 1 < g_timer.ev.size();

@@ -1,12 +1,5 @@
 #!/bin/bash
-timeout 600 python tools/shard_sim.py --config c3 > gpurun_out/shard_sim.jsonl 2>&1
-timeout 600 python tools/shard_sim.py --config c3 --prf chacha20_et >> gpurun_out/shard_sim.jsonl 2>&1
-timeout 900 python tools/shard_sim.py --config c4 --steps 3 >> gpurun_out/shard_sim.jsonl 2>&1
-timeout 600 python tools/shard_sim.py --config c4 --prf chacha20_et --steps 5 >> gpurun_out/shard_sim.jsonl 2>&1
-timeout 600 python tools/shard_sim.py --config c3 --rank -1 --shards 8 >> gpurun_out/shard_sim.jsonl 2>&1
-python -c "
-import json
-for l in open('gpurun_out/shard_sim.jsonl'):
-    try: d=json.loads(l)
-    except Exception: print(l[:200]); continue
-    print(d['config'], d['prf'], d['G'], d['rows'], d['ms_per_gpu'], d['kernel_frac'], d['step_frac'], d['projected_qps'])"
+timeout 900 python -m pytest tests -m gpu -q -x --timeout 600 2>&1 | tail -2
+for a in "c2" "c2 --prf chacha20_et" "c3" "c3 --prf chacha20_et" "t5 --prf chacha20_et" "c1"; do echo "== $a"; bash tools/bench_brief.sh $a --steps 30 | cut -c1-120; done
+timeout 600 python tools/batch_sweep.py --log-n 22 --D 64 --B 1 2 4 > gpurun_out/bs.jsonl 2>&1; cut -c1-150 gpurun_out/bs.jsonl
+timeout 600 python tools/shard_sim.py --config c3 --prf chacha20_et 2>&1 | cut -c1-160
