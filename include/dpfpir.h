@@ -271,6 +271,16 @@ size_t dpf_eval_grouped_workspace_bytes(const dpf_eval_group *groups, uint32_t n
 int dpf_eval_grouped(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D, uint32_t prf, void *workspace,
                      size_t workspace_bytes, void *stream);
 
+/* The same on the tensor cores: every group's `table` is its limb-packed
+ * shard (dpf_table_pack with that group's row_begin, row_count and D); the
+ * groups share one tcgen05 configuration (key tile = MMA N chosen to
+ * minimise the padded work).  Requires log_n >= 3 (5 with early
+ * termination).  Same errors. */
+size_t dpf_eval_grouped_packed_workspace_bytes(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D,
+                                               uint32_t prf);
+int dpf_eval_grouped_packed(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D, uint32_t prf,
+                            void *workspace, size_t workspace_bytes, void *stream);
+
 /* End-to-end serving call: as dpf_eval_batch_shard, but shares_host is a HOST
  * buffer (pinned for best speed) that receives the B x D answers; the call
  * synchronises `stream` before returning.  The table stays device-resident

@@ -1061,6 +1061,58 @@ struct Staging {
 };
 thread_local Staging g_staging;
 
+// The tcgen05 fused kernel (single CTAs or CTA pairs) for a plan, timed by
+// the optional kernel timer.  Used by single-table and grouped launches.
+int launch_tc_kernel(const Plan &pl, const dev::FusedParams &p, cudaStream_t st) {
+  const bool timed = g_timer.on && 2 * g_timer.used + 1 < g_timer.ev.size();
+  dev::TcParams tp;
+  tp.f = p;
+  tp.y_stage_bytes = pl.y_stage_bytes;
+  tp.tmem_cols = pl.tmem_cols;
+  static const uint32_t spin = [] {
+    const char *e = getenv("DPF_LOADER_SPIN");
+    return uint32_t(e && atoi(e) == 1);
+  }();
+  tp.loader_spin = spin;
+  static const uint32_t nomma = [] {
+    const char *e = getenv("DPF_DEBUG_NOMMA");
+    return uint32_t(e && atoi(e) == 1);
+  }();
+  tp.debug_nomma = nomma;
+  using TcFn = void (*)(const dev::TcParams);
+  TcFn fn;
+  if (pl.prf == DPF_PRF_AES128)
+    fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, true>
+                 : &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, false>;
+  else if (pl.prf == DPF_PRF_CHACHA20_ET)
+    fn = pl.pair ? (pl.nsy == 3 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 3, 4, true>
+                                : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, true>)
+                 : (pl.nsy == 3 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 3, 4, false>
+                                : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, false>);
+  else
+    fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, true>
+                 : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, false>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
+    return DPF_ECUDA;
+  cudaLaunchConfig_t cfg;
+  std::memset(&cfg, 0, sizeof cfg);
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(32 * (kTcNP + 4 + 1));
+  cfg.dynamicSmemBytes = pl.smem_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = pl.pair ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
+  if (cudaLaunchKernelEx(&cfg, fn, tp) != cudaSuccess) return DPF_ECUDA;
+  if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used++ + 1], st);
+  return cudaGetLastError() == cudaSuccess ? DPF_OK : DPF_ECUDA;
+}
+
 int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint32_t B, const uint32_t *table,
                 uint32_t D, uint32_t *out, const Workspace &ws, cudaStream_t st, uint32_t *kernels,
                 uint32_t flags = 0) {
@@ -1134,53 +1186,9 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
   p.n_chunks = pl.n_chunks;
   p.NST = pl.NST;
   if (pl.tc) {
-    dev::TcParams tp;
-    tp.f = p;
-    tp.y_stage_bytes = pl.y_stage_bytes;
-    tp.tmem_cols = pl.tmem_cols;
-    static const uint32_t spin = [] {
-      const char *e = getenv("DPF_LOADER_SPIN");
-      return uint32_t(e && atoi(e) == 1);
-    }();
-    tp.loader_spin = spin;
-    static const uint32_t nomma = [] {
-      const char *e = getenv("DPF_DEBUG_NOMMA");
-      return uint32_t(e && atoi(e) == 1);
-    }();
-    tp.debug_nomma = nomma;
-    using TcFn = void (*)(const dev::TcParams);
-    TcFn fn;
-    if (pl.prf == DPF_PRF_AES128)
-      fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, true>
-                   : &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, false>;
-    else if (pl.prf == DPF_PRF_CHACHA20_ET)
-      fn = pl.pair ? (pl.nsy == 3 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 3, 4, true>
-                                  : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, true>)
-                   : (pl.nsy == 3 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 3, 4, false>
-                                  : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, false>);
-    else
-      fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, true>
-                   : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, false>;
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
-      return DPF_ECUDA;
-    cudaLaunchConfig_t cfg;
-    std::memset(&cfg, 0, sizeof cfg);
-    cfg.gridDim = dim3(pl.grid);
-    cfg.blockDim = dim3(32 * (kTcNP + 4 + 1));
-    cfg.dynamicSmemBytes = pl.smem_bytes;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = pl.pair ? 2 : 1;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
-    if (cudaLaunchKernelEx(&cfg, fn, tp) != cudaSuccess) return DPF_ECUDA;
-    if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used++ + 1], st);
+    const int rc = launch_tc_kernel(pl, p, st);
+    if (rc) return rc;
     ++nk;
-    if (cudaGetLastError() != cudaSuccess) return DPF_ECUDA;
     if (kernels) *kernels = nk;
     return DPF_OK;
   }
@@ -1546,7 +1554,11 @@ struct GroupedPlan {
 // largest batch; per group the subtree depth m_g keeps >= Ft frontier nodes
 // per key and f_g = n_g - m_g <= kTopSmemLevels (one grouped top launch);
 // items ordered by subtree size so the static round-robin stays balanced.
-int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t prf, GroupedPlan &gp) {
+int make_grouped_tc_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t prf, GroupedPlan &gp);
+
+int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t prf, GroupedPlan &gp,
+                      bool packed = false) {
+  if (packed) return make_grouped_tc_plan(gs, G, D, prf, gp);
   if (!gs || G == 0 || D == 0 || D > 1024 || (D & 3)) return DPF_EINVAL;
   if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128 && prf != DPF_PRF_CHACHA20_ET) return DPF_EUNSUPPORTED;
   const bool et = prf == DPF_PRF_CHACHA20_ET;
@@ -1680,6 +1692,121 @@ int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t
   return DPF_OK;
 }
 
+// Groups share one tcgen05 configuration (MMA N = key tile, window, rings):
+// the key tile minimises the padded work sum_g ceil(B_g/N) N rows_g (larger
+// on ties); per group the subtree depth as in the IMAD planner (>= 8 items
+// per worker overall, >= one window per subtree); tables are limb-packed
+// (dpf_table_pack with the group's row_begin / row_count).
+int make_grouped_tc_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t prf, GroupedPlan &gp) {
+  if (!gs || G == 0 || D == 0 || D > 1024 || (D & 3)) return DPF_EINVAL;
+  if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128 && prf != DPF_PRF_CHACHA20_ET) return DPF_EUNSUPPORTED;
+  const bool et = prf == DPF_PRF_CHACHA20_ET;
+  const uint32_t v = et ? DPF_ET_BITS : 0u;
+  const uint32_t m_min = et ? 1 : 3;
+  for (uint32_t i = 0; i < G; ++i) {
+    const dpf_eval_group &g = gs[i];
+    if (!g.keys_wire || !g.table || !g.shares || g.B == 0 || g.log_n < m_min + v || g.log_n > DPF_MAX_LOG_N ||
+        g.row_count == 0)
+      return DPF_EINVAL;
+    const uint64_t dom = 1ull << g.log_n;
+    if (g.row_begin >= dom || g.row_count > dom - g.row_begin) return DPF_EINVAL;
+    if ((reinterpret_cast<uintptr_t>(g.table) & 15) || (reinterpret_cast<uintptr_t>(g.keys_wire) & 15))
+      return DPF_EINVAL;
+  }
+  // shared MMA N: probe the single-table planner's TMEM rule with B = N
+  Plan probe;
+  if (make_tc_plan(1u << 30, 20, 0, 1u << 20, D, probe, et) != DPF_OK) return DPF_EINVAL;
+  const uint32_t nmax = probe.pair ? 2 * probe.Kt : probe.Kt, nmin = probe.pair ? 32 : 16;
+  uint32_t best = nmax;
+  double best_cost = -1;
+  for (uint32_t k = nmin; k <= nmax; k <<= 1) {
+    double cost = 0;
+    for (uint32_t i = 0; i < G; ++i) cost += double((gs[i].B + k - 1) / k) * k * double(gs[i].row_count);
+    if (best_cost < 0 || cost <= best_cost) {
+      best_cost = cost;
+      best = k;
+    }
+  }
+  Plan &pl = gp.cfg;
+  int rc = make_tc_plan(best, 20, 0, 1u << 20, D, pl, et);
+  if (rc) return rc;
+  pl.prf = prf;
+  const uint32_t Ktp = pl.pair ? 2 * pl.Kt : pl.Kt;
+  const size_t fixed = 1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(pl.nsy) * pl.y_stage_bytes;
+  const size_t level_bytes = size_t(32) * kTcNP * 16;
+  uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / level_bytes));
+  const uint32_t workers = pl.pair ? max_pairs(fixed + size_t(m_cap) * level_bytes) : uint32_t(num_sms());
+  {
+    double units = 0;
+    for (uint32_t i = 0; i < G; ++i) units += double((gs[i].B + Ktp - 1) / Ktp) * double(gs[i].row_count >> v);
+    const double per_item = units / (double(pl.Ft) * 8.0 * workers);
+    uint32_t m_bal = 1;
+    while (m_bal < 14 && double(2u << m_bal) <= per_item) ++m_bal;
+    m_cap = std::min(m_cap, std::max(m_bal, m_min));
+  }
+  if (m_cap < m_min) return DPF_EINVAL;
+  gp.desc.assign(G, dev::GroupDesc{});
+  uint32_t lg_ft = 0;
+  while ((2u << lg_ft) <= pl.Ft) ++lg_ft;
+  uint32_t m_max = 0;
+  for (uint32_t i = 0; i < G; ++i) {
+    const dpf_eval_group &g = gs[i];
+    dev::GroupDesc &d = gp.desc[i];
+    const uint32_t n = g.log_n - v;
+    uint32_t lg_rows = 0;
+    while ((2ull << lg_rows) <= (g.row_count >> v)) ++lg_rows;
+    uint32_t m = lg_rows > lg_ft ? lg_rows - lg_ft : 1;
+    m = std::max(m_min, std::min(std::min(m, n), m_cap));
+    d.n = n;
+    d.m = m;
+    d.r0 = g.row_begin;
+    d.r1 = g.row_begin + g.row_count;
+    d.nr0 = d.r0 >> v;
+    d.nr1 = ((d.r1 - 1) >> v) + 1;
+    d.lo_f = d.nr0 >> m;
+    d.F = ((d.nr1 - 1) >> m) - d.lo_f + 1;
+    d.cap = d.F;
+    d.r0a = d.r0 & ~7ull;
+    d.packed_rows = ((d.r1 + 7) & ~7ull) - d.r0a;
+    d.B = g.B;
+    d.kstride = uint32_t(dpf_key_wire_size_prf(g.log_n, prf));
+    d.n_ktiles = (g.B + Ktp - 1) / Ktp;
+    d.T = g.table;
+    d.shares = g.shares;
+    d.nwin = (et ? (1u << m) : (1u << (m - 1))) / pl.W;
+    m_max = std::max(m_max, m);
+  }
+  pl.smem_bytes = fixed + size_t(m_max) * level_bytes;
+  gp.order.resize(G);
+  for (uint32_t i = 0; i < G; ++i) gp.order[i] = i;
+  std::stable_sort(gp.order.begin(), gp.order.end(),
+                   [&](uint32_t a, uint32_t b) { return gp.desc[a].m > gp.desc[b].m; });
+  uint64_t items = 0, keys = 0, blocks = 0;
+  gp.front_bytes = 0;
+  gp.keys_bytes = 0;
+  for (uint32_t oi : gp.order) {
+    dev::GroupDesc &d = gp.desc[oi];
+    d.item_base = uint32_t(items);
+    d.key_base = uint32_t(keys);
+    const uint64_t it = uint64_t(d.n_ktiles) * ((d.F + pl.Ft - 1) / pl.Ft);
+    items += it;
+    keys += d.B;
+    gp.front_bytes += 2 * align_up(size_t(d.B) * d.cap * 16, kAlign);
+    gp.keys_bytes += align_up(size_t(d.B) * d.kstride, kAlign);
+    uint64_t top = 0;
+    for (uint32_t k = 0; k < d.n - d.m; ++k) top += ((d.nr1 - 1) >> (d.n - k)) - (d.nr0 >> (d.n - k)) + 1;
+    const uint64_t per = ((1ull << d.m) - 1) + (et ? (1ull << d.m) : 0);
+    blocks += uint64_t(d.B) * top + it * pl.tasks * per;
+  }
+  if (items > 0x7FFFFFFFull || keys > 0x7FFFFFFFull) return DPF_EINVAL;
+  pl.n_items = uint32_t(items);
+  pl.prf_blocks = blocks;
+  pl.grid = pl.pair ? 2 * std::min<uint32_t>(pl.n_items, workers) : std::min<uint32_t>(pl.n_items, workers);
+  gp.desc_bytes = align_up(size_t(G) * sizeof(dev::GroupDesc), kAlign);
+  gp.total_bytes = gp.front_bytes + gp.keys_bytes + gp.desc_bytes;
+  return DPF_OK;
+}
+
 thread_local Staging g_desc_staging;
 
 }  // namespace
@@ -1692,12 +1819,39 @@ extern "C" size_t dpf_eval_grouped_workspace_bytes(const dpf_eval_group *groups,
   return gp.total_bytes;
 }
 
+extern "C" size_t dpf_eval_grouped_packed_workspace_bytes(const dpf_eval_group *groups, uint32_t n_groups,
+                                                          uint32_t D, uint32_t prf) {
+  GroupedPlan gp;
+  if (make_grouped_plan(groups, n_groups, D, prf, gp, true) != DPF_OK) return 0;
+  return gp.total_bytes;
+}
+
+namespace dpfpir {
+namespace {
+int eval_grouped_impl(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D, uint32_t prf, void *workspace,
+                      size_t workspace_bytes, void *stream, bool packed);
+}
+}  // namespace dpfpir
+
 extern "C" int dpf_eval_grouped(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D, uint32_t prf,
                                 void *workspace, size_t workspace_bytes, void *stream) {
+  return dpfpir::eval_grouped_impl(groups, n_groups, D, prf, workspace, workspace_bytes, stream, false);
+}
+
+extern "C" int dpf_eval_grouped_packed(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D, uint32_t prf,
+                                       void *workspace, size_t workspace_bytes, void *stream) {
+  return dpfpir::eval_grouped_impl(groups, n_groups, D, prf, workspace, workspace_bytes, stream, true);
+}
+
+namespace dpfpir {
+namespace {
+
+int eval_grouped_impl(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D, uint32_t prf, void *workspace,
+                      size_t workspace_bytes, void *stream, bool packed) {
   if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128 && prf != DPF_PRF_CHACHA20_ET) return DPF_EUNSUPPORTED;
   if (!workspace || (reinterpret_cast<uintptr_t>(workspace) & (kAlign - 1))) return DPF_EINVAL;
   GroupedPlan gp;
-  int rc = make_grouped_plan(groups, n_groups, D, prf, gp);
+  int rc = make_grouped_plan(groups, n_groups, D, prf, gp, packed);
   if (rc) return rc;
   if (workspace_bytes < gp.total_bytes) return DPF_ENOMEM;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -1789,15 +1943,19 @@ extern "C" int dpf_eval_grouped(const dpf_eval_group *groups, uint32_t n_groups,
   p.CN = pl.CN;
   p.n_chunks = pl.n_chunks;
   p.NST = pl.NST;
-  auto kfn = pl.kc.get(prf);
-  if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
-    return DPF_ECUDA;
-  const bool timed = g_timer.on && 2 * g_timer.used + 1 < g_timer.ev.size();
-  if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
-  kfn<<<pl.grid, 32 * (pl.kc.NP + kNC + 1), pl.smem_bytes, st>>>(p);
-  if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used++ + 1], st);
+  if (pl.tc) {
+    if ((rc = launch_tc_kernel(pl, p, st)) != DPF_OK) return rc;
+  } else {
+    auto kfn = pl.kc.get(prf);
+    if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
+      return DPF_ECUDA;
+    const bool timed = g_timer.on && 2 * g_timer.used + 1 < g_timer.ev.size();
+    if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
+    kfn<<<pl.grid, 32 * (pl.kc.NP + kNC + 1), pl.smem_bytes, st>>>(p);
+    if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used++ + 1], st);
+    if (cudaGetLastError() != cudaSuccess) return DPF_ECUDA;
+  }
   ++nk;
-  if (cudaGetLastError() != cudaSuccess) return DPF_ECUDA;
   g_stats.prf_blocks = pl.prf_blocks;
   g_stats.kernels = nk;
   g_stats.frontier_depth = 0;
@@ -1807,3 +1965,6 @@ extern "C" int dpf_eval_grouped(const dpf_eval_group *groups, uint32_t n_groups,
   g_stats.grid = pl.grid;
   return DPF_OK;
 }
+
+}  // namespace
+}  // namespace dpfpir

@@ -98,6 +98,9 @@ def lib() -> ctypes.CDLL:
     L.dpf_eval_grouped_workspace_bytes.argtypes = [vp, u32, u32, u32]
     L.dpf_eval_grouped_workspace_bytes.restype = sz
     L.dpf_eval_grouped.argtypes = [vp, u32, u32, u32, vp, sz, vp]
+    L.dpf_eval_grouped_packed_workspace_bytes.argtypes = [vp, u32, u32, u32]
+    L.dpf_eval_grouped_packed_workspace_bytes.restype = sz
+    L.dpf_eval_grouped_packed.argtypes = [vp, u32, u32, u32, vp, sz, vp]
     L.dpf_last_eval_stats.argtypes = [vp]
     L.dpf_eval_plan.argtypes = [u32, u32, u32, u64, u64, u32, ctypes.c_int, vp]
     L.dpf_kernel_timer_begin.argtypes = [u32]
@@ -115,6 +118,7 @@ EXPORTED_SYMBOLS = ("dpf_gen", "dpf_key_wire_size", "dpf_key_wire_size_prf", "dp
                     "dpf_serve_batch", "dpf_eval_leaves", "dpf_last_eval_stats", "dpf_eval_plan", "dpf_kernel_timer_begin",
                     "dpf_table_packed_bytes", "dpf_table_pack", "dpf_eval_batch_packed", "dpf_eval_batch_wire_packed",
                     "dpf_eval_grouped_workspace_bytes", "dpf_eval_grouped",
+                    "dpf_eval_grouped_packed_workspace_bytes", "dpf_eval_grouped_packed",
                     "dpf_eval_batch_wire_ex", "dpf_ipc_export", "dpf_ipc_open", "dpf_ipc_close",
                     "dpf_kernel_timer_read", "dpf_strerror", "dpf_version")
 
@@ -402,15 +406,23 @@ def eval_batch_wire_packed(keys_wire_dev, log_n: int, packed: PackedTable, out=N
 
 
 def _group_array(groups):
+    """groups: (keys_wire, log_n, table, row_begin, shares); `table` a row-major
+    CUDA shard or a PackedTable (dpf_eval_grouped_packed)."""
     arr = (DpfEvalGroup * len(groups))()
     for i, g in enumerate(groups):
         keys_wire, log_n, table, row_begin, shares = g
         arr[i].keys_wire = keys_wire.data_ptr()
         arr[i].B = keys_wire.shape[0]
         arr[i].log_n = log_n
-        arr[i].table = table.data_ptr()
+        if isinstance(table, PackedTable):
+            arr[i].table = table.data.data_ptr()
+            arr[i].row_count = table.row_count
+            if table.row_begin != row_begin:
+                raise ValueError("packed table row_begin differs from the group's")
+        else:
+            arr[i].table = table.data_ptr()
+            arr[i].row_count = table.shape[0]
         arr[i].row_begin = row_begin
-        arr[i].row_count = table.shape[0]
         arr[i].shares = shares.data_ptr()
     return arr
 
@@ -430,6 +442,24 @@ def eval_grouped(groups, D: int, prf: int = DPF_PRF_CHACHA20, workspace=None, st
     ws = workspace if workspace is not None else _workspace(need, dev)
     _check(lib().dpf_eval_grouped(arr, len(groups), D, prf, ws.data_ptr(), ws.numel() * ws.element_size(),
                                   _stream_ptr(stream)), "dpf_eval_grouped")
+    return [g[4] for g in groups]
+
+
+def eval_grouped_packed_workspace_bytes(groups, D: int, prf: int = DPF_PRF_CHACHA20) -> int:
+    return lib().dpf_eval_grouped_packed_workspace_bytes(_group_array(groups), len(groups), D, prf)
+
+
+def eval_grouped_packed(groups, D: int, prf: int = DPF_PRF_CHACHA20, workspace=None, stream=None):
+    """dpf_eval_grouped_packed: as eval_grouped with every group's table a
+    PackedTable (table_pack of that group's shard), tcgen05 contraction."""
+    arr = _group_array(groups)
+    need = lib().dpf_eval_grouped_packed_workspace_bytes(arr, len(groups), D, prf)
+    if need == 0:
+        raise DpfError(DPF_EINVAL, "dpf_eval_grouped_packed_workspace_bytes")
+    dev = groups[0][4].device
+    ws = workspace if workspace is not None else _workspace(need, dev)
+    _check(lib().dpf_eval_grouped_packed(arr, len(groups), D, prf, ws.data_ptr(), ws.numel() * ws.element_size(),
+                                         _stream_ptr(stream)), "dpf_eval_grouped_packed")
     return [g[4] for g in groups]
 
 

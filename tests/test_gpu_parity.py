@@ -500,3 +500,29 @@ def test_grouped_early_termination(dp, oracle, kt_keys):
     torch.cuda.synchronize()
     for (wire, n, Td, r0, out), want in zip(groups, expect):
         np.testing.assert_array_equal(dp.as_u32(out), want)
+
+
+@pytest.mark.parametrize("prf,D", [(1, 32), (3, 32), (1, 256), (3, 64), (2, 128)])
+def test_grouped_packed_tc(dp, oracle, prf, D):
+    """dpf_eval_grouped_packed: many (keys, limb-packed table) groups through the
+    tcgen05 kernel (CTA pairs at D = 256) in one launch; mixed key counts, ragged
+    row ranges, tiny and deep domains."""
+    shapes = [(14, 1 << 14, 0, 1 << 14, 40), (12, 3001, 0, 3001, 17), (10, 1000, 37, 900, 3), (16, 60000, 0, 60000, 33),
+              (9, 300, 0, 300, 1), (13, 5000, 4096, 904, 64)]
+    groups, expect = [], []
+    for i, (n, N, r0, rows, B) in enumerate(shapes):
+        if prf == 2 and n > 12:
+            continue
+        T = synth.table(N, D, 990 + i)
+        al = synth.alphas(B, N, 990 + i)
+        keys = [dp.gen(n, int(a), 1, s, prf=prf)[(j + i) % 2] for j, (a, s) in enumerate(zip(al, synth.gen_seeds(B, 995 + i)))]
+        okeys = [oracle.key_from_wire(dp.key_serialize(k)) for k in keys]
+        Tsh = T[r0:r0 + rows]
+        wire = torch.from_numpy(dp.keys_to_wire(keys)).cuda()
+        out = torch.empty((B, D), dtype=torch.int32, device="cuda")
+        groups.append((wire, n, dp.table_pack(to_dev(Tsh), r0), r0, out))
+        expect.append(oracle.answer_batch(okeys, Tsh, row_begin=r0, threads=8))
+    dp.eval_grouped_packed(groups, D, prf=prf)
+    torch.cuda.synchronize()
+    for g, want in zip(groups, expect):
+        np.testing.assert_array_equal(dp.as_u32(g[4]), want)

@@ -30,6 +30,7 @@ ap.add_argument("--need", type=int, default=3)
 ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--check", type=int, default=2, help="inferences whose rows are reconstructed and checked")
 ap.add_argument("--prf", default="chacha20", choices=["chacha20", "chacha20_et"])
+ap.add_argument("--packed", action="store_true", help="limb-packed tables + tcgen05 (dpf_eval_grouped_packed)")
 a = ap.parse_args()
 prf = dpfpir.DPF_PRF_CHACHA20_ET if a.prf == "chacha20_et" else dpfpir.DPF_PRF_CHACHA20
 D = synth.CODESIGN_D
@@ -40,9 +41,12 @@ for t, lg in enumerate(synth.CODESIGN_LOG2_ROWS):
     T = synth.table(N, D, 0xC5000 + t)
     sp = codesign.HotSplit.from_frequency(synth.codesign_frequency(t, N), a.hot)
     H = sp.hot_table(T)
-    tables.append(dict(N=N, T=T, Td=torch.from_numpy(T.view(np.int32)).cuda(), split=sp, hmap=sp.hot_index(),
-                       Hd=torch.from_numpy(H.view(np.int32)).cuda(), nH=codesign.log2_domain(sp.n_hot),
-                       nF=codesign.log2_domain(N)))
+    Td = torch.from_numpy(T.view(np.int32)).cuda()
+    Hd = torch.from_numpy(H.view(np.int32)).cuda()
+    if a.packed:  # server state, re-laid-out once
+        Td, Hd = dpfpir.table_pack(Td), dpfpir.table_pack(Hd)
+    tables.append(dict(N=N, T=T, Td=Td, split=sp, hmap=sp.hot_index(), Hd=Hd,
+                       nH=codesign.log2_domain(sp.n_hot), nF=codesign.log2_domain(N)))
 torch.cuda.synchronize()
 seed_iter = iter(synth.gen_seeds(200000, 0xC5))
 for Binf in a.batches:
@@ -63,14 +67,20 @@ for Binf in a.batches:
                 gl.append((wire, n, tbl, 0, out))
             real.append((t, kind, plans))
     n_keys = sum(g[0].shape[0] for g in groups0)
-    ws = torch.empty(dpfpir.eval_grouped_workspace_bytes(groups0, D, prf=prf), dtype=torch.uint8, device="cuda")
+    wsb = (dpfpir.eval_grouped_packed_workspace_bytes if a.packed else dpfpir.eval_grouped_workspace_bytes)(
+        groups0, D, prf=prf)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    run_grouped = dpfpir.eval_grouped_packed if a.packed else dpfpir.eval_grouped
 
     def grouped():
-        dpfpir.eval_grouped(groups0, D, prf=prf, workspace=ws)
+        run_grouped(groups0, D, prf=prf, workspace=ws)
 
     def separate():
         for (wire, n, tbl, r0, out) in groups0:
-            dpfpir.eval_batch_wire(wire, n, tbl, r0, out=out, prf=prf)
+            if a.packed:
+                dpfpir.eval_batch_wire_packed(wire, n, tbl, out=out, prf=prf)
+            else:
+                dpfpir.eval_batch_wire(wire, n, tbl, r0, out=out, prf=prf)
 
     res = {}
     for name, fn in (("grouped", grouped), ("separate", separate)):
@@ -87,7 +97,7 @@ for Binf in a.batches:
     # correctness: second server, reconstruct the first inferences' real queries
     grouped()
     plan = dpfpir.last_eval_stats()
-    dpfpir.eval_grouped(groups1, D, prf=prf)
+    run_grouped(groups1, D, prf=prf)
     torch.cuda.synchronize()
     ok = True
     for gi, (t, kind, plans) in enumerate(real):
@@ -103,7 +113,7 @@ for Binf in a.batches:
     blocks = sum(g[0].shape[0] * ((g[2].shape[0] - 1) if prf == dpfpir.DPF_PRF_CHACHA20 else max(1, g[2].shape[0] // 8 - 1))
                  for g in groups0)
     ms = res["grouped"]
-    print(json.dumps({"workload": "c5 co-design", "prf": a.prf, "inferences_per_batch": Binf, "keys_per_batch": n_keys,
+    print(json.dumps({"workload": "c5 co-design", "prf": a.prf, "packed": a.packed, "inferences_per_batch": Binf, "keys_per_batch": n_keys,
                       "q_hot": a.q_hot, "q_full": a.q_full, "hot_fraction": a.hot, "need_per_table": a.need,
                       "dropped_rows": dropped, "ms_grouped": round(ms, 4), "ms_separate": round(res["separate"], 4),
                       "inferences_per_s": round(Binf / (ms * 1e-3), 1), "dpf_queries_per_s": round(n_keys / (ms * 1e-3)),
