@@ -226,3 +226,38 @@ def test_planner_all_schemes_and_paths(lib):
     for prf, per in ((1, (1 << 20) - 1), (ET, (1 << 17) - 1)):
         for packed in (False, True):
             assert dpfpir.eval_plan(256, 20, 1 << 20, 256, prf, 0, packed)["prf_blocks"] == 256 * per
+
+
+def test_new_entry_points_reject_bad_args_without_gpu(lib):
+    """dpf_eval_batch_wire_ex, the IPC helpers and the packed grouped planner
+    validate their arguments before any CUDA call."""
+    L = lib
+    keys = ctypes.create_string_buffer(4096 + 16)
+    kp = (ctypes.addressof(keys) + 15) // 16 * 16
+    ws = ctypes.create_string_buffer(1 << 16)
+    wsp = (ctypes.addressof(ws) + 255) // 256 * 256
+    out = ctypes.create_string_buffer(4096)
+    # unknown flag bits, null keys, misaligned keys
+    assert L.dpf_eval_batch_wire_ex(kp, 1, 8, 1, kp, 0, 0, 16, 4, out, 2, wsp, 60000, None) == dpfpir.DPF_EINVAL
+    assert L.dpf_eval_batch_wire_ex(None, 1, 8, 1, kp, 0, 0, 16, 4, out, 1, wsp, 60000, None) == dpfpir.DPF_EINVAL
+    assert L.dpf_eval_batch_wire_ex(kp + 4, 1, 8, 1, kp, 0, 0, 16, 4, out, 1, wsp, 60000, None) == dpfpir.DPF_EINVAL
+    # unknown scheme
+    assert L.dpf_eval_batch_wire_ex(kp, 1, 8, 9, kp, 0, 0, 16, 4, out, 0, wsp, 60000, None) == dpfpir.DPF_EUNSUPPORTED
+    h = (ctypes.c_uint8 * dpfpir.IPC_HANDLE_BYTES)()
+    off = ctypes.c_uint64()
+    p = ctypes.c_void_p()
+    assert L.dpf_ipc_export(None, h, ctypes.byref(off)) == dpfpir.DPF_EINVAL
+    assert L.dpf_ipc_open(None, ctypes.byref(p)) == dpfpir.DPF_EINVAL
+    assert L.dpf_ipc_close(None) == dpfpir.DPF_EINVAL
+    # grouped planners: an empty group list and a bad D plan nothing
+    assert L.dpf_eval_grouped_workspace_bytes(None, 0, 32, 1) == 0
+    assert L.dpf_eval_grouped_packed_workspace_bytes(None, 0, 32, 1) == 0
+    g = dpfpir.DpfEvalGroup()
+    g.keys_wire, g.B, g.log_n, g.table, g.row_begin, g.row_count, g.shares = kp, 3, 10, kp, 0, 1000, kp
+    arr = (dpfpir.DpfEvalGroup * 1)(g)
+    assert L.dpf_eval_grouped_packed_workspace_bytes(arr, 1, 32, 1) > 0
+    assert L.dpf_eval_grouped_packed_workspace_bytes(arr, 1, 30, 1) == 0   # D % 4
+    assert L.dpf_eval_grouped_packed_workspace_bytes(arr, 1, 32, 3) > 0    # early termination
+    g.log_n = 2                                                             # below the packed minimum depth
+    arr = (dpfpir.DpfEvalGroup * 1)(g)
+    assert L.dpf_eval_grouped_packed_workspace_bytes(arr, 1, 32, 1) == 0

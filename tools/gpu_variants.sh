@@ -1,4 +1,3 @@
 #!/bin/bash
-timeout 600 python -m pytest tests -m gpu -q -x --timeout 300 -k "grouped" 2>&1 | tail -3
-timeout 900 python tools/codesign_bench.py --packed --prf chacha20_et --batches 16 64 256 1024 > gpurun_out/c5_et_packed.jsonl 2>&1; cut -c1-330 gpurun_out/c5_et_packed.jsonl
-timeout 900 python tools/codesign_bench.py --packed --batches 16 64 256 > gpurun_out/c5_packed.jsonl 2>&1; cut -c1-330 gpurun_out/c5_packed.jsonl
+timeout 600 python -m pytest tests -m gpu -q -x --timeout 300 -k "packed or et_ or runs" 2>&1 | tail -2
+for a in "c3" "c3 --prf chacha20_et" "t5 --prf chacha20_et" "t5" "c3 --prf aes128 --steps 5"; do echo "== $a"; bash tools/bench_brief.sh $a --steps 20 | cut -c1-100; done
