@@ -305,9 +305,14 @@ def main():
     e2e_steps = args.e2e_steps or max(3, args.steps // 2)
     host_out = torch.empty((w.B, w.D), dtype=torch.int32).pin_memory()
 
+    # G == 1: the graph-captured serving step (dpf_server_*): host wire keys in,
+    # host answers out, one graph launch per batch
+    server = dpfpir.Server(w.B, w.log_n, Tp if use_packed else T, r0, prf=prf, stream=stream) if G == 1 else None
+    host_out_np = host_out.numpy().view(np.uint32)
+
     def e2e_step():
-        if G == 1 and not use_packed:
-            dpfpir.serve_batch(keys0, T, host_out, r0, workspace=ws, stream=stream)
+        if server is not None:
+            server.run(wire_host, host_out_np)
             return
         if use_packed:
             dpfpir.eval_batch_packed(keys0, Tp, out=out, workspace=ws, stream=stream)
@@ -391,7 +396,7 @@ def main():
                        "l2": "no flush: table shard (%d MiB) >= L2 and the path is ALU-bound" %
                              (rows * w.D * 4 >> 20)},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(wire_host.nbytes),
-                    "d2h_bytes_per_step": w.B * w.D * 4, "api": ("dpf_serve_batch" if G == 1 and not use_packed else
+                    "d2h_bytes_per_step": w.B * w.D * 4, "api": ("dpf_server_run (CUDA-graph serving step)" if G == 1 else
                             "dpf_eval_batch%s + %sD2H" % ("_packed" if use_packed else "_shard",
                                                           "NCCL reduce + " if G > 1 else ""))},
             "gpu_launches": int(stats["kernels"]) * args.steps,

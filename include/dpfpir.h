@@ -174,6 +174,28 @@ int dpf_eval_batch_wire(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n
                         uint64_t row_begin, uint64_t row_count, uint32_t D, uint32_t *partial_shares,
                         void *workspace, size_t workspace_bytes, void *stream);
 
+/* ---- graph-captured serving step (one fixed shape) ----
+ * dpf_server_create captures, on `stream`, one whole serving step for B keys
+ * of (log_n, prf) against a table shard (row-major, or packed = 1 for a
+ * dpf_table_pack'ed one) as a CUDA graph: H2D of the keys from a pinned
+ * staging buffer, zeroing, top BFS, fused kernel, D2H of the B x D answers
+ * into pinned memory.  dpf_server_run copies host wire keys (B records of
+ * dpf_key_wire_size_prf(log_n, prf) bytes; headers checked: DPF_EKEY) into
+ * the staging buffer, replays the graph with ONE launch, waits, and copies
+ * the answers to shares_host.  The caller owns `table` and `workspace`
+ * (DEVICE, >= dpf_server_workspace_bytes, 256-byte aligned) for the server's
+ * lifetime; the library owns the two pinned buffers (freed by destroy).
+ * `stream` is synchronised once at create (the table must be ready); the
+ * server captures and replays on its own stream.  Not thread-safe per server
+ * object. */
+typedef struct dpf_server dpf_server;
+size_t dpf_server_workspace_bytes(uint32_t B, uint32_t log_n, uint32_t prf, uint64_t row_count, uint32_t D);
+int dpf_server_create(uint32_t B, uint32_t log_n, uint32_t prf, const void *table, int packed, uint64_t row_begin,
+                      uint64_t row_count, uint32_t D, void *workspace, size_t workspace_bytes, void *stream,
+                      dpf_server **out);
+int dpf_server_run(dpf_server *server, const uint8_t *keys_wire_host, uint32_t *shares_host);
+void dpf_server_destroy(dpf_server *server);
+
 /* ---- fused cross-GPU reduction (multi-GPU row sharding) ----
  * The G row shards' partial answers sum to the answer (Z_2^32 is a group).
  * Instead of a separate collective, each rank's fused kernel can add its

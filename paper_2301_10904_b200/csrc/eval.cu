@@ -1478,6 +1478,123 @@ extern "C" int dpf_serve_batch(const dpf_key *keys, uint32_t B, const uint32_t *
   return DPF_OK;
 }
 
+// ------------------------------------------------------------ graph server
+// A serving step for one fixed shape captured once as a CUDA graph: pinned
+// key staging -> H2D -> zeroing, top BFS, fused kernel -> D2H of the answers,
+// replayed with ONE cudaGraphLaunch per batch (the per-call launch overhead of
+// the small configurations is host-side; the graph removes it).
+struct dpf_server {
+  uint32_t B, log_n, prf, D, kstride;
+  uint8_t *keys_pinned = nullptr;   // B x kstride (library-owned pinned staging)
+  uint32_t *out_pinned = nullptr;   // B x D
+  cudaStream_t st = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+extern "C" size_t dpf_server_workspace_bytes(uint32_t B, uint32_t log_n, uint32_t prf, uint64_t row_count,
+                                             uint32_t D) {
+  const size_t kstride = dpf_key_wire_size_prf(log_n, prf);
+  const size_t ev = dpf_eval_workspace_bytes(B, log_n, row_count, D);
+  if (kstride == 0 || ev == 0) return 0;
+  return ev + align_up(size_t(B) * kstride, kAlign) + align_up(size_t(B) * D * 4, kAlign);
+}
+
+extern "C" int dpf_server_create(uint32_t B, uint32_t log_n, uint32_t prf, const void *table, int packed,
+                                 uint64_t row_begin, uint64_t row_count, uint32_t D, void *workspace,
+                                 size_t workspace_bytes, void *stream, dpf_server **out) {
+  if (!out || !table || !workspace || B == 0) return DPF_EINVAL;
+  *out = nullptr;
+  const size_t need = dpf_server_workspace_bytes(B, log_n, prf, row_count, D);
+  if (need == 0) return DPF_EINVAL;
+  if (workspace_bytes < need) return DPF_ENOMEM;
+  if (reinterpret_cast<uintptr_t>(workspace) & (kAlign - 1)) return DPF_EINVAL;
+  const size_t ev = dpf_eval_workspace_bytes(B, log_n, row_count, D);
+  dpf_server *sv = new dpf_server;
+  sv->B = B;
+  sv->log_n = log_n;
+  sv->prf = prf;
+  sv->D = D;
+  sv->kstride = uint32_t(dpf_key_wire_size_prf(log_n, prf));
+  // the caller's stream orders the table's preparation; the server captures
+  // and replays on a private stream (the legacy NULL stream cannot be captured)
+  if (cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&sv->st, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    sv->st = nullptr;
+    dpf_server_destroy(sv);
+    return DPF_ECUDA;
+  }
+  uint8_t *ws = static_cast<uint8_t *>(workspace);
+  uint8_t *keys_dev = ws + ev;
+  uint32_t *out_dev = reinterpret_cast<uint32_t *>(keys_dev + align_up(size_t(B) * sv->kstride, kAlign));
+  const size_t kb = size_t(B) * sv->kstride, ob = size_t(B) * D * 4;
+  int rc = DPF_OK;
+  cudaGraph_t graph = nullptr;
+  if (cudaHostAlloc(&sv->keys_pinned, kb, cudaHostAllocDefault) != cudaSuccess ||
+      cudaHostAlloc(&sv->out_pinned, ob, cudaHostAllocDefault) != cudaSuccess) {
+    rc = DPF_ENOMEM;
+  } else {
+    std::memset(sv->keys_pinned, 0, kb);
+    // warm-up launch outside capture: first-use attribute/occupancy queries happen here
+    rc = eval_impl(nullptr, B, keys_dev, log_n, prf, static_cast<const uint32_t *>(table), row_begin, row_count, D,
+                   out_dev, ws, ev, sv->st, packed != 0);
+    if (rc == DPF_OK && cudaStreamSynchronize(sv->st) != cudaSuccess) rc = DPF_ECUDA;
+  }
+  if (rc == DPF_OK) {
+    if (cudaStreamBeginCapture(sv->st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      rc = DPF_ECUDA;
+    } else {
+      int r1 = cudaMemcpyAsync(keys_dev, sv->keys_pinned, kb, cudaMemcpyHostToDevice, sv->st) == cudaSuccess
+                   ? DPF_OK : DPF_ECUDA;
+      if (r1 == DPF_OK)
+        r1 = eval_impl(nullptr, B, keys_dev, log_n, prf, static_cast<const uint32_t *>(table), row_begin, row_count,
+                       D, out_dev, ws, ev, sv->st, packed != 0);
+      if (r1 == DPF_OK && cudaMemcpyAsync(sv->out_pinned, out_dev, ob, cudaMemcpyDeviceToHost, sv->st) != cudaSuccess)
+        r1 = DPF_ECUDA;
+      const cudaError_t e = cudaStreamEndCapture(sv->st, &graph);
+      rc = r1 != DPF_OK ? r1 : (e == cudaSuccess ? DPF_OK : DPF_ECUDA);
+      if (rc == DPF_OK && cudaGraphInstantiate(&sv->exec, graph, 0) != cudaSuccess) rc = DPF_ECUDA;
+    }
+  }
+  if (graph) cudaGraphDestroy(graph);
+  if (rc != DPF_OK) {
+    cudaGetLastError();
+    dpf_server_destroy(sv);
+    return rc;
+  }
+  *out = sv;
+  return DPF_OK;
+}
+
+// Wire-format header checks of a host key (include/dpfpir.h "Wire format").
+static bool wire_header_ok(const uint8_t *k, uint32_t log_n, uint32_t prf) {
+  uint32_t magic;
+  std::memcpy(&magic, k, 4);
+  const uint8_t party = k[6];
+  return magic == DPF_KEY_MAGIC && k[4] == DPF_KEY_VERSION && k[5] == prf && party <= 1 && k[7] == log_n &&
+         (k[16] & 1u) == party;
+}
+
+extern "C" int dpf_server_run(dpf_server *sv, const uint8_t *keys_wire_host, uint32_t *shares_host) {
+  if (!sv || !keys_wire_host || !shares_host) return DPF_EINVAL;
+  for (uint32_t b = 0; b < sv->B; ++b)
+    if (!wire_header_ok(keys_wire_host + size_t(b) * sv->kstride, sv->log_n, sv->prf)) return DPF_EKEY;
+  std::memcpy(sv->keys_pinned, keys_wire_host, size_t(sv->B) * sv->kstride);
+  if (cudaGraphLaunch(sv->exec, sv->st) != cudaSuccess) return DPF_ECUDA;
+  if (cudaStreamSynchronize(sv->st) != cudaSuccess) return DPF_ECUDA;
+  std::memcpy(shares_host, sv->out_pinned, size_t(sv->B) * sv->D * 4);
+  return DPF_OK;
+}
+
+extern "C" void dpf_server_destroy(dpf_server *sv) {
+  if (!sv) return;
+  if (sv->exec) cudaGraphExecDestroy(sv->exec);
+  if (sv->keys_pinned) cudaFreeHost(sv->keys_pinned);
+  if (sv->out_pinned) cudaFreeHost(sv->out_pinned);
+  if (sv->st) cudaStreamDestroy(sv->st);
+  delete sv;
+}
+
 extern "C" int dpf_eval_leaves(const dpf_key *keys, uint32_t B, uint32_t *leaves, void *workspace,
                                size_t workspace_bytes, void *stream) {
   if (!keys || B == 0 || !leaves || !workspace) return DPF_EINVAL;

@@ -89,6 +89,12 @@ def lib() -> ctypes.CDLL:
     L.dpf_ipc_export.argtypes = [vp, vp, ctypes.POINTER(u64)]
     L.dpf_ipc_open.argtypes = [vp, ctypes.POINTER(vp)]
     L.dpf_ipc_close.argtypes = [vp]
+    L.dpf_server_workspace_bytes.argtypes = [u32, u32, u32, u64, u32]
+    L.dpf_server_workspace_bytes.restype = sz
+    L.dpf_server_create.argtypes = [u32, u32, u32, vp, ctypes.c_int, u64, u64, u32, vp, sz, vp, ctypes.POINTER(vp)]
+    L.dpf_server_run.argtypes = [vp, vp, vp]
+    L.dpf_server_destroy.argtypes = [vp]
+    L.dpf_server_destroy.restype = None
     L.dpf_eval_leaves.argtypes = [vp, u32, vp, vp, sz, vp]
     L.dpf_table_packed_bytes.argtypes = [u64, u64, u32]
     L.dpf_table_packed_bytes.restype = sz
@@ -120,6 +126,7 @@ EXPORTED_SYMBOLS = ("dpf_gen", "dpf_key_wire_size", "dpf_key_wire_size_prf", "dp
                     "dpf_eval_grouped_workspace_bytes", "dpf_eval_grouped",
                     "dpf_eval_grouped_packed_workspace_bytes", "dpf_eval_grouped_packed",
                     "dpf_eval_batch_wire_ex", "dpf_ipc_export", "dpf_ipc_open", "dpf_ipc_close",
+                    "dpf_server_workspace_bytes", "dpf_server_create", "dpf_server_run", "dpf_server_destroy",
                     "dpf_kernel_timer_read", "dpf_strerror", "dpf_version")
 
 
@@ -326,6 +333,49 @@ def ipc_open(handle: bytes) -> int:
 
 def ipc_close(ptr: int) -> None:
     _check(lib().dpf_ipc_close(ptr), "dpf_ipc_close")
+
+
+class Server:
+    """dpf_server_*: one serving step of a fixed shape captured as a CUDA graph.
+    run(keys_wire_host uint8 [B, w], out int32 [B, D] host) -> out."""
+
+    def __init__(self, B: int, log_n: int, table, row_begin: int = 0, prf: int = DPF_PRF_CHACHA20, stream=None):
+        import torch
+        packed = isinstance(table, PackedTable)
+        rows, D = (table.row_count, table.D) if packed else table.shape
+        dev = table.data.device if packed else table.device
+        need = lib().dpf_server_workspace_bytes(B, log_n, prf, rows, D)
+        if need == 0:
+            raise DpfError(DPF_EINVAL, "dpf_server_workspace_bytes")
+        self.ws = _workspace(need, dev)
+        self.table = table  # keep alive
+        self.B, self.D, self.wire = B, D, key_wire_size(log_n, prf)
+        h = ctypes.c_void_p()
+        tptr = table.data.data_ptr() if packed else table.data_ptr()
+        _check(lib().dpf_server_create(B, log_n, prf, tptr, int(packed), row_begin, rows, D, self.ws.data_ptr(),
+                                       self.ws.numel() * self.ws.element_size(), _stream_ptr(stream), ctypes.byref(h)),
+               "dpf_server_create")
+        self.h = h
+
+    def run(self, keys_wire_host: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
+        kw = np.ascontiguousarray(keys_wire_host, dtype=np.uint8)
+        if kw.size != self.B * self.wire:
+            raise ValueError("expected %d keys of %d wire bytes" % (self.B, self.wire))
+        if out is None:
+            out = np.empty((self.B, self.D), dtype=np.uint32)
+        _check(lib().dpf_server_run(self.h, kw.ctypes.data, out.ctypes.data), "dpf_server_run")
+        return out
+
+    def close(self):
+        if self.h is not None and self.h.value:
+            lib().dpf_server_destroy(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def eval_batch_wire(keys_wire_dev, log_n: int, table_shard, row_begin: int = 0, out=None, workspace=None,

@@ -526,3 +526,25 @@ def test_grouped_packed_tc(dp, oracle, prf, D):
     torch.cuda.synchronize()
     for g, want in zip(groups, expect):
         np.testing.assert_array_equal(dp.as_u32(g[4]), want)
+
+
+@pytest.mark.parametrize("prf,D,packed", [(1, 64, False), (1, 256, True), (3, 128, True), (2, 64, False), (3, 64, False)])
+def test_graph_server_replays_new_keys(dp, oracle, prf, D, packed):
+    """dpf_server_*: the captured serving graph answers fresh host keys on every
+    replay (H2D of the staging buffer inside the graph) and checks headers."""
+    n, N, B = 12, 3000, 40
+    T = synth.table(N, D, 1200 + D)
+    Td = to_dev(T)
+    srv = dp.Server(B, n, dp.table_pack(Td) if packed else Td, prf=prf)
+    for rep in range(3):
+        al = synth.alphas(B, N, 1300 + rep)
+        keys = [dp.gen(n, int(a), 1, s, prf=prf)[(i + rep) % 2]
+                for i, (a, s) in enumerate(zip(al, synth.gen_seeds(B, 1400 + rep)))]
+        got = srv.run(dp.keys_to_wire(keys))
+        want = oracle.answer_batch([oracle.key_from_wire(dp.key_serialize(k)) for k in keys], T, threads=8)
+        np.testing.assert_array_equal(got, want)
+    bad = dp.keys_to_wire(keys).copy()
+    bad[3, 0] ^= 1  # magic
+    with pytest.raises(dp.DpfError):
+        srv.run(bad)
+    srv.close()
