@@ -145,8 +145,12 @@ constexpr uint32_t kTopSmemLevels = 10;
 template <class Prf>
 __global__ void __launch_bounds__(256) expand_top_split_kernel(const uint8_t *__restrict__ keys, uint32_t kstride,
                                                                uint32_t n, uint32_t s, uint32_t f, uint64_t r0,
-                                                               uint64_t r1, uint4 *__restrict__ out, uint64_t cap) {
+                                                               uint64_t r1, uint4 *__restrict__ out, uint64_t cap,
+                                                               uint4 *__restrict__ zero, uint64_t zero_vec) {
   __shared__ uint4 buf[2][1u << kTopSmemLevels];
+  // a7's zeroing of the answers rides along (saves a launch per step)
+  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < zero_vec; i += uint64_t(gridDim.x) * blockDim.x)
+    zero[i] = make_uint4(0, 0, 0, 0);
   const uint64_t lo_s = r0 >> (n - s), cnt_s = ((r1 - 1) >> (n - s)) - lo_s + 1;
   const uint32_t b = uint32_t(blockIdx.x / cnt_s);
   const uint64_t ps = lo_s + blockIdx.x % cnt_s;  // this CTA's level-s node
@@ -1118,9 +1122,13 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
                 uint32_t flags = 0) {
   uint32_t nk = 0;
   // a7: answers start at zero, unless the caller accumulates (DPF_EVAL_ACCUMULATE:
-  // `out` may be another rank's buffer mapped over NVLink, zeroed by its owner)
-  if (!(flags & DPF_EVAL_ACCUMULATE) && cudaMemsetAsync(out, 0, size_t(B) * D * 4, st) != cudaSuccess)
-    return DPF_ECUDA;
+  // `out` may be another rank's buffer mapped over NVLink, zeroed by its owner).
+  // With a top BFS the zeroing is folded into it (B*D is a multiple of 4 words).
+  const bool zero = !(flags & DPF_EVAL_ACCUMULATE);
+  const bool fold = pl.f >= 1 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+  if (zero && !fold && cudaMemsetAsync(out, 0, size_t(B) * D * 4, st) != cudaSuccess) return DPF_ECUDA;
+  uint4 *zero_ptr = (zero && fold) ? reinterpret_cast<uint4 *>(out) : nullptr;
+  const uint64_t zero_vec = zero_ptr ? uint64_t(B) * D / 4 : 0;
   // a2: levels 1..f; level k lands in front[(f-k)&1] so level f is front[0].
   if (pl.f == 0) {
     dev::copy_roots_kernel<<<(B + 127) / 128, 128, 0, st>>>(keys_dev, kstride, B, ws.front[0], pl.cap);
@@ -1137,10 +1145,10 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
     if (grid > 0x7FFFFFFFull) return DPF_EINVAL;
     if (pl.prf == DPF_PRF_AES128)
       dev::expand_top_split_kernel<dev::PrfAesBs><<<uint32_t(grid), 256, 0, st>>>(
-          keys_dev, kstride, pl.n, s, pl.f, pl.nr0, pl.nr1, ws.front[0], pl.cap);
+          keys_dev, kstride, pl.n, s, pl.f, pl.nr0, pl.nr1, ws.front[0], pl.cap, zero_ptr, zero_vec);
     else
       dev::expand_top_split_kernel<dev::PrfChacha><<<uint32_t(grid), 256, 0, st>>>(
-          keys_dev, kstride, pl.n, s, pl.f, pl.nr0, pl.nr1, ws.front[0], pl.cap);
+          keys_dev, kstride, pl.n, s, pl.f, pl.nr0, pl.nr1, ws.front[0], pl.cap, zero_ptr, zero_vec);
     ++nk;
   }
   const bool timed = g_timer.on && 2 * g_timer.used + 1 < g_timer.ev.size();
