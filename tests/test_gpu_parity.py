@@ -548,3 +548,45 @@ def test_graph_server_replays_new_keys(dp, oracle, prf, D, packed):
     with pytest.raises(dp.DpfError):
         srv.run(bad)
     srv.close()
+
+
+def test_random_shapes_fuzz(dp, oracle):
+    """Seeded random shapes through every entry point family (IMAD and tcgen05
+    incl. pairs and padded D, all three schemes, shards with ragged ends, the
+    accumulate flag): bit-exact against the oracle."""
+    rng = np.random.default_rng(20261017)
+    cases = 0
+    while cases < 120:
+        prf = int(rng.choice([1, 2, 3], p=[0.45, 0.15, 0.4]))
+        n = int(rng.integers(5 if prf == 3 else 3, 15))
+        N = int(rng.integers(max(8, (1 << n) // 3), (1 << n) + 1))
+        D = int(rng.choice([4, 16, 32, 60, 64, 100, 128, 192, 256, 320, 512]))
+        B = int(rng.choice([1, 3, 16, 17, 33, 64, 100, 129, 200]))
+        if prf == 2 and (n > 11 or B > 64):
+            continue  # keep the oracle's AES time bounded
+        r0 = int(rng.integers(0, N // 2 + 1))
+        rows = int(rng.integers(1, N - r0 + 1))
+        packed = bool(rng.integers(0, 2)) and n >= 3
+        seed = int(rng.integers(1 << 30))
+        T = synth.table(N, D, seed)
+        al = synth.alphas(B, N, seed)
+        keys = [dp.gen(n, int(a), 1, s, prf=prf)[i % 2] for i, (a, s) in enumerate(zip(al, synth.gen_seeds(B, seed)))]
+        okeys = [oracle.key_from_wire(dp.key_serialize(k)) for k in keys]
+        Tsh = T[r0:r0 + rows]
+        Td = to_dev(Tsh)
+        want = oracle.answer_batch(okeys, Tsh, row_begin=r0, threads=16)
+        if packed:
+            got = dp.as_u32(dp.eval_batch_packed(keys, dp.table_pack(Td, r0)))
+        else:
+            got = dp.as_u32(dp.eval_batch_shard(keys, Td, r0))
+        assert np.array_equal(got, want), (prf, n, N, D, B, r0, rows, packed)
+        # accumulate twice into one buffer through the wire path: 2x the answer
+        wire = torch.from_numpy(dp.keys_to_wire(keys)).cuda()
+        acc = torch.zeros((B, D), dtype=torch.int32, device="cuda")
+        ws = torch.empty(dp.eval_workspace_bytes(B, n, rows, D), dtype=torch.uint8, device="cuda")
+        for _ in range(2):
+            dp.eval_batch_wire_ex(wire, n, dp.table_pack(Td, r0) if packed else Td, r0, rows, D, acc.data_ptr(),
+                                  dp.DPF_EVAL_ACCUMULATE, ws, prf=prf, packed=packed)
+        torch.cuda.synchronize()
+        assert np.array_equal(dp.as_u32(acc), (2 * want.astype(np.uint64) % (1 << 32)).astype(np.uint32))
+        cases += 1
