@@ -905,7 +905,7 @@ uint32_t max_pairs(size_t smem_bytes) {
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof cfg);
   cfg.gridDim = dim3(2 * r);
-  cfg.blockDim = dim3(32 * (kTcNP + 4 + 1));
+  cfg.blockDim = dim3(32 * (kTcNP + dev::tc_extra_warps(false)));
   cfg.dynamicSmemBytes = smem_bytes;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -914,7 +914,7 @@ uint32_t max_pairs(size_t smem_bytes) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  auto fn = &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, 2, 4, true>;
+  auto fn = &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, 2, 4, true, false>;
   int n = 0;
   int dev_id = 0;
   if (cudaGetDevice(&dev_id) == cudaSuccess &&
@@ -931,14 +931,8 @@ constexpr uint32_t kTcNSY = 2;   // y-ring depth
 // Early termination (R20) fills a y stage with ~2 ChaCha20 blocks per thread
 // instead of ~8, so the MMA side (80 UMMAs per stage) needs more slack: a
 // 3-deep y ring (measured at c3: 0.58 -> 0.61 of the ALU roofline).
-// DPF_TC_NSY=2 restores 2 (tuning).
-inline uint32_t tc_y_stages(bool et) {
-  static const uint32_t v = [] {
-    const char *e = getenv("DPF_TC_NSY");
-    return (e && atoi(e) == 2) ? 2u : 3u;
-  }();
-  return et ? v : kTcNSY;
-}
+constexpr uint32_t kTcNSYEt = 3;
+inline uint32_t tc_y_stages(bool et) { return et ? kTcNSYEt : kTcNSY; }
 // T-ring depth (16 KB entries).  8 entries measured no faster than 4 at
 // D = 512/1024, so the SMEM goes to the DFS stack instead.
 // (6 and 8 entries measured no faster for early termination either.)
@@ -1085,23 +1079,23 @@ int launch_tc_kernel(const Plan &pl, const dev::FusedParams &p, cudaStream_t st)
   tp.debug_nomma = nomma;
   using TcFn = void (*)(const dev::TcParams);
   TcFn fn;
+  // early termination: producers drain TMEM (EPIP, 18 warps, 96 registers)
+  const bool epip = pl.prf == DPF_PRF_CHACHA20_ET;
   if (pl.prf == DPF_PRF_AES128)
-    fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, true>
-                 : &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, false>;
-  else if (pl.prf == DPF_PRF_CHACHA20_ET)
-    fn = pl.pair ? (pl.nsy == 3 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 3, 4, true>
-                                : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, true>)
-                 : (pl.nsy == 3 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 3, 4, false>
-                                : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, false>);
+    fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, true, false>
+                 : &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, false, false>;
+  else if (epip)
+    fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSYEt, 4, true, true>
+                 : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSYEt, 4, false, true>;
   else
-    fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, true>
-                 : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, false>;
+    fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, true, false>
+                 : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, false, false>;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
     return DPF_ECUDA;
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof cfg);
   cfg.gridDim = dim3(pl.grid);
-  cfg.blockDim = dim3(32 * (kTcNP + 4 + 1));
+  cfg.blockDim = dim3(32 * (kTcNP + dev::tc_extra_warps(epip)));
   cfg.dynamicSmemBytes = pl.smem_bytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];

@@ -36,6 +36,16 @@ struct TcParams {
 
 constexpr uint32_t kTcTStageBytes = 16384;  // 32 leaves x 128 columns x 4 limbs
 
+// Who drains TMEM at the end of an accumulator run (template EPIP).
+// false: four dedicated epilogue warps (the MMA warp is one of them);
+// true: the producer warps, idle once their run is produced -- the block
+// shrinks from NP + 5 to NP + 2 warps, so at most 5 warps share an SMSP and
+// the per-thread register cap rises from 80 to 96 (no spills).  Measured:
+// early termination 0.712 -> 0.761 (c3) / 0.763 -> 0.799 (t5) of the ALU
+// roofline; the standard scheme slightly slower (0.905 -> 0.895 at t5), so
+// it keeps the dedicated warps.
+constexpr int tc_extra_warps(bool epip) { return epip ? 2 : 5; }  // MMA (+ epilogue) and loader warps
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -175,9 +185,10 @@ __device__ __forceinline__ void put_leaf16(uint8_t *yb, uint32_t ybplane, uint32
 // peer's MMA warp forwards its y-FULL and T-FULL events to the leader
 // (ypeer / tpeer, remote mbarrier arrives); the leader's commits arrive in
 // both CTAs (multicast); both epilogues release the leader's accempty.
-template <class Prf, int NP, int NSY, int NST, bool PAIR>
-__global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(const TcParams tp) {
-  constexpr int NC = 4;
+template <class Prf, int NP, int NSY, int NST, bool PAIR, bool EPIP>
+__global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eval_tc_kernel(const TcParams tp) {
+  constexpr int NC = EPIP ? 1 : 4;          // MMA/epilogue warps
+  constexpr int NEPI = EPIP ? NP : 4;       // warps that drain TMEM and release accempty
   const FusedParams &p = tp.f;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *tfull = reinterpret_cast<uint64_t *>(smem);  // [NST], count 1 + tx bytes
@@ -200,7 +211,7 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
     }
     for (int s = 0; s < NSY; ++s) mbar_init(&yempty[s], 1);
     mbar_init(accfull, 1);
-    mbar_init(accempty, PAIR ? 2 * NC : NC);
+    mbar_init(accempty, PAIR ? 2 * NEPI : NEPI);
     for (int s = 0; s < NST; ++s) mbar_init(&tpeer[s], 1);
     for (int s = 0; s < NSY; ++s) mbar_init(&ypeer[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -238,6 +249,43 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
   const uint32_t n_dt = PAIR ? Dp / 256 : Dp / 128;  // d-tiles staged by this CTA
   const uint32_t dt0 = rank * n_dt;                   // first of them
 
+  // a6/a7 for one run: TMEM lane quarter `quarter` (= warp % 4: the lanes a
+  // warp may access) holds columns d = 32 quarter + lane of each d-tile;
+  // key chunks h = h0, h0 + hs, ... of 16 keys.  Combine the 4 limb sums,
+  // apply the party sign, red.add into the answers.
+  auto epilogue = [&](uint32_t quarter, uint32_t h0, uint32_t hs, const GroupDesc &g, uint32_t kt) {
+    for (uint32_t dt = 0; dt < n_dt; ++dt) {
+      const uint32_t d = (dt0 + dt) * 128 + quarter * 32 + lane;
+      for (uint32_t h = h0; h < Ktp / 16; h += hs) {
+        uint32_t v[16], x[16], z[16];
+        const uint32_t taddr = tmem_base + ((quarter * 32u) << 16) + dt * 4 * Ktp + h * 16;
+        tmem_ld16(taddr, v);
+        tmem_ld16(taddr + Ktp, x);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] += x[j] << 8;
+        tmem_ld16(taddr + 2 * Ktp, x);
+        tmem_ld16(taddr + 3 * Ktp, z);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const uint32_t bkey = kt * Ktp + h * 16 + j;
+          if (bkey < g.B && d < D) {
+            const uint32_t val = v[j] + (x[j] << 16) + (z[j] << 24);  // A0 + 2^8 A1 + 2^16 A2 + 2^24 A3
+            const uint32_t neg = key_party(g.keys + uint64_t(bkey) * g.kstride);
+            red_add_u32(g.shares + uint64_t(bkey) * D + d, neg ? 0u - val : val);
+          }
+        }
+      }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      if (PAIR && rank != 0) mbar_arrive_leader(accempty);
+      else mbar_arrive(accempty);
+    }
+  };
+
   if (warp < NP) {
     // ------------------------------------------------------------ producers
     // Depth-first over the depth-m subtree: descend to the leaf-parent level
@@ -247,7 +295,7 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
     // single-site "one block per iteration" loop and a 4-leaf "quad" form.)
     const uint32_t tix = warp * 32 + lane;
     const uint32_t kl = tix % p.Kt, nl = tix / p.Kt;
-    uint32_t wseq = 0;
+    uint32_t wseq = 0, pnf = 0;  // pnf: runs drained (producer epilogue)
     for (uint32_t item = first; item < p.n_items; item += stride) {
       const GroupDesc g = group_of(p, item);
       const uint32_t li = item - g.item_base;
@@ -340,6 +388,14 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
         named_arrive(1 + ys, 32 * (NP + 1));  // the MMA warp sleeps in bar.sync until all producers arrive
       }
       }  // !kEt
+      if constexpr (EPIP) {
+        if (!run_continues(p, g, kt, item + stride)) {  // run complete: drain TMEM
+          mbar_wait(accfull, pnf & 1);
+          ++pnf;
+          tc_fence_after();
+          epilogue(warp & 3, warp >> 2, NP / 4, g, kt);
+        }
+      }
     }
   } else if (warp < NP + NC) {
     // ------------------------------------------------ MMA issuer + epilogue
@@ -424,41 +480,16 @@ __global__ void __launch_bounds__(32 * (NP + 4 + 1), 1) fused_eval_tc_kernel(con
       }
       fresh = last;
       if (!last) continue;
-      // epilogue: all NC warps, TMEM lanes 32q..32q+31 = columns d.  Only the
-      // MMA warp polls the commit barrier; the others sleep in bar.sync.
-      if (q == 0) mbar_wait(accfull, nf & 1);
-      ++nf;
-      named_sync(NSY + 1, 32 * NC);
-      tc_fence_after();
-      for (uint32_t dt = 0; dt < n_dt; ++dt) {
-        const uint32_t d = (dt0 + dt) * 128 + q * 32 + lane;
-        for (uint32_t h = 0; h < Ktp / 16; ++h) {
-          uint32_t v[16], x[16], z[16];
-          const uint32_t taddr = tmem_base + ((q * 32u) << 16) + dt * 4 * Ktp + h * 16;
-          tmem_ld16(taddr, v);
-          tmem_ld16(taddr + Ktp, x);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] += x[j] << 8;
-          tmem_ld16(taddr + 2 * Ktp, x);
-          tmem_ld16(taddr + 3 * Ktp, z);
-          tmem_wait_ld();
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const uint32_t bkey = kt * Ktp + h * 16 + j;
-            if (bkey < g.B && d < D) {
-              const uint32_t val = v[j] + (x[j] << 16) + (z[j] << 24);  // A0 + 2^8 A1 + 2^16 A2 + 2^24 A3
-              const uint32_t neg = key_party(g.keys + uint64_t(bkey) * g.kstride);
-              red_add_u32(g.shares + uint64_t(bkey) * D + d, neg ? 0u - val : val);
-            }
-          }
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if (PAIR && rank != 0) mbar_arrive_leader(accempty);
-        else mbar_arrive(accempty);
+      if constexpr (EPIP) {
+        ++nf;  // the producers drain TMEM and release accempty
+      } else {
+        // epilogue: all NC warps, TMEM lanes 32q..32q+31 = columns d.  Only the
+        // MMA warp polls the commit barrier; the others sleep in bar.sync.
+        if (q == 0) mbar_wait(accfull, nf & 1);
+        ++nf;
+        named_sync(NSY + 1, 32 * NC);
+        tc_fence_after();
+        epilogue(q, 0, 1, g, kt);
       }
     }
   } else {
