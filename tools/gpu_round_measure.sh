@@ -21,3 +21,14 @@ for a in "c3 chacha20" "c3 chacha20_et" "t5 chacha20_et"; do set -- $a
   python tools/sass_hot.py /tmp/prof_$1_$2.ncu-rep 25 >> gpurun_out/ncu_$1_$2.txt 2>&1
 done
 ls -la gpurun_out
+timeout 900 python tools/codesign_bench.py > gpurun_out/c5.jsonl 2>&1
+timeout 900 python tools/codesign_bench.py --prf chacha20_et > gpurun_out/c5_et.jsonl 2>&1
+timeout 900 python tools/codesign_bench.py --packed --prf chacha20_et --batches 16 64 256 1024 > gpurun_out/c5_et_packed.jsonl 2>&1
+timeout 600 python tools/batch_sweep.py > gpurun_out/batch_sweep_c3.jsonl 2>&1
+timeout 600 python tools/batch_sweep.py --log-n 22 --D 64 > gpurun_out/batch_sweep_22x64.jsonl 2>&1
+timeout 600 python tools/batch_sweep.py --prf chacha20_et > gpurun_out/batch_sweep_c3_et.jsonl 2>&1
+timeout 600 python tools/shard_sim.py --config c3 > gpurun_out/shard_sim.jsonl 2>&1
+timeout 600 python tools/shard_sim.py --config c3 --prf chacha20_et >> gpurun_out/shard_sim.jsonl 2>&1
+timeout 900 python tools/shard_sim.py --config c4 --steps 3 >> gpurun_out/shard_sim.jsonl 2>&1
+timeout 600 python tools/shard_sim.py --config c4 --prf chacha20_et --steps 5 >> gpurun_out/shard_sim.jsonl 2>&1
+ls -la gpurun_out
