@@ -736,18 +736,25 @@ const std::vector<KernelChoice> &tiles() {
 // Producer warps of the IMAD kernel: 16 (4 per SMSP, measured best) when the
 // consumer accumulators are small enough to share the register file
 // (Kt*D <= 4096 words per CTA), else 8.  DPF_NP=8|16 overrides (tuning).
-int producer_warps(uint32_t Kt, uint32_t D) {
+int producer_warps(uint32_t Kt, uint32_t D, bool et) {
   static int forced = [] {
     const char *e = getenv("DPF_NP");
     const int v = e ? atoi(e) : 0;
     return (v == 8 || v == 16) ? v : 0;
   }();
   if (forced) return forced;
-  return Kt * D <= 4096 ? 16 : 8;
+  // 8 producers when the contraction is heavy next to the PRF (consumers need
+  // the issue slots: D >= 256, or early termination's 8x cheaper tree) or the
+  // batch streams the table (Kt <= 2: smaller windows keep the T ring ahead).
+  // Measured (batch_sweep / codesign_bench): 2^20 x 256 B = 8: 0.598 -> 0.493
+  // ms; 2^22 x 64 B = 1: 0.406 -> 0.374 ms; c5 ET batch 16: 2.84 -> 2.64 ms;
+  // but 2^22 x 64 B = 4 and c5 batch 4/16 are faster with 16.
+  if (Kt * D > 4096 || D >= 256 || et || Kt <= 2) return 8;
+  return 16;
 }
 
-bool pick_kernel(uint32_t Kt, uint32_t D, Plan &pl) {
-  const int NP = producer_warps(Kt, D);
+bool pick_kernel(uint32_t Kt, uint32_t D, Plan &pl, bool et) {
+  const int NP = producer_warps(Kt, D, et);
   const std::vector<KernelChoice> &ts = NP == 16 ? tiles<16>() : tiles<8>();
   uint64_t best = ~0ull;
   for (const KernelChoice &kc : ts) {
@@ -853,7 +860,7 @@ int make_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D
   // Key tile: lanes <-> keys (Kt <= 32), remaining lanes <-> frontier nodes.
   pl.Kt = std::min<uint32_t>(32, pow2ceil(B));
   while (pl.Kt * D > 8192 && pl.Kt > 1) pl.Kt >>= 1;  // accumulator budget: Kt*D <= 8192 words/CTA
-  if (!pick_kernel(pl.Kt, D, pl)) return DPF_EINVAL;
+  if (!pick_kernel(pl.Kt, D, pl, et)) return DPF_EINVAL;
   const uint32_t NP = uint32_t(pl.kc.NP);
   pl.Ft = 32 * NP / pl.Kt;
   // one T-ring entry must hold at least one node's 2-row segment
