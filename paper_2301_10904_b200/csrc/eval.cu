@@ -901,6 +901,9 @@ int make_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D
 }
 
 constexpr uint32_t kTcNP = 16;   // producer warps (4 per SMSP)
+// y-ring depth: 3 stages (with CTA pairs and N = 128 the SMEM fits them
+// beside a full DFS stack; measured t5 0.906 -> 0.916, c3 0.894 -> 0.896).
+constexpr uint32_t kTcNSY = 3;
 
 // How many 2-CTA clusters of the tcgen05 kernel fit on the device at once
 // (cudaOccupancyMaxActiveClusters; num_sms/2 without a device).
@@ -921,7 +924,7 @@ uint32_t max_pairs(size_t smem_bytes) {
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  auto fn = &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, 2, 4, true, false>;
+  auto fn = &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, true, false>;
   int n = 0;
   int dev_id = 0;
   if (cudaGetDevice(&dev_id) == cudaSuccess &&
@@ -934,7 +937,6 @@ uint32_t max_pairs(size_t smem_bytes) {
   cached_smem = smem_bytes;
   return r;
 }
-constexpr uint32_t kTcNSY = 2;   // y-ring depth
 // Early termination (R20) fills a y stage with ~2 ChaCha20 blocks per thread
 // instead of ~8, so the MMA side (80 UMMAs per stage) needs more slack: a
 // 3-deep y ring (measured at c3: 0.58 -> 0.61 of the ALU roofline).
