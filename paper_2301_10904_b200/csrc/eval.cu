@@ -942,6 +942,13 @@ uint32_t max_pairs(size_t smem_bytes) {
 // 3-deep y ring (measured at c3: 0.58 -> 0.61 of the ALU roofline).
 constexpr uint32_t kTcNSYEt = 3;
 inline uint32_t tc_y_stages(bool et) { return et ? kTcNSYEt : kTcNSY; }
+// smallest subtree depth holding one window: 2^(m-1) >= W leaf pairs, or
+// 2^m >= W final nodes with early termination
+inline uint32_t tc_m_min(bool et, uint32_t W) {
+  uint32_t m = 1;
+  while ((et ? (1u << m) : (1u << (m - 1))) < W) ++m;
+  return et ? m : std::max(m, 3u);
+}
 // T-ring depth (16 KB entries).  8 entries measured no faster than 4 at
 // D = 512/1024, so the SMEM goes to the DFS stack instead.
 // (6 and 8 entries measured no faster for early termination either.)
@@ -951,7 +958,29 @@ inline uint32_t tc_t_stages(uint32_t) { return 4u; }
 // Kt = MMA N = 64/32/16 keys so that 4 limb accumulators x D/128 tiles x Kt
 // columns fit the 512 TMEM columns; Ft = 512/Kt frontier nodes per item;
 // W = 4 leaf pairs per node per window (one 8-row packed block).
+int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et,
+                   uint32_t W);
+
+// W (leaf pairs per node per window, standard scheme): 8 when the problem is
+// deep enough for subtrees of >= 4 levels (m >= 4 under W = 4), else 4 --
+// half the y-ring handshakes per block (measured c3 0.896 -> 0.912, t5 0.914
+// -> 0.925).  Early termination: one final node per window.
 int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et = false) {
+  if (et) return make_tc_plan_w(B, log_n, r0, rows, D, pl, true, 1);
+  int rc = make_tc_plan_w(B, log_n, r0, rows, D, pl, false, 4);
+  if (rc != DPF_OK || pl.m < 4) return rc;
+  static const bool allow8 = [] {  // DPF_TC_W=4 pins the 4-leaf-pair window (tuning)
+    const char *e = getenv("DPF_TC_W");
+    return !(e && atoi(e) == 4);
+  }();
+  if (!allow8) return rc;
+  Plan p8;
+  if (make_tc_plan_w(B, log_n, r0, rows, D, p8, false, 8) == DPF_OK) pl = p8;
+  return DPF_OK;
+}
+
+int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et,
+                   uint32_t W) {
   std::memset(&pl, 0, sizeof pl);
   if (D == 0 || D % 4 || D > 1024 || log_n < 3) return DPF_EINVAL;
   pl.tc = true;
@@ -982,9 +1011,8 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
   pl.Ft = 32 * kTcNP / pl.Kt;
   pl.tasks = Ktp * pl.Ft;  // per item (both CTAs of a pair)
   pl.n_ktiles = (B + Ktp - 1) / Ktp;
-  // W units per node per window: 4 leaf pairs (one 8-row packed block), or
+  // W units per node per window: W leaf pairs (W/4 8-row packed blocks), or
   // one final node (16 rows) with early termination.
-  const uint32_t W = et ? 1 : 4;
   pl.R = unit_rows(pl) * W;
   const uint32_t Kw = pl.Ft * pl.R;
   pl.y_stage_bytes = 4 * pl.Kt * Kw;
@@ -992,7 +1020,7 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
   pl.nst = tc_t_stages(D);
   const size_t fixed = 1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(pl.nsy) * pl.y_stage_bytes;
   const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / (32 * kTcNP * 16)));
-  const uint32_t m_min = et ? 1 : 3;
+  const uint32_t m_min = tc_m_min(et, W);  // a subtree holds >= one window
   if (m_cap < m_min || n < m_min) return DPF_EINVAL;
   // co-resident CTA pairs: a GPC with an odd SM count leaves an SM unpaired
   const uint32_t workers = pl.pair ? max_pairs(fixed + size_t(m_cap) * 32 * kTcNP * 16) : uint32_t(num_sms());
@@ -1010,6 +1038,7 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
   pl.n_items = uint32_t(items);
   pl.W = W;
   pl.nwin = (et ? (1u << pl.m) : (1u << (pl.m - 1))) / W;
+  if (pl.nwin == 0) return DPF_EINVAL;
   const uint32_t cols = n_dt_cta * 4 * Ktp;
   pl.tmem_cols = 32;
   while (pl.tmem_cols < cols) pl.tmem_cols <<= 1;
@@ -1830,10 +1859,10 @@ int make_grouped_tc_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint3
   if (prf != DPF_PRF_CHACHA20 && prf != DPF_PRF_AES128 && prf != DPF_PRF_CHACHA20_ET) return DPF_EUNSUPPORTED;
   const bool et = prf == DPF_PRF_CHACHA20_ET;
   const uint32_t v = et ? DPF_ET_BITS : 0u;
-  const uint32_t m_min = et ? 1 : 3;
+  const uint32_t m_min0 = et ? 1 : 3;
   for (uint32_t i = 0; i < G; ++i) {
     const dpf_eval_group &g = gs[i];
-    if (!g.keys_wire || !g.table || !g.shares || g.B == 0 || g.log_n < m_min + v || g.log_n > DPF_MAX_LOG_N ||
+    if (!g.keys_wire || !g.table || !g.shares || g.B == 0 || g.log_n < m_min0 + v || g.log_n > DPF_MAX_LOG_N ||
         g.row_count == 0)
       return DPF_EINVAL;
     const uint64_t dom = 1ull << g.log_n;
@@ -1856,9 +1885,11 @@ int make_grouped_tc_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint3
     }
   }
   Plan &pl = gp.cfg;
-  int rc = make_tc_plan(best, 20, 0, 1u << 20, D, pl, et);
+  // the shared window: W = 4 leaf pairs (tiny groups need shallow subtrees)
+  int rc = make_tc_plan_w(best, 20, 0, 1u << 20, D, pl, et, et ? 1 : 4);
   if (rc) return rc;
   pl.prf = prf;
+  const uint32_t m_min = tc_m_min(et, pl.W);
   const uint32_t Ktp = pl.pair ? 2 * pl.Kt : pl.Kt;
   const size_t fixed = 1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(pl.nsy) * pl.y_stage_bytes;
   const size_t level_bytes = size_t(32) * kTcNP * 16;
