@@ -1,5 +1,10 @@
 #!/bin/bash
-timeout 900 python -m pytest tests -m gpu -q -x --timeout 120 2>&1 | tail -4
-timeout 200 python __graft_entry__.py smoke 2>&1 | tail -1
-for a in c3 t5 c2 "c4 --steps 3" "c3 --prf aes128 --steps 5" "c3 --prf chacha20_et"; do echo "== $a"; timeout 300 bash tools/bench_brief.sh $a --steps 20 2>&1 | cut -c1-90; done
-timeout 600 python tools/codesign_bench.py --packed --prf chacha20_et --batches 64 2>&1 | cut -c150-300
+: > gpurun_out/sanitizer.txt
+python tools/sanitize_run.py >> gpurun_out/sanitizer.txt 2>&1
+for t in memcheck racecheck synccheck initcheck; do
+  echo "== $t" >> gpurun_out/sanitizer.txt
+  timeout 900 compute-sanitizer --tool $t python tools/sanitize_run.py 2>&1 | tail -3 >> gpurun_out/sanitizer.txt
+done
+echo "== racecheck detail" >> gpurun_out/sanitizer.txt
+timeout 900 compute-sanitizer --tool racecheck --racecheck-report hazard --print-limit 2 python tools/sanitize_run.py 2>&1 | grep -v "Host Frame\|Saved host" | grep "Error\|Thread\|SUMMARY" | head -12 >> gpurun_out/sanitizer.txt
+cat gpurun_out/sanitizer.txt
