@@ -1,10 +1,3 @@
 #!/bin/bash
-: > gpurun_out/sanitizer.txt
-python tools/sanitize_run.py >> gpurun_out/sanitizer.txt 2>&1
-for t in memcheck racecheck synccheck initcheck; do
-  echo "== $t" >> gpurun_out/sanitizer.txt
-  timeout 900 compute-sanitizer --tool $t python tools/sanitize_run.py 2>&1 | tail -3 >> gpurun_out/sanitizer.txt
-done
-echo "== racecheck detail" >> gpurun_out/sanitizer.txt
-timeout 900 compute-sanitizer --tool racecheck --racecheck-report hazard --print-limit 2 python tools/sanitize_run.py 2>&1 | grep -v "Host Frame\|Saved host" | grep "Error\|Thread\|SUMMARY" | head -12 >> gpurun_out/sanitizer.txt
-cat gpurun_out/sanitizer.txt
+DPF_ET_W=2 timeout 600 python -m pytest tests -m gpu -q -x --timeout 120 -k "et_ or fuzz or grouped" 2>&1 | tail -2
+for v in "" "DPF_ET_W=2" "" "DPF_ET_W=2"; do for a in "c3 --prf chacha20_et" "t5 --prf chacha20_et"; do echo "== $v $a"; env $v timeout 300 bash tools/bench_brief.sh $a --steps 30 2>&1 | cut -c1-90; done; done
