@@ -590,3 +590,19 @@ def test_random_shapes_fuzz(dp, oracle):
         torch.cuda.synchronize()
         assert np.array_equal(dp.as_u32(acc), (2 * want.astype(np.uint64) % (1 << 32)).astype(np.uint32))
         cases += 1
+
+
+@pytest.mark.parametrize("n,N,r0,rows,D,B", [
+    (17, 1 << 17, 0, 1 << 17, 256, 130), (18, 250001, 7, 200000, 64, 64), (17, 100000, 4096, 60001, 512, 40),
+    (16, 1 << 16, 3, 65000, 128, 300),
+])
+def test_packed_deep_windows_shards(dp, oracle, n, N, r0, rows, D, B):
+    """Deep subtrees (8 leaf pairs per window, CTA pairs at D = 256/512) on
+    ragged shards: bit-exact against the oracle."""
+    T = synth.table(N, D, 7700 + n)
+    al = synth.alphas(B, N, 7700 + n)
+    keys, okeys = make_keys(dp, oracle, n, al, 7800 + n)
+    Tsh = T[r0:r0 + rows]
+    Td = to_dev(Tsh)
+    got = dp.as_u32(dp.eval_batch_packed(keys, dp.table_pack(Td, r0)))
+    np.testing.assert_array_equal(got, oracle.answer_batch(okeys, Tsh, row_begin=r0, threads=16))
