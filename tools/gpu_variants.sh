@@ -1,3 +1,12 @@
 #!/bin/bash
-DPF_ET_W=2 timeout 600 python -m pytest tests -m gpu -q -x --timeout 120 -k "et_ or fuzz or grouped" 2>&1 | tail -2
-for v in "" "DPF_ET_W=2" "" "DPF_ET_W=2"; do for a in "c3 --prf chacha20_et" "t5 --prf chacha20_et"; do echo "== $v $a"; env $v timeout 300 bash tools/bench_brief.sh $a --steps 30 2>&1 | cut -c1-90; done; done
+# Scratch A/B driver for tuning passes on the GPU box (gpurun): edit the
+# variant list, run, compare the one-line summaries of tools/bench_brief.sh.
+# Tuning switches read by libdpfpir (all default off): DPF_NP=8|16,
+# DPF_FORCE_M=<m>, DPF_GRID_ALIGN=0|1, DPF_TC_PAIR=0, DPF_TC_W=4,
+# DPF_LOADER_SPIN=1, DPF_DEBUG_NOMMA=1 (skips the MMAs: wrong answers).
+for v in "" "DPF_TC_W=4"; do
+  for a in c3 t5 "c3 --prf chacha20_et"; do
+    echo "== $v $a"
+    env $v timeout 300 bash tools/bench_brief.sh $a --steps 20 2>&1 | cut -c1-100
+  done
+done
