@@ -5,6 +5,10 @@
     python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
         --master-port P bench.py --gpus N ...
 
+`python bench.py --gpus N` with N > 1 and no WORLD_SIZE in the environment
+re-launches itself under torch.distributed.run with N ranks (one per GPU);
+under torchrun WORLD_SIZE must equal --gpus.
+
 A step = one server's answer to one batch of B DPF keys (BASELINE config c3 by
 default: 2^20 x 256 int32 table, B = 256): a1 key ingest, a2 top BFS, a3-a6
 the fused expansion x table kernel, a7 the B x D answer; for N > 1 the table is
@@ -12,21 +16,31 @@ row-sharded (rank r owns rows [r N/G, (r+1) N/G)) and the partial answers are
 summed mod 2^32 by one NCCL reduce to rank 0 -- strong scaling,
 the total work per step is fixed.
 
-`value`: keys already in HBM (dpf_eval_batch_wire), timed with CUDA events
-over exactly K steps between barriers, max over ranks.  `e2e`: the same through
-the host-buffer API (host keys -> pinned staging -> H2D, answer D2H to pinned
-host memory every step).  `roofline`: the fused kernel's live per-launch CUDA
-event time against the ALU-pipe peak.  `cpu_baseline`:
-the CPU oracle (oracle/, test infrastructure) on a bounded sample of the same
-keys, which also re-checks bit-exact parity before the line is printed.
-`--impl reference`: the oracle alone (the paper has no public GPU code), on the
-host cores, same metric and config.
+`value`: keys already in HBM (dpf_eval_batch_wire*), timed with CUDA events
+over exactly K steps between barriers, max over ranks; per-step events give
+p10/p50/p90.  `e2e`: the same through the host-buffer API (host keys ->
+pinned staging -> H2D, answer D2H to pinned host memory every step).
+`roofline`: the fused kernel's live per-launch CUDA-event time against the
+binding resource (ALU pipe, tensor pipe or HBM).
+`cpu_baseline`: the CPU oracle (oracle/, test infrastructure) on a bounded
+sample of the same keys.
+
+Parity gates the line: every query must reconstruct T[alpha], a sample of the
+device answers must equal the oracle bit-exactly (N > 1: the reduced answers
+against the oracle on the whole table, plus an all-0xFFFFFFFF-table case
+whose partial answers wrap int32), and the e2e answers must equal the
+device-path ones.  Any miss prints the diagnostics to stderr and exits 3
+without a JSON line on stdout.
+
+`--impl reference`: the oracle alone (the paper has no public GPU code) on
+the host cores: keys from the oracle's own Gen, same metric and config.
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -40,33 +54,126 @@ sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
 
-# ALU-pipe ops per tree node: ChaCha20 = 320 XOR + 320
-# rotate per block (80 quarter rounds; the adds run on the FMA pipe).  AES-128
-# (bitsliced, table-free) = the compiled ALU instructions of one node's two
-# encryptions + key schedule in this formulation (9 x 411 + 336 + 40 setup;
-# Boyar-Peralta S-box = 95 LOP3): a better circuit would lower it.
-ALU_OPS_PER_BLOCK = {"chacha20": 640, "aes128": 4075, "chacha20_et": 640}
+# ALU-pipe ops per PRF unit.  ChaCha20 = 320 XOR + 320
+# rotate per block (80 quarter rounds; the adds run on the FMA pipe).  AES-128:
+# the circuit count of one tree node (two encryptions sharing one key
+# schedule), derived in DESIGN.md §7 from the gate counts of the published
+# circuits, independent of this implementation's instruction stream.
+ALU_OPS_PER_BLOCK = {"chacha20": 640, "chacha20_et": 640}
 # leaf rows per tree leaf: early termination (R20) ends the tree at final
 # nodes of 16 rows, each converted by one more ChaCha20 block (counter 1).
 ET_BITS = {"chacha20": 0, "aes128": 0, "chacha20_et": 4}
+PRFS = ("chacha20", "aes128", "chacha20_et")
+L2_BYTES = 126 * 1024 * 1024
+# Parity-failure hook for the bench contract test (flips one answer word
+# before the checks): never set in a measurement.
+INJECT_ENV = "DPF_BENCH_INJECT_MISMATCH"
+
+METRIC = "DPF-PIR queries/sec"
+UNIT = "queries/s"
+
+
+def aes_alu_ops_per_node() -> float:
+    """Circuit count of one AES-128 tree node (R8/R9: the two blocks 0^120||0
+    and 0^120||1 encrypted under the node seed, one shared key schedule),
+    independent of this implementation: 2-input bit gates of
+    the smallest published circuits, divided by 32 (one 32-bit ALU op applies
+    a gate to 32 bit-slices):
+      SubBytes    10 rounds x 32 S-boxes (16 bytes x 2 blocks) x 113 gates
+                  (Boyar-Matthews-Peralta 2013: 32 AND + 81 XOR/XNOR)
+      MixColumns  9 rounds x 8 columns (4 x 2 blocks) x 92 XOR (Maximov 2019)
+      AddRoundKey 11 x 256 XOR (128 bits x 2 blocks)
+      KeyExpand   10 rounds x (4 S-boxes x 113 + 128 XOR) + popcount(Rcon) XOR
+    ShiftRows and RotWord are wiring (free in a circuit)."""
+    rcon = (0x01, 0x02, 0x04, 0x08, 0x10, 0x20, 0x40, 0x80, 0x1B, 0x36)
+    sbox = 113
+    gates = (10 * 32 * sbox + 9 * 8 * 92 + 11 * 256 + 10 * (4 * sbox + 128) + sum(bin(r).count("1") for r in rcon))
+    return gates / 32.0
+
+
+ALU_OPS_PER_BLOCK["aes128"] = aes_alu_ops_per_node()
 
 
 def prf_code(dpfpir, name):
     return {"chacha20": dpfpir.DPF_PRF_CHACHA20, "aes128": dpfpir.DPF_PRF_AES128,
             "chacha20_et": dpfpir.DPF_PRF_CHACHA20_ET}[name]
-METRIC = "DPF-PIR queries/sec"
-UNIT = "queries/s"
 
 
 def peaks():
-    p = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
+    p = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
         with open(path) as f:
             m = json.load(f)
-        p.update(hbm_gbs=float(m.get("hbm_gbs", p["hbm_gbs"])), sm_max_mhz=float(m.get("sm_max_mhz", 1965.0)),
-                 source="measured (MEASURED_PEAKS.json)")
+        p.update(hbm_gbs=float(m.get("hbm_gbs", p["hbm_gbs"])), bf16_tflops=float(m.get("bf16_tflops", 1590.0)),
+                 sm_max_mhz=float(m.get("sm_max_mhz", 1965.0)), source="measured (MEASURED_PEAKS.json)")
     return p
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_threads():
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count() or 1
+    return max(1, min(n, 64))
+
+
+def workload_config(w, prf: str, gpus: int) -> dict:
+    """The workload both arms run (identical dicts: the driver compares them)."""
+    rows = w.N // gpus
+    return {"workload": w.name + ": " + w.note, "log_n": w.log_n, "N": w.N, "D": w.D, "B": w.B, "prf": prf,
+            "parallelism": "1 GPU" if gpus == 1 else "row-shard x%d, answers summed mod 2^32 at rank 0" % gpus,
+            "l2": ("no flush: the table shard (%d MiB) exceeds L2 (126 MiB) and the path is ALU-bound" %
+                   (rows * w.D * 4 >> 20)) if rows * w.D * 4 > L2_BYTES else
+                  "L2 flushed between timed steps (256 MiB write; table shard %d MiB < L2)" % (rows * w.D * 4 >> 20)}
+
+
+def percentiles(xs):
+    a = np.asarray(xs, np.float64)
+    return {"p10": float(np.percentile(a, 10)), "p50": float(np.percentile(a, 50)),
+            "p90": float(np.percentile(a, 90))}
+
+
+def parity_ok(parity: dict) -> bool:
+    """Every boolean flag must hold (and there must be at least one)."""
+    flags = [v for v in parity.values() if isinstance(v, bool)]
+    return bool(flags) and all(flags)
+
+
+def emit(line: dict, parity: dict) -> int:
+    """Print the JSON line only when parity holds; otherwise stderr + rc 3."""
+    if not parity_ok(parity):
+        sys.stderr.write("bench.py: PARITY FAILURE, no result line: %s\n" % json.dumps(parity))
+        sys.stderr.write(json.dumps(line) + "\n")
+        return 3
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def free_port() -> int:
+    s = socket.socket(socket.AF_INET, socket.SOCK_STREAM)
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def spawn(n: int, argv) -> int:
+    """Re-launch this script with n ranks under torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__), *argv]
+    return subprocess.call(cmd)
 
 
 class ClockSampler:
@@ -120,52 +227,43 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def make_keys(w, dpfpir, prf=1):
-    """B client queries of config w: party-0 keys go to this server (the
-    second server is an identical, independent machine)."""
-    al = synth.alphas(w.B, w.N, w.seed)
-    seeds = synth.gen_seeds(w.B, w.seed)
-    pairs = [dpfpir.gen(w.log_n, int(a), 1, s, prf=prf) for a, s in zip(al, seeds)]
-    return al, pairs
-
-
-def oracle_sample(w, keys_wire, T, threads, sample):
-    """CPU oracle on `sample` keys with `threads` POSIX threads; returns
-    (shares, seconds)."""
+def oracle_answers(okeys, T, threads):
+    """CPU oracle answers for oracle keys with `threads` POSIX threads;
+    returns (shares, seconds)."""
     from oracle import oracle as orc
     orc.build()
-    okeys = [orc.key_from_wire(bytes(keys_wire[i])) for i in range(sample)]
     t0 = time.perf_counter()
     sh = orc.answer_batch(okeys, T, threads=threads)
     return sh, time.perf_counter() - t0
 
 
-def cpu_threads():
-    try:
-        n = len(os.sched_getaffinity(0))
-    except AttributeError:
-        n = os.cpu_count() or 1
-    return max(1, min(n, 64))
+def oracle_keys_from_wire(wire_rows):
+    from oracle import oracle as orc
+    orc.build()
+    return [orc.key_from_wire(bytes(r)) for r in wire_rows]
 
 
 # ---------------------------------------------------------------------- reference arm
 
-def run_reference(args, rank, world):
+def run_reference(args, rank):
+    """The oracle alone on the host cores (the paper publishes no code): keys
+    from the oracle's Gen with the same seeds as the GPU arm (byte-identical
+    keys, tests/test_abi.py), full table, bounded per-step sample."""
     if rank != 0:
         return 0
+    from oracle import oracle as orc
+    orc.build()
     w = synth.CONFIGS[args.config]
-    from paper_2301_10904_b200 import build as pbuild
-    from paper_2301_10904_b200 import dpfpir
-    pbuild.build()  # host-side Gen only (client work, outside the timed region)
-    prf = prf_code(dpfpir, args.prf)
-    _, pairs = make_keys(w, dpfpir, prf)
-    wire = dpfpir.keys_to_wire([p[0] for p in pairs])
+    code = {"chacha20": orc.PRF_CHACHA20, "aes128": orc.PRF_AES128, "chacha20_et": orc.PRF_CHACHA20_ET}[args.prf]
+    al = synth.alphas(w.B, w.N, w.seed)
+    seeds = synth.gen_seeds(w.B, w.seed)
     T = synth.table(w.N, w.D, w.seed)
     threads = cpu_threads()
     sample = min(w.B, threads)
+    okeys = [orc.gen(w.log_n, int(a), 1, s, prf=code)[0] for a, s in zip(al[:sample], seeds[:sample])]
     times = []
     for i in range(args.warmup + args.steps):
-        _, dt = oracle_sample(w, wire, T, threads, sample)
+        _, dt = oracle_answers(okeys, T, threads)
         if i >= args.warmup:
             times.append(dt)
     step = sum(times) / len(times)
@@ -174,13 +272,14 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": w.name + ": " + w.note, "log_n": w.log_n, "N": w.N, "D": w.D, "B": w.B},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+        "config": workload_config(w, args.prf, args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "cpu": cpu_model(),
                          "sample": "%d of the %d keys per step (one key per thread), full 2^%d-row table" %
                                    (sample, w.B, w.log_n)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "latency_ms": percentiles([t * 1e3 for t in times]),
         "note": "the paper publishes no code; the reference arm is this repo's plain CPU oracle "
-                "(oracle/dpf_oracle.c) on the host cores",
+                "(oracle/dpf_oracle.c, its own Gen) on the host cores",
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -188,7 +287,7 @@ def run_reference(args, rank, world):
 
 # ---------------------------------------------------------------------- our arm
 
-def main():
+def parse(argv):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
@@ -196,23 +295,46 @@ def main():
     ap.add_argument("--config", default="c3", choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--prf", default="chacha20", choices=["chacha20", "aes128", "chacha20_et"],
+    ap.add_argument("--prf", default="chacha20", choices=list(PRFS),
                     help="tree PRF (chacha20 = the paper's fastest standard PRF, Table 5; aes128 = its baseline; "
                          "chacha20_et = ChaCha20 with early-terminated 16-row leaves, DESIGN.md R20)")
     ap.add_argument("--table", default="auto", choices=["auto", "packed", "rowmajor"],
-                    help="packed = limb-packed table + tcgen05 contraction (any D %% 4 == 0, padded to 128-column tiles); rowmajor = IMAD path")
+                    help="packed = limb-packed table + tcgen05 contraction (any D %% 4 == 0, padded to 128-column "
+                         "tiles); rowmajor = IMAD path")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--reduce", default="nccl", choices=["nccl", "p2p"],
                     help="N > 1: sum the row shards' partial answers with one NCCL reduce, or inside the fused "
                          "kernels (every rank red.adds into rank 0's buffer over a CUDA IPC / NVLink mapping)")
-    args = ap.parse_args()
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.impl == "reference":
-        return run_reference(args, rank, world)
-    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+    ap.add_argument("--dry-env", action="store_true", help=argparse.SUPPRESS)  # launch-contract test hook
+    return ap.parse_args(argv)
 
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    rank = int(os.environ.get("RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    if "WORLD_SIZE" not in os.environ:
+        if args.gpus > 1:
+            return spawn(args.gpus, argv)
+        world = 1
+    else:
+        world = int(os.environ["WORLD_SIZE"])
+        if world != args.gpus:
+            raise SystemExit("bench.py: WORLD_SIZE=%d but --gpus %d" % (world, args.gpus))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dry_env:
+        print(json.dumps({"rank": rank, "world": world, "local_rank": local_rank,
+                          "master_addr": os.environ.get("MASTER_ADDR")}), flush=True)
+        return 0
+    assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
+    return run_ours(args, rank, world, local_rank)
+
+
+def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2301_10904_b200 import dpfpir, shard
@@ -227,6 +349,7 @@ def main():
     w = synth.CONFIGS[args.config]
     r0, rows = shard.row_range(w.N, G, rank)
     g = (G - 1).bit_length()  # path levels each rank descends above its subtree(s)
+    inject = os.environ.get(INJECT_ENV) == "1"
 
     T_host = synth.table_rows(w.N, w.D, w.seed, r0, r0 + rows)
     T = torch.from_numpy(T_host.view(np.int32)).to(dev)
@@ -235,7 +358,9 @@ def main():
     Tp = dpfpir.table_pack(T, r0) if use_packed else None
     torch.cuda.synchronize()
     prf = prf_code(dpfpir, args.prf)
-    al, pairs = make_keys(w, dpfpir, prf)
+    al = synth.alphas(w.B, w.N, w.seed)
+    seeds = synth.gen_seeds(w.B, w.seed)
+    pairs = [dpfpir.gen(w.log_n, int(a), 1, s, prf=prf) for a, s in zip(al, seeds)]
     keys0 = dpfpir.KeyBatch.from_keys([p[0] for p in pairs])
     wire_host = dpfpir.keys_to_wire(keys0)
     wire = torch.from_numpy(wire_host).to(dev)
@@ -243,6 +368,8 @@ def main():
     out = torch.empty((w.B, w.D), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
     peer = shard.PeerShareReducer(out, dst=0) if (G > 1 and args.reduce == "p2p") else None
+    flush_l2 = rows * w.D * 4 <= L2_BYTES
+    scrub = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush_l2 else None
 
     def step():
         if peer is not None:  # fused reduction: accumulate into rank 0's answers
@@ -265,7 +392,10 @@ def main():
 
     # ---- correctness before timing: both servers' answers reconstruct T[alpha]
     step()
+    barrier()
     share0 = dpfpir.as_u32(out) if rank == 0 else None
+    if share0 is not None and inject:
+        share0[0, 0] ^= 1
     keys1 = dpfpir.KeyBatch.from_keys([p[1] for p in pairs])
     out1 = (dpfpir.eval_batch_packed(keys1, Tp, workspace=ws) if use_packed else
             dpfpir.eval_batch_shard(keys1, T, r0, workspace=ws))
@@ -276,6 +406,8 @@ def main():
         recon = dpfpir.reconstruct(share0, dpfpir.as_u32(out1))
         want = np.stack([synth.table_rows(w.N, w.D, w.seed, int(a), int(a) + 1)[0] for a in al])
         parity["reconstruct_all_queries"] = bool(np.array_equal(recon, want))
+    if G > 1:
+        parity.update(wrap_check(args, dpfpir, shard, dist, G, rank, dev, use_packed, prf, inject))
     barrier()
 
     # ---- value: device-resident keys, K steps between barriers
@@ -285,26 +417,32 @@ def main():
     sampler = ClockSampler(_nvsmi_index(local_rank))
     sampler.start()
     dpfpir.kernel_timer_begin(args.steps)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for _ in range(args.steps):
+    for i in range(args.steps):
+        if scrub is not None:
+            scrub.fill_(i & 0xFF)  # L2 flush between timed steps (outside the per-step events)
+        evs[i][0].record(stream)
         step()
+        evs[i][1].record(stream)
     ev1.record(stream)
     barrier()
-    ms = ev0.elapsed_time(ev1)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    region_ms = ev0.elapsed_time(ev1)
     kernel_ms = dpfpir.kernel_timer_read(args.steps)
     stats = dpfpir.last_eval_stats()
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([region_ms if scrub is None else sum(step_ms)] + step_ms, dtype=torch.float64, device=dev)
     if G > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    ms_per_step = ms_max / args.steps
+    tl = t.cpu().tolist()
+    ms_per_step = tl[0] / args.steps
+    lat = percentiles(tl[1:])
     value = w.B / (ms_per_step * 1e-3)
 
     # ---- e2e: host keys in, host answer out, every step
     e2e_steps = args.e2e_steps or max(3, args.steps // 2)
     host_out = torch.empty((w.B, w.D), dtype=torch.int32).pin_memory()
-
     # G == 1: the graph-captured serving step (dpf_server_*): host wire keys in,
     # host answers out, one graph launch per batch
     server = dpfpir.Server(w.B, w.log_n, Tp if use_packed else T, r0, prf=prf, stream=stream) if G == 1 else None
@@ -339,70 +477,35 @@ def main():
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_value = w.B / (float(te.item()) / e2e_steps * 1e-3)
     if rank == 0:
-        parity["e2e_equals_device_path"] = bool(np.array_equal(host_out.numpy().view(np.uint32), share0))
+        e2e_ans = host_out.numpy().view(np.uint32).copy()
+        if inject:
+            e2e_ans[0, 0] ^= 1
+        parity["e2e_equals_device_path"] = bool(np.array_equal(e2e_ans, share0))
 
-    # ---- roofline of the dominant kernel (fused eval), live CUDA-event time
-    pk = peaks()
-    v = ET_BITS[args.prf]
-    m = w.log_n - v - stats["frontier_depth"]
-    # algorithmic blocks per launch (no padding): the subtrees' internal nodes,
-    # plus one Convert block per final node with early termination
-    fused_blocks = w.B * ((rows >> v) >> m) * ((1 << m) - 1 + ((1 << m) if v else 0))
-    kern_avg_ms = sum(kernel_ms) / len(kernel_ms)
-    alu_peak = 148 * 64 * pk["sm_max_mhz"] * 1e6  # ALU-pipe lane-ops/s
-    ops_per_block = ALU_OPS_PER_BLOCK[args.prf]
-    achieved = ops_per_block * fused_blocks / (kern_avg_ms * 1e-3)
-    tree_blocks = (rows - 1 + g) if not v else (2 * (rows >> v) - 1 + g)
-    qps_roof = alu_peak / (ops_per_block * tree_blocks)
-    hbm_qps_roof = G * pk["hbm_gbs"] * 1e9 * w.B / (4.0 * w.N * w.D)
-    traffic = _ncu_traffic(w.name if args.prf == "chacha20" else "%s_%s" % (w.name, args.prf))
-    roofline = {
-        "bound": "alu", "achieved": achieved * 1e-12, "peak": alu_peak * 1e-12, "unit": "Tops/s",
-        "frac": achieved / alu_peak, "traffic": traffic,
-        "kernel": "fused_eval_tc_kernel" if use_packed else "fused_eval_kernel", "kernel_ms": kern_avg_ms,
-        "kernel_share_of_step": kern_avg_ms / ms_per_step,
-        "ops": ("640 ALU-pipe int32 ops (LOP3 xor + SHF rotate) per ChaCha20 block" if args.prf != "aes128" else
-                "4075 ALU-pipe ops per bitsliced AES-128 node (2 blocks + key schedule)") +
-               " x %d blocks per launch" % fused_blocks,
-        "peak_basis": "148 SMs x 64 ALU lanes/clk x %.0f MHz (%s)" % (pk["sm_max_mhz"], pk["source"]),
-        "qps_at_prf_roofline": qps_roof, "frac_qps": value / qps_roof, "qps_at_hbm_roofline": hbm_qps_roof,
-    }
+    roofline = roofline_of(args, w, rows, g, G, stats, kernel_ms, ms_per_step, value, use_packed)
 
-    # ---- CPU oracle beside it (rank 0, N = 1 only), doubles as a parity sample
+    # ---- CPU oracle beside it (rank 0): the parity sample; timed only at N = 1
     cpu = None
-    if rank == 0 and G == 1 and not args.no_cpu_baseline:
-        threads = cpu_threads()
-        T_full = T_host  # G == 1: the whole table
-        # bounded sample: chunks of `threads` keys (one per thread) until ~10 s
-        # of CPU work or the whole batch; every key is also a parity check
-        chunk = min(w.B, max(threads, 8))
-        sample, dt, exact = 0, 0.0, True
-        while sample < w.B and (sample == 0 or dt < 10.0):
-            k = min(chunk, w.B - sample)
-            sh, t = oracle_sample(w, wire_host[sample:sample + k], T_full, threads, k)
-            exact &= bool(np.array_equal(sh, share0[sample:sample + k]))
-            sample += k
-            dt += t
-        parity["oracle_sample_keys"] = sample
-        parity["bit_exact_vs_oracle"] = exact
-        cpu = {"value": sample / dt, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": "first %d of the %d party-0 keys, full table, %d threads, %.1f s wall" %
-                         (sample, w.B, threads, dt)}
+    if rank == 0:
+        cpu, sample_parity = oracle_leg(args, w, wire_host, share0, T_host if G == 1 else None, G)
+        parity.update(sample_parity)
+    if G > 1:
+        dist.barrier(device_ids=[local_rank])
 
+    rc = 0
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": G, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": w.name + ": " + w.note, "log_n": w.log_n, "N": w.N, "D": w.D, "B": w.B,
-                       "prf": args.prf,
-                       "parallelism": ("row-shard x%d + %s" % (G, "NCCL reduce" if args.reduce == "nccl" else
-                                       "in-kernel red.add into rank 0 over NVLink (CUDA IPC)")) if G > 1 else "1 GPU",
-                       "keys": "device-resident wire keys (dpf_eval_batch_wire%s)" % ("_packed" if use_packed else ""),
-                       "table": "limb-packed (dpf_table_pack, tcgen05 kind::i8 contraction)" if use_packed
-                       else "row-major int32 (IMAD contraction)",
-                       "l2": "no flush: table shard (%d MiB) >= L2 and the path is ALU-bound" %
-                             (rows * w.D * 4 >> 20)},
+            "config": workload_config(w, args.prf, G),
+            "impl_detail": {
+                "reduce": "none" if G == 1 else ("one NCCL reduce (int32 SUM)" if args.reduce == "nccl" else
+                                                 "in-kernel red.add.sys into rank 0 over NVLink (CUDA IPC)"),
+                "keys": "device-resident wire keys (dpf_eval_batch_wire%s)" % ("_packed" if use_packed else ""),
+                "table": "limb-packed (dpf_table_pack, tcgen05 kind::i8 contraction)" if use_packed
+                else "row-major int32 (IMAD contraction)"},
+            "latency_ms": lat,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(wire_host.nbytes),
                     "d2h_bytes_per_step": w.B * w.D * 4, "api": ("dpf_server_run (CUDA-graph serving step)" if G == 1 else
                             "dpf_eval_batch%s + %sD2H" % ("_packed" if use_packed else "_shard",
@@ -414,13 +517,158 @@ def main():
             "parity": parity,
             "plan": stats,
         }
-        print(json.dumps(line), flush=True)
+        rc = emit(line, parity)
     if peer is not None:
         peer.close()
     if G > 1:
+        flag = torch.tensor([rc], dtype=torch.int32, device=dev)
+        dist.broadcast(flag, src=0)
+        rc = int(flag.item())
         dist.barrier(device_ids=[local_rank])
         dist.destroy_process_group()
-    return 0
+    return rc
+
+
+def wrap_check(args, dpfpir, shard, dist, G, rank, dev, use_packed, prf, inject):
+    """N > 1: an all-0xFFFFFFFF table of 2^12 rows, row-sharded like the real
+    one, 32 keys with random beta: each rank's partial answers are (minus) sums
+    of leaf shares, so their int32 sum overflows in about half the words.  The
+    reduced answers must equal the oracle on the whole table bit-exactly, which
+    proves the reduce is addition mod 2^32 on this box's NCCL / NVLink path."""
+    import torch
+    n, N, D, B = 12, 1 << 12, 128, 32
+    a0, cnt = shard.row_range(N, G, rank)
+    Tw = torch.full((cnt, D), -1, dtype=torch.int32, device=dev)
+    Twp = dpfpir.table_pack(Tw, a0) if use_packed else None
+    al = synth.alphas(B, N, 0x3A9)
+    be = synth.betas(B, 0x3A9, random=True)
+    keys = [dpfpir.gen(n, int(a), int(b), s, prf=prf)[0] for a, b, s in zip(al, be, synth.gen_seeds(B, 0x3A9))]
+    kb = dpfpir.KeyBatch.from_keys(keys)
+    outw = torch.empty((B, D), dtype=torch.int32, device=dev)
+    if args.reduce == "p2p":
+        pr = shard.PeerShareReducer(outw, dst=0)
+        wire = torch.from_numpy(dpfpir.keys_to_wire(kb)).to(dev)
+        wsw = torch.empty(dpfpir.eval_workspace_bytes(B, n, cnt, D), dtype=torch.uint8, device=dev)
+        pr.begin()
+        dpfpir.eval_batch_wire_ex(wire, n, Twp if use_packed else Tw, a0, cnt, D, pr.ptr, dpfpir.DPF_EVAL_ACCUMULATE,
+                                  wsw, prf=prf, packed=use_packed)
+        pr.finish()
+        pr.close()
+    else:
+        if use_packed:
+            dpfpir.eval_batch_packed(kb, Twp, out=outw)
+        else:
+            dpfpir.eval_batch_shard(kb, Tw, a0, out=outw)
+        shard.reduce_partial_shares(outw, dst=0)
+    torch.cuda.synchronize()
+    if rank != 0:
+        return {}
+    from oracle import oracle as orc
+    got = dpfpir.as_u32(outw)
+    if inject:
+        got[0, 0] ^= 1
+    okeys = oracle_keys_from_wire(dpfpir.keys_to_wire(kb))
+    ones = np.full((N, D), 0xFFFFFFFF, np.uint32)
+    want = orc.answer_batch(okeys, ones, threads=cpu_threads())
+    # how many answer words overflow int32 when the per-rank partials are summed
+    parts = [orc.answer_batch(okeys, ones[r0:r0 + c], row_begin=r0, threads=cpu_threads())
+             for r0, c in (shard.row_range(N, G, r) for r in range(G))]
+    s = sum(p.view(np.int32).astype(np.int64) for p in parts)
+    wraps = int(np.count_nonzero((s < -(1 << 31)) | (s >= (1 << 31))))
+    return {"wrap_reduce_exact": bool(np.array_equal(got, want)), "wrap_reduce_words_overflowing": wraps,
+            "wrap_case_exercised": wraps > 0}
+
+
+def oracle_leg(args, w, wire_host, share0, T_full, G):
+    """rank 0.  N = 1: the CPU oracle on chunks of one key per host thread until
+    ~10 s of CPU work or the whole batch (every key is a parity check), plus one
+    key single-threaded -> cpu_baseline.  N > 1: a sample of the reduced
+    answers against the oracle on the whole table (regenerated here with
+    synth), untimed (cpu_baseline is rank 0 at N = 1 only)."""
+    parity = {}
+    threads = cpu_threads()
+    if G > 1:
+        T_all = synth.table(w.N, w.D, w.seed)
+        k = min(w.B, max(4, min(threads, 8 if w.log_n >= 24 else threads)))
+        sh, _ = oracle_answers(oracle_keys_from_wire(wire_host[:k]), T_all, min(threads, k))
+        parity["oracle_sample_keys"] = k
+        parity["bit_exact_vs_oracle"] = bool(np.array_equal(sh, share0[:k]))
+        return None, parity
+    if args.no_cpu_baseline:
+        sh, _ = oracle_answers(oracle_keys_from_wire(wire_host[:1]), T_full, 1)
+        parity["oracle_sample_keys"] = 1
+        parity["bit_exact_vs_oracle"] = bool(np.array_equal(sh, share0[:1]))
+        return None, parity
+    chunk = min(w.B, max(threads, 8))
+    sample, dt, exact = 0, 0.0, True
+    while sample < w.B and (sample == 0 or dt < 10.0):
+        k = min(chunk, w.B - sample)
+        sh, t = oracle_answers(oracle_keys_from_wire(wire_host[sample:sample + k]), T_full, threads)
+        exact &= bool(np.array_equal(sh, share0[sample:sample + k]))
+        sample += k
+        dt += t
+    # one key on one thread (the paper's 1-thread CPU column, P:856-862)
+    sh1, t1 = oracle_answers(oracle_keys_from_wire(wire_host[w.B - 1:w.B]), T_full, 1)
+    exact &= bool(np.array_equal(sh1, share0[w.B - 1:w.B]))
+    parity["oracle_sample_keys"] = min(w.B, sample + 1)
+    parity["bit_exact_vs_oracle"] = exact
+    cpu = {"value": sample / dt, "unit": UNIT, "cores": threads, "kind": "oracle", "cpu": cpu_model(),
+           "single_thread_value": 1.0 / t1,
+           "sample": "first %d of the %d party-0 keys, full table, %d threads, %.1f s wall; single thread: "
+                     "key %d alone, %.2f s" % (sample, w.B, threads, dt, w.B - 1, t1)}
+    return cpu, parity
+
+
+def roofline_of(args, w, rows, g, G, stats, kernel_ms, ms_per_step, value, use_packed):
+    """The dominant (fused) kernel against whichever resource binds it:
+    algorithmic work per launch / that resource's peak, the largest of
+      alu    = ALU-pipe ops of the PRF blocks (640 per ChaCha20 block; the
+               AES circuit count per node)            / 148 x 64 lanes x clock
+      tensor = 10 u8 limb MACs x 2 ops per (key, row, column) of the
+               contraction (tcgen05 path)             / 2 x the measured bf16
+               dense peak (int8 = fp8 rate = 2 x bf16, B200_PROFILING.md)
+      hbm    = the table shard read once              / the measured copy BW
+    frac = (that lower bound) / the live per-launch time."""
+    pk = peaks()
+    v = ET_BITS[args.prf]
+    m = w.log_n - v - stats["frontier_depth"]
+    # algorithmic blocks per launch (no padding): the subtrees' internal nodes,
+    # plus one Convert block per final node with early termination
+    fused_blocks = w.B * ((rows >> v) >> m) * ((1 << m) - 1 + ((1 << m) if v else 0))
+    kern_avg_ms = sum(kernel_ms) / len(kernel_ms)
+    alu_peak = 148 * 64 * pk["sm_max_mhz"] * 1e6  # ALU-pipe lane-ops/s
+    ops_per_block = ALU_OPS_PER_BLOCK[args.prf]
+    alu_work = ops_per_block * fused_blocks
+    tensor_peak = 2.0 * pk["bf16_tflops"] * 1e12
+    tensor_work = 2.0 * 10 * w.B * rows * w.D if use_packed else 0.0
+    hbm_peak = pk["hbm_gbs"] * 1e9
+    hbm_work = 4.0 * rows * w.D
+    bounds = {"alu": alu_work / alu_peak, "tensor": tensor_work / tensor_peak, "hbm": hbm_work / hbm_peak}
+    bound = max(bounds, key=bounds.get)
+    work, peak, unit = {"alu": (alu_work, alu_peak, "Tops/s"), "tensor": (tensor_work, tensor_peak, "TOPS (int8)"),
+                        "hbm": (hbm_work, hbm_peak, "GB/s")}[bound]
+    scale = 1e-9 if bound == "hbm" else 1e-12
+    achieved = work / (kern_avg_ms * 1e-3)
+    tree_blocks = (rows - 1 + g) if not v else (2 * (rows >> v) - 1 + g)
+    qps_roof = min(alu_peak / (ops_per_block * tree_blocks),
+                   w.B / max(bounds["tensor"], bounds["hbm"], 1e-30))
+    traffic = _ncu_traffic(w.name if args.prf == "chacha20" else "%s_%s" % (w.name, args.prf))
+    return {
+        "bound": bound, "achieved": achieved * scale, "peak": peak * scale, "unit": unit,
+        "frac": achieved / peak, "traffic": traffic,
+        "bounds_ms": {k: v_ * 1e3 for k, v_ in bounds.items()},
+        "kernel": "fused_eval_tc_kernel" if use_packed else "fused_eval_kernel", "kernel_ms": kern_avg_ms,
+        "kernel_share_of_step": kern_avg_ms / ms_per_step,
+        "ops": ("%g ALU-pipe ops per %s x %d per launch" %
+                (ops_per_block, "AES-128 node (circuit count, DESIGN.md §7)" if args.prf == "aes128" else
+                 "ChaCha20 block (LOP3 xor + SHF rotate)", fused_blocks)),
+        "peak_basis": {"alu": "148 SMs x 64 ALU lanes/clk x %.0f MHz" % pk["sm_max_mhz"],
+                       "tensor": "2 x %.1f TFLOP/s bf16 (%s)" % (pk["bf16_tflops"], pk["source"]),
+                       "hbm": "%.0f GB/s (%s)" % (pk["hbm_gbs"], pk["source"])},
+        "qps_at_roofline": qps_roof, "frac_qps": value / qps_roof,
+        "table_bytes_streamed": 4.0 * rows * (((w.D + 127) // 128 * 128) if use_packed else w.D) *
+                                max(1, -(-w.B // max(1, stats["keys_per_tile"]))),
+    }
 
 
 def _nvsmi_index(local_rank: int) -> int:

@@ -17,9 +17,12 @@
  *
  * Conventions: all multi-byte integers are little-endian.  Every function
  * returns a dpf_status code (never aborts, never throws across the ABI).
- * Buffers are always owned by the caller; the library keeps no global mutable
- * state and allocates nothing on the evaluation path (the device workspace is
- * caller-provided), so all entry points are thread-safe and reentrant.
+ * Buffers are always owned by the caller; the library allocates nothing on
+ * the evaluation path (the device workspace is caller-provided).  Its only
+ * process-wide state is a mutex-guarded per-device cache of SM / co-resident
+ * cluster counts used by the planners and per-host-thread key staging and
+ * kernel timers, so all entry points are thread-safe and reentrant (a
+ * workspace must not be used by two calls at once).
  * "device" pointers are CUDA device (or managed) pointers on the current
  * device; `stream` is a cudaStream_t passed as void* (NULL = legacy default
  * stream).  Device-side entry points are asynchronous on `stream` unless
@@ -163,9 +166,9 @@ int dpf_eval_batch_shard(const dpf_key *keys, uint32_t B, const uint32_t *table_
 
 /* Device-resident keys: as dpf_eval_batch_shard, but the B keys are already
  * on the device as consecutive wire-format records (dpf_key_serialize
- * output, stride dpf_key_wire_size(log_n) bytes, 16-byte aligned base),
- * e.g. received by the server straight into HBM; `prf` (enum dpf_prf) must be
- * the keys' PRF (stride dpf_key_wire_size_prf(log_n, prf) for ET keys).  The keys are NOT re-validated (device memory is not read by
+ * output, stride dpf_key_wire_size_prf(log_n, prf) bytes, 16-byte aligned
+ * base), e.g. received by the server straight into HBM; `prf` (enum dpf_prf)
+ * must be the keys' PRF.  The keys are NOT re-validated (device memory is not read by
  * the host): callers validate at dpf_key_deserialize time.  No host->device
  * traffic; fully asynchronous (AES keys are bitsliced into a private copy in
  * the workspace). */
@@ -274,7 +277,7 @@ int dpf_eval_batch_wire_packed(const uint8_t *keys_wire_dev, uint32_t B, uint32_
  *   shares[b][d] = sum_{row_begin <= j < row_begin+row_count}
  *                    Eval(keys[b], j) * table[j - row_begin][d]  (mod 2^32) */
 typedef struct dpf_eval_group {
-  const uint8_t *keys_wire; /* DEVICE: B wire-format keys (stride dpf_key_wire_size(log_n)), 16-B aligned */
+  const uint8_t *keys_wire; /* DEVICE: B wire-format keys, stride dpf_key_wire_size_prf(log_n, prf), 16-B aligned */
   uint32_t B;               /* keys in this group, >= 1 */
   uint32_t log_n;           /* depth of these keys' trees */
   const uint32_t *table;    /* DEVICE: row_count x D uint32, row-major, 16-B aligned */

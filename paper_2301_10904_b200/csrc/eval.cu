@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -36,6 +37,7 @@
 
 namespace dpfpir {
 bool host_key_valid(const dpf_key &k);
+bool wire_header_valid(const uint8_t *header32);
 
 namespace dev {
 
@@ -111,8 +113,14 @@ __device__ __forceinline__ void bulk_g2s(void *dst_smem, const void *src_gmem, u
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-__device__ __forceinline__ void red_add_u32(uint32_t *addr, uint32_t v) {
-  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+// a6 flush.  `sys`: the answers may live in another GPU's memory (peer
+// mapped, DPF_EVAL_ACCUMULATE, several GPUs adding concurrently): the atomic
+// must be system-scoped to be atomic across devices (PTX memory model).
+__device__ __forceinline__ void red_add_u32(uint32_t *addr, uint32_t v, uint32_t sys) {
+  if (sys)
+    asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
+  else
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
 }
 
 // Wire-format key accessors (include/dpfpir.h).
@@ -227,6 +235,7 @@ struct FusedParams {
   uint32_t CG, KG, SG;     // consumer col groups / key groups / slot groups
   uint32_t y_stage_words, t_stage_words;  // t: one T-ring entry (CN nodes x 2W rows x D + pad)
   uint32_t CN, n_chunks, NST;             // IMAD kernel: nodes per T entry, entries per window, ring depth
+  uint32_t sys_red;                       // flush with system-scope atomics (answers in peer memory)
 };
 
 __device__ __forceinline__ GroupDesc group_of(const FusedParams &p, uint32_t item) {
@@ -471,7 +480,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
 #pragma unroll
             for (int c = 0; c < CPL; ++c) {
               const uint32_t col = colbase + 32 * c;
-              if (col < p.D) red_add_u32(g.shares + uint64_t(b) * p.D + col, neg ? 0u - acc[k][c] : acc[k][c]);
+              if (col < p.D) red_add_u32(g.shares + uint64_t(b) * p.D + col, neg ? 0u - acc[k][c] : acc[k][c], p.sys_red);
             }
           }
 #pragma unroll
@@ -703,15 +712,29 @@ struct Plan {
   uint64_t prf_blocks;
 };
 
+// SM count of the current device, cached per device (mutex-guarded: the
+// planners may run on several host threads).  148 without a device.
+int current_device() {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return dev;
+}
+std::mutex g_cache_mu;
 int num_sms() {
-  static int sms = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
-                                                  cudaSuccess)
-      sms = 148;
-  });
+  static std::map<int, int> cache;
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int sms = 148;
+  if (dev >= 0 && cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    sms = 148;
+  }
+  cache[dev] = sms;
   return sms;
 }
 
@@ -908,10 +931,14 @@ constexpr uint32_t kTcNSY = 3;
 // How many 2-CTA clusters of the tcgen05 kernel fit on the device at once
 // (cudaOccupancyMaxActiveClusters; num_sms/2 without a device).
 uint32_t max_pairs(size_t smem_bytes) {
-  static uint32_t cached = 0;
-  static size_t cached_smem = 0;
-  if (cached && cached_smem == smem_bytes) return cached;
+  static std::map<std::pair<int, size_t>, uint32_t> cache;  // (device, smem) -> pairs; under g_cache_mu
+  const int dev_id = current_device();
   uint32_t r = uint32_t(num_sms()) / 2;
+  {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto it = cache.find({dev_id, smem_bytes});
+    if (it != cache.end()) return it->second;
+  }
   cudaLaunchConfig_t cfg;
   std::memset(&cfg, 0, sizeof cfg);
   cfg.gridDim = dim3(2 * r);
@@ -926,15 +953,14 @@ uint32_t max_pairs(size_t smem_bytes) {
   cfg.numAttrs = 1;
   auto fn = &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, true, false>;
   int n = 0;
-  int dev_id = 0;
-  if (cudaGetDevice(&dev_id) == cudaSuccess &&
+  if (dev_id >= 0 &&
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_bytes)) == cudaSuccess &&
       cudaOccupancyMaxActiveClusters(&n, fn, &cfg) == cudaSuccess && n > 0)
     r = std::min<uint32_t>(r, uint32_t(n));
   else
     cudaGetLastError();  // clear: no device (host-only planning)
-  cached = r;
-  cached_smem = smem_bytes;
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  cache[{dev_id, smem_bytes}] = r;
   return r;
 }
 // Early termination (R20) fills a y stage with ~2 ChaCha20 blocks per thread
@@ -1225,6 +1251,7 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
   p.CN = pl.CN;
   p.n_chunks = pl.n_chunks;
   p.NST = pl.NST;
+  p.sys_red = (flags & DPF_EVAL_ACCUMULATE) ? 1u : 0u;
   if (pl.tc) {
     const int rc = launch_tc_kernel(pl, p, st);
     if (rc) return rc;
@@ -1607,12 +1634,11 @@ extern "C" int dpf_server_create(uint32_t B, uint32_t log_n, uint32_t prf, const
 }
 
 // Wire-format header checks of a host key (include/dpfpir.h "Wire format").
+// The codec's own predicate (dpf_key_deserialize: magic, version, prf,
+// party, log_n range, lsb(root) == party, reserved == 0, ET cw_out == 0) plus
+// this server's shape.
 static bool wire_header_ok(const uint8_t *k, uint32_t log_n, uint32_t prf) {
-  uint32_t magic;
-  std::memcpy(&magic, k, 4);
-  const uint8_t party = k[6];
-  return magic == DPF_KEY_MAGIC && k[4] == DPF_KEY_VERSION && k[5] == prf && party <= 1 && k[7] == log_n &&
-         (k[16] & 1u) == party;
+  return dpfpir::wire_header_valid(k) && k[5] == prf && k[7] == log_n;
 }
 
 extern "C" int dpf_server_run(dpf_server *sv, const uint8_t *keys_wire_host, uint32_t *shares_host) {
@@ -2102,6 +2128,7 @@ int eval_grouped_impl(const dpf_eval_group *groups, uint32_t n_groups, uint32_t 
   p.CN = pl.CN;
   p.n_chunks = pl.n_chunks;
   p.NST = pl.NST;
+  p.sys_red = 0;  // grouped answers are this device's buffers
   if (pl.tc) {
     if ((rc = launch_tc_kernel(pl, p, st)) != DPF_OK) return rc;
   } else {

@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
           if (bkey < g.B && d < D) {
             const uint32_t val = v[j] + (x[j] << 16) + (z[j] << 24);  // A0 + 2^8 A1 + 2^16 A2 + 2^24 A3
             const uint32_t neg = key_party(g.keys + uint64_t(bkey) * g.kstride);
-            red_add_u32(g.shares + uint64_t(bkey) * D + d, neg ? 0u - val : val);
+            red_add_u32(g.shares + uint64_t(bkey) * D + d, neg ? 0u - val : val, p.sys_red);
           }
         }
       }

@@ -326,4 +326,15 @@ extern "C" const char *dpf_version(void) { return "libdpfpir 0.2 (sm_100a, ChaCh
 // Shared with eval.cu: key validation for the device path.
 namespace dpfpir {
 bool host_key_valid(const dpf_key &k) { return key_ok(k); }
+// The header predicate of dpf_key_deserialize on a 32-byte wire header.
+bool wire_header_valid(const uint8_t *in) {
+  dpf_key t;
+  std::memset(&t, 0, sizeof t);
+  t.magic = ld32(in);
+  t.version = in[4]; t.prf = in[5]; t.party = in[6]; t.log_n = in[7];
+  t.cw_out = ld32(in + 8);
+  t.reserved = ld32(in + 12);
+  std::memcpy(t.root, in + 16, 16);
+  return key_ok(t);
+}
 }  // namespace dpfpir

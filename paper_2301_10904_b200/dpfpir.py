@@ -235,9 +235,12 @@ def eval_workspace_bytes(B: int, log_n: int, rows: int, D: int) -> int:
 _ws_cache: dict = {}
 
 
-def _workspace(nbytes: int, device):
+def _workspace(nbytes: int, device, stream=None):
+    """Scratch workspace for calls that pass none: one buffer per (device,
+    stream), so calls ordered on one stream never overlap on it; a call on
+    another stream gets another buffer.  Long-lived users (Server) own theirs."""
     import torch
-    key = (str(device),)
+    key = (str(device), _stream_ptr(stream))
     ws = _ws_cache.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=device)
@@ -273,7 +276,7 @@ def eval_batch_shard(keys, table_shard, row_begin: int = 0, out=None, workspace=
     need = eval_workspace_bytes(B, kb.log_n, rows, D)
     if need == 0:
         raise DpfError(DPF_EINVAL, "dpf_eval_workspace_bytes")
-    ws = workspace if workspace is not None else _workspace(need, table_shard.device)
+    ws = workspace if workspace is not None else _workspace(need, table_shard.device, stream)
     _check(lib().dpf_eval_batch_shard(kb.ptr, B, table_shard.data_ptr(), row_begin, rows, D, out.data_ptr(),
                                       ws.data_ptr(), ws.numel() * ws.element_size(), _stream_ptr(stream)),
            "dpf_eval_batch_shard")
@@ -347,7 +350,9 @@ class Server:
         need = lib().dpf_server_workspace_bytes(B, log_n, prf, rows, D)
         if need == 0:
             raise DpfError(DPF_EINVAL, "dpf_server_workspace_bytes")
-        self.ws = _workspace(need, dev)
+        # private workspace: the captured graph replays on the server's own
+        # stream for the object's lifetime, so no other call may share it
+        self.ws = torch.empty(need, dtype=torch.uint8, device=dev)
         self.table = table  # keep alive
         self.B, self.D, self.wire = B, D, key_wire_size(log_n, prf)
         h = ctypes.c_void_p()
@@ -388,7 +393,7 @@ def eval_batch_wire(keys_wire_dev, log_n: int, table_shard, row_begin: int = 0, 
     if out is None:
         out = torch.empty((B, D), dtype=torch.int32, device=table_shard.device)
     need = eval_workspace_bytes(B, log_n, rows, D)
-    ws = workspace if workspace is not None else _workspace(need, table_shard.device)
+    ws = workspace if workspace is not None else _workspace(need, table_shard.device, stream)
     _check(lib().dpf_eval_batch_wire(keys_wire_dev.data_ptr(), B, log_n, prf, table_shard.data_ptr(), row_begin, rows, D,
                                      out.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(),
                                      _stream_ptr(stream)), "dpf_eval_batch_wire")
@@ -432,7 +437,7 @@ def eval_batch_packed(keys, packed: PackedTable, out=None, workspace=None, strea
     if out is None:
         out = torch.empty((B, D), dtype=torch.int32, device=packed.data.device)
     need = eval_workspace_bytes(B, kb.log_n, packed.row_count, D)
-    ws = workspace if workspace is not None else _workspace(need, packed.data.device)
+    ws = workspace if workspace is not None else _workspace(need, packed.data.device, stream)
     _check(lib().dpf_eval_batch_packed(kb.ptr, B, packed.data.data_ptr(), packed.row_begin, packed.row_count, D,
                                        out.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(),
                                        _stream_ptr(stream)), "dpf_eval_batch_packed")
@@ -447,7 +452,7 @@ def eval_batch_wire_packed(keys_wire_dev, log_n: int, packed: PackedTable, out=N
     if out is None:
         out = torch.empty((B, D), dtype=torch.int32, device=packed.data.device)
     need = eval_workspace_bytes(B, log_n, packed.row_count, D)
-    ws = workspace if workspace is not None else _workspace(need, packed.data.device)
+    ws = workspace if workspace is not None else _workspace(need, packed.data.device, stream)
     _check(lib().dpf_eval_batch_wire_packed(keys_wire_dev.data_ptr(), B, log_n, prf, packed.data.data_ptr(),
                                             packed.row_begin, packed.row_count, D, out.data_ptr(), ws.data_ptr(),
                                             ws.numel() * ws.element_size(), _stream_ptr(stream)),
@@ -489,7 +494,7 @@ def eval_grouped(groups, D: int, prf: int = DPF_PRF_CHACHA20, workspace=None, st
     if need == 0:
         raise DpfError(DPF_EINVAL, "dpf_eval_grouped_workspace_bytes")
     dev = groups[0][2].device
-    ws = workspace if workspace is not None else _workspace(need, dev)
+    ws = workspace if workspace is not None else _workspace(need, dev, stream)
     _check(lib().dpf_eval_grouped(arr, len(groups), D, prf, ws.data_ptr(), ws.numel() * ws.element_size(),
                                   _stream_ptr(stream)), "dpf_eval_grouped")
     return [g[4] for g in groups]
@@ -507,7 +512,7 @@ def eval_grouped_packed(groups, D: int, prf: int = DPF_PRF_CHACHA20, workspace=N
     if need == 0:
         raise DpfError(DPF_EINVAL, "dpf_eval_grouped_packed_workspace_bytes")
     dev = groups[0][4].device
-    ws = workspace if workspace is not None else _workspace(need, dev)
+    ws = workspace if workspace is not None else _workspace(need, dev, stream)
     _check(lib().dpf_eval_grouped_packed(arr, len(groups), D, prf, ws.data_ptr(), ws.numel() * ws.element_size(),
                                          _stream_ptr(stream)), "dpf_eval_grouped_packed")
     return [g[4] for g in groups]
@@ -524,7 +529,7 @@ def serve_batch(keys, table_shard, shares_host, row_begin: int = 0, workspace=No
     rows, D = table_shard.shape
     B = len(kb)
     need = serve_workspace_bytes(B, kb.log_n, rows, D)
-    ws = workspace if workspace is not None else _workspace(need, table_shard.device)
+    ws = workspace if workspace is not None else _workspace(need, table_shard.device, stream)
     if isinstance(shares_host, np.ndarray):
         assert shares_host.dtype in (np.uint32, np.int32) and shares_host.size >= B * D
         hptr = shares_host.ctypes.data
@@ -542,7 +547,7 @@ def eval_leaves(keys, device="cuda", stream=None):
     kb = _as_batch(keys)
     B, n = len(kb), kb.log_n
     out = torch.empty((B, 1 << n), dtype=torch.int32, device=device)
-    ws = _workspace(B * key_wire_size(n, kb.prf) + 256, out.device)
+    ws = _workspace(B * key_wire_size(n, kb.prf) + 256, out.device, stream)
     _check(lib().dpf_eval_leaves(kb.ptr, B, out.data_ptr(), ws.data_ptr(), ws.numel(), _stream_ptr(stream)),
            "dpf_eval_leaves")
     return out

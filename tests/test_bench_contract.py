@@ -48,3 +48,67 @@ def test_gpu_arm_refuses_without_cuda():
     r = _run(["--config", "c1", "--steps", "1", "--warmup", "3"])
     assert r.returncode != 0
     assert "CUDA" in (r.stdout + r.stderr)
+
+
+def test_reference_arm_is_pure_oracle_and_same_config():
+    """The reference arm never loads libdpfpir (keys from the oracle's Gen) and
+    its config dict is the GPU arm's (bench.workload_config)."""
+    r = _run(["--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "3", "--gpus", "2"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    import bench
+    assert d["config"] == bench.workload_config(bench.synth.CONFIGS["c1"], "chacha20", 2)
+    assert d["n_gpus"] == 2 and "cpu" in d["cpu_baseline"]
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    ref = src[src.index("def run_reference"):src.index("# ---------------------------------------------------------------------- our arm")]
+    assert "dpfpir" not in ref and "paper_2301_10904_b200" not in ref
+
+
+def test_gpus_n_self_spawns_n_ranks():
+    """`bench.py --gpus 2` without WORLD_SIZE re-launches itself under
+    torch.distributed.run with 2 ranks (the GPU arm is replaced by --dry-env,
+    which prints each rank's launch environment)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-env"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    rows = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert sorted(x["rank"] for x in rows) == [0, 1]
+    assert all(x["world"] == 2 and x["master_addr"] == "127.0.0.1" for x in rows)
+    assert sorted(x["local_rank"] for x in rows) == [0, 1]
+
+
+def test_world_size_must_match_gpus():
+    r = _run(["--gpus", "4", "--dry-env"], {"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode != 0 and "WORLD_SIZE=2" in (r.stdout + r.stderr)
+
+
+def test_gpus_1_runs_in_process():
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--dry-env"], capture_output=True,
+                       text=True, timeout=120, env=env, cwd=ROOT)
+    assert r.returncode == 0
+    rows = [json.loads(ln) for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert rows == [{"rank": 0, "world": 1, "local_rank": 0, "master_addr": None}]
+
+
+def test_parity_miss_suppresses_line_and_fails(capsys):
+    import bench
+    line = {"metric": bench.METRIC, "value": 1.0}
+    assert bench.emit(line, {"reconstruct_all_queries": True, "bit_exact_vs_oracle": False}) == 3
+    out = capsys.readouterr()
+    assert out.out == "" and "PARITY FAILURE" in out.err
+    assert bench.emit(line, {}) == 3  # no checks ran: also a failure
+    capsys.readouterr()
+    assert bench.emit(line, {"reconstruct_all_queries": True, "oracle_sample_keys": 4,
+                             "bit_exact_vs_oracle": True}) == 0
+    assert json.loads(capsys.readouterr().out)["value"] == 1.0
+
+
+def test_aes_circuit_count():
+    """gates of BMP13 S-box (113), Maximov MixColumns (92),
+    AddRoundKey, key expansion (+ Rcon bits), / 32 bit-slices per word."""
+    import bench
+    gates = 10 * 32 * 113 + 9 * 8 * 92 + 11 * 256 + 10 * (4 * 113 + 128) + 16
+    assert bench.aes_alu_ops_per_node() == gates / 32
+    assert 1600 < bench.ALU_OPS_PER_BLOCK["aes128"] < 1610

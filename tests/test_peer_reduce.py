@@ -25,7 +25,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, case, outdir):
+def _worker(rank, world, port, case, outdir, mode="p2p"):
     import torch.distributed as dist
     from paper_2301_10904_b200 import dpfpir, shard
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -42,6 +42,21 @@ def _worker(rank, world, port, case, outdir):
     wire = torch.from_numpy(dpfpir.keys_to_wire(keys)).cuda()
     ws = torch.empty(dpfpir.eval_workspace_bytes(B, n, rows, D), dtype=torch.uint8, device="cuda")
     out = torch.full((B, D), -1, dtype=torch.int32, device="cuda")  # garbage until the owner zeroes it
+    if mode == "reduce":
+        # the product's shard evaluation under a process group, answers summed
+        # by shard.reduce_partial_shares (the bench's NCCL path; gloo on host
+        # tensors here because the ranks share one GPU)
+        for _ in range(2):
+            part = dpfpir.eval_batch_wire_packed(wire, n, tbl, out=out, workspace=ws, prf=prf) if packed else \
+                dpfpir.eval_batch_wire(wire, n, tbl, r0, out=out, workspace=ws, prf=prf)
+            host = part.cpu()
+            shard.reduce_partial_shares(host, dst=0)
+        if rank == 0:
+            np.save(os.path.join(outdir, "sum.npy"), host.numpy().view(np.uint32))
+            np.save(os.path.join(outdir, "keys.npy"), dpfpir.keys_to_wire(keys))
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     red = shard.PeerShareReducer(out, dst=0)
     for _ in range(3):  # repeated steps: zero, accumulate, complete
         red.begin()
@@ -61,13 +76,14 @@ def _worker(rank, world, port, case, outdir):
     (3, (12, 4000, 256, 70, 1, True)),      # tcgen05 CTA pairs, unequal shards
     (2, (14, 10000, 128, 33, 3, True)),     # early termination, tcgen05
 ])
-def test_peer_accumulate_equals_oracle(oracle, tmp_path, world, case):
+@pytest.mark.parametrize("mode", ["p2p", "reduce"])
+def test_peer_accumulate_equals_oracle(oracle, tmp_path, world, case, mode):
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
     from paper_2301_10904_b200 import build as pbuild
     pbuild.build()
-    mp.spawn(_worker, args=(world, _free_port(), case, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), case, str(tmp_path), mode), nprocs=world, join=True)
     n, N, D, B, prf, packed = case
     got = np.load(tmp_path / "sum.npy")
     wire = np.load(tmp_path / "keys.npy")
