@@ -327,8 +327,9 @@ def main(argv=None):
             raise SystemExit("bench.py: WORLD_SIZE=%d but --gpus %d" % (world, args.gpus))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.dry_env:
-        print(json.dumps({"rank": rank, "world": world, "local_rank": local_rank,
-                          "master_addr": os.environ.get("MASTER_ADDR")}), flush=True)
+        # one write(2) per line: atomic on a pipe shared by the ranks
+        os.write(1, (json.dumps({"rank": rank, "world": world, "local_rank": local_rank,
+                                 "master_addr": os.environ.get("MASTER_ADDR")}) + "\n").encode())
         return 0
     assert args.warmup >= 3, "timing rules: at least 3 warm-up steps"
     return run_ours(args, rank, world, local_rank)

@@ -107,8 +107,10 @@ __device__ __forceinline__ uint32_t leaf_value(const uint4 s, uint32_t cw_out) {
 __device__ __forceinline__ void leaf_values16(const uint4 s, const uint32_t (&cwl)[16], uint32_t (&y)[16]) {
   chacha_convert16(s, y);
   const uint32_t t = s.x & 1u;
+  // y += t * CWL as IMAD on the FMA pipe (a select would take ALU slots
+  // from the PRF; t is 0 or 1)
 #pragma unroll
-  for (int c = 0; c < 16; ++c) y[c] += t * cwl[c];
+  for (int c = 0; c < 16; ++c) asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(y[c]) : "r"(t), "r"(cwl[c]));
 }
 
 // CWL of a wire key: the 16 LE words in the column after tree level h.

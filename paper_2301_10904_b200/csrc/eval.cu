@@ -924,6 +924,10 @@ int make_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D
 }
 
 constexpr uint32_t kTcNP = 16;   // producer warps (4 per SMSP)
+// DFS stack of the tcgen05 kernel: one uint4 per producer thread for each of
+// the subtree depths 1..m-1 (pending right children).
+constexpr size_t kTcLevelBytes = size_t(32) * kTcNP * 16;
+inline size_t tc_stack_bytes(uint32_t m) { return m > 1 ? size_t(m - 1) * kTcLevelBytes : 0; }
 // y-ring depth: 3 stages (with CTA pairs and N = 128 the SMEM fits them
 // beside a full DFS stack; measured t5 0.906 -> 0.916, c3 0.894 -> 0.896).
 constexpr uint32_t kTcNSY = 3;
@@ -992,7 +996,18 @@ int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint3
 // half the y-ring handshakes per block (measured c3 0.896 -> 0.912, t5 0.914
 // -> 0.925).  Early termination: one final node per window.
 int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et = false) {
-  if (et) return make_tc_plan_w(B, log_n, r0, rows, D, pl, true, 1);
+  if (et) {
+    // Early termination: two final nodes per window with a 2-deep y ring
+    // (half the y handshakes; measured c3 0.778 -> 0.784, t5 0.803 -> 0.815
+    // with the T loader polling), else one final node and a 3-deep ring.
+    // DPF_ET_W=1 pins the single-node window (tuning).
+    static const bool allow2 = [] {
+      const char *e = getenv("DPF_ET_W");
+      return !(e && atoi(e) == 1);
+    }();
+    if (allow2 && make_tc_plan_w(B, log_n, r0, rows, D, pl, true, 2) == DPF_OK) return DPF_OK;
+    return make_tc_plan_w(B, log_n, r0, rows, D, pl, true, 1);
+  }
   int rc = make_tc_plan_w(B, log_n, r0, rows, D, pl, false, 4);
   if (rc != DPF_OK || pl.m < 4) return rc;
   static const bool allow8 = [] {  // DPF_TC_W=4 pins the 4-leaf-pair window (tuning)
@@ -1033,7 +1048,7 @@ int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint3
   const uint32_t kmin = pl.pair ? 32 : 16;
   while (Ktp > kmin && Ktp / 2 >= B) Ktp >>= 1;
   pl.Kt = pl.pair ? Ktp / 2 : Ktp;
-  pl.nsy = tc_y_stages(et);
+  pl.nsy = (et && W == 2) ? 2u : tc_y_stages(et);
   pl.Ft = 32 * kTcNP / pl.Kt;
   pl.tasks = Ktp * pl.Ft;  // per item (both CTAs of a pair)
   pl.n_ktiles = (B + Ktp - 1) / Ktp;
@@ -1045,11 +1060,11 @@ int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint3
   // SMEM: T ring + y ring + the DFS stack (16 B per producer thread per level)
   pl.nst = tc_t_stages(D);
   const size_t fixed = 1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(pl.nsy) * pl.y_stage_bytes;
-  const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / (32 * kTcNP * 16)));
+  const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / kTcLevelBytes) + 1);
   const uint32_t m_min = tc_m_min(et, W);  // a subtree holds >= one window
   if (m_cap < m_min || n < m_min) return DPF_EINVAL;
   // co-resident CTA pairs: a GPC with an odd SM count leaves an SM unpaired
-  const uint32_t workers = pl.pair ? max_pairs(fixed + size_t(m_cap) * 32 * kTcNP * 16) : uint32_t(num_sms());
+  const uint32_t workers = pl.pair ? max_pairs(fixed + tc_stack_bytes(m_cap)) : uint32_t(num_sms());
   pl.m = choose_m_target(pl, n, m_min, m_cap, workers);
   if (const char *e = getenv("DPF_FORCE_M")) {  // tuning override
     const uint32_t fm = uint32_t(atoi(e));
@@ -1068,7 +1083,7 @@ int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint3
   const uint32_t cols = n_dt_cta * 4 * Ktp;
   pl.tmem_cols = 32;
   while (pl.tmem_cols < cols) pl.tmem_cols <<= 1;
-  pl.smem_bytes = fixed + size_t(pl.m) * 32 * kTcNP * 16;  // stack slots 1..m-1 (slot 0 unused)
+  pl.smem_bytes = fixed + tc_stack_bytes(pl.m);
   if (pl.smem_bytes > 227 * 1024) return DPF_EINVAL;
   pl.grid = pl.pair ? 2 * choose_grid(pl.n_items, pl.n_ktiles, workers) : choose_grid(pl.n_items, pl.n_ktiles);
   pl.prf_blocks = count_blocks(pl, B);
@@ -1135,12 +1150,19 @@ int launch_tc_kernel(const Plan &pl, const dev::FusedParams &p, cudaStream_t st)
     const char *e = getenv("DPF_LOADER_SPIN");
     return uint32_t(e && atoi(e) == 1);
   }();
-  tp.loader_spin = spin;
+  // early termination's T ring turns over 4x faster per block: the loader
+  // polls (try_wait) instead of sleeping (measured t5 ET 0.807 -> 0.815)
+  tp.loader_spin = spin || pl.prf == DPF_PRF_CHACHA20_ET;
   static const uint32_t nomma = [] {
     const char *e = getenv("DPF_DEBUG_NOMMA");
     return uint32_t(e && atoi(e) == 1);
   }();
   tp.debug_nomma = nomma;
+  static const uint32_t role_swap = [] {
+    const char *e = getenv("DPF_ROLE_SWAP");
+    return uint32_t(e && atoi(e) == 1);
+  }();
+  tp.role_swap = role_swap;
   using TcFn = void (*)(const dev::TcParams);
   TcFn fn;
   // early termination: producers drain TMEM (EPIP, 18 warps, 96 registers)
@@ -1149,8 +1171,10 @@ int launch_tc_kernel(const Plan &pl, const dev::FusedParams &p, cudaStream_t st)
     fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, true, false>
                  : &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, false, false>;
   else if (epip)
-    fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSYEt, 4, true, true>
-                 : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSYEt, 4, false, true>;
+    fn = pl.nsy == 2 ? (pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, true, true>
+                                : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, false, true>)
+                     : (pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSYEt, 4, true, true>
+                                : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSYEt, 4, false, true>);
   else
     fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, true, false>
                  : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, false, false>;
@@ -1918,9 +1942,8 @@ int make_grouped_tc_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint3
   const uint32_t m_min = tc_m_min(et, pl.W);
   const uint32_t Ktp = pl.pair ? 2 * pl.Kt : pl.Kt;
   const size_t fixed = 1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(pl.nsy) * pl.y_stage_bytes;
-  const size_t level_bytes = size_t(32) * kTcNP * 16;
-  uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / level_bytes));
-  const uint32_t workers = pl.pair ? max_pairs(fixed + size_t(m_cap) * level_bytes) : uint32_t(num_sms());
+  uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / kTcLevelBytes) + 1);
+  const uint32_t workers = pl.pair ? max_pairs(fixed + tc_stack_bytes(m_cap)) : uint32_t(num_sms());
   {
     double units = 0;
     for (uint32_t i = 0; i < G; ++i) units += double((gs[i].B + Ktp - 1) / Ktp) * double(gs[i].row_count >> v);
@@ -1961,7 +1984,7 @@ int make_grouped_tc_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint3
     d.nwin = (et ? (1u << m) : (1u << (m - 1))) / pl.W;
     m_max = std::max(m_max, m);
   }
-  pl.smem_bytes = fixed + size_t(m_max) * level_bytes;
+  pl.smem_bytes = fixed + tc_stack_bytes(m_max);
   gp.order.resize(G);
   for (uint32_t i = 0; i < G; ++i) gp.order[i] = i;
   std::stable_sort(gp.order.begin(), gp.order.end(),
