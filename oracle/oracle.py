@@ -5,7 +5,9 @@ bench.py's cpu_baseline / ``--impl reference`` legs -- never by the product
 package ``paper_2301_10904_b200``.  Shares no code with the CUDA path.
 
 Every function here is argument marshalling around the plain C oracle; the
-citations for what each computes are in dpf_oracle.c.
+citations for what each computes are in dpf_oracle.c.  The exception is the
+PBR section at the end (partial batch retrieval): plain Python
+loops over bins, each bin answered by the C oracle's answer_batch.
 """
 from __future__ import annotations
 
@@ -228,3 +230,60 @@ def key_from_wire(b: bytes) -> OracleKey:
     if rc:
         raise ValueError("bad key wire bytes (rc=%d)" % rc)
     return k
+
+
+# ---------------------------------------------------------------- PBR (row f2)
+# Partial batch retrieval (§4.1): "segmenting table T into
+# L/I bins of size I, and issuing individual DPF-PIR queries to each bin ...
+# a single PBR can fetch only one query from each bin.  If more than one query
+# index fall into the same bin, the rest of the queries except for the one
+# must be dropped."  Reading R21: I = 2^log_i; bin b holds rows
+# [bI, min(bI + I, N)) (the last bin is ragged: its rows >= N are absent, R12);
+# the kept query of a bin is the first of its rows in the client's request
+# order; a bin with no needed row gets a dummy query (its index is the
+# caller's choice: P:656-659 pads with dummies so the count leaks nothing).
+
+
+def pbr_n_bins(N: int, log_i: int) -> int:
+    """L/I bins (rounded up: the last bin is ragged when I does not divide N)."""
+    return (N + (1 << log_i) - 1) >> log_i
+
+
+def pbr_plan(needed_rows, N: int, log_i: int):
+    """Client side of PBR, written as the loop the text describes.
+    Returns (index, dropped): index[b] = the in-bin index queried in bin b, or
+    -1 where bin b gets a dummy; dropped = the needed rows that were not kept,
+    in request order.  Duplicate requests of one row count once."""
+    I = 1 << log_i
+    index = [-1] * pbr_n_bins(N, log_i)
+    dropped = []
+    seen = set()
+    for r in needed_rows:
+        r = int(r)
+        if r in seen:
+            continue
+        seen.add(r)
+        b = r // I
+        if index[b] < 0:
+            index[b] = r - b * I
+        else:
+            dropped.append(r)
+    return index, dropped
+
+
+def pbr_answer(bin_keys, T: np.ndarray, log_i: int, threads: int = 1) -> np.ndarray:
+    """Server side of PBR: bin b's keys (each over the I-row domain
+    of the bin) answered against the bin's rows T[bI : bI + I] exactly as a
+    plain PIR query on that small table (answer_batch).  Returns
+    shares[n_bins][B][D] (every bin carries the same B keys per client batch)."""
+    T = np.ascontiguousarray(T, np.uint32)
+    N, D = T.shape
+    I = 1 << log_i
+    nb = pbr_n_bins(N, log_i)
+    assert len(bin_keys) == nb
+    B = len(bin_keys[0])
+    out = np.zeros((nb, B, D), np.uint32)
+    for b in range(nb):
+        assert len(bin_keys[b]) == B and all(k.log_n == log_i for k in bin_keys[b])
+        out[b] = answer_batch(bin_keys[b], T[b * I:(b + 1) * I], 0, threads)
+    return out
