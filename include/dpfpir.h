@@ -306,6 +306,31 @@ size_t dpf_eval_grouped_packed_workspace_bytes(const dpf_eval_group *groups, uin
 int dpf_eval_grouped_packed(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D, uint32_t prf,
                             void *workspace, size_t workspace_bytes, void *stream);
 
+/* ---- partial batch retrieval (PBR; reading R21) ----
+ * Several rows of ONE table per client: the N rows are segmented into
+ * n_bins = ceil(N / I) bins of I = 2^log_i rows (bin b = rows [bI,
+ * min(bI + I, N)), the last bin ragged) and every client sends one ordinary
+ * DPF key per bin over the bin's I-row domain (log_n = log_i; alpha = the
+ * wanted row minus bI, or a dummy index).  A client retrieves up to n_bins
+ * rows for the PRF work of one full-table query (n_bins x (I - 1)
+ * blocks); rows that share a bin beyond the first are dropped by the client
+ * (codesign.PbrPlan), never seen by the server.
+ *   keys_wire : DEVICE, bin-major: the key of client c for bin b at
+ *               keys_wire + (b * B + c) * dpf_key_wire_size_prf(log_i, prf),
+ *               16-B aligned.  Every key has log_n == log_i and this prf.
+ *   table     : DEVICE, the whole table: row-major N x D uint32 (packed = 0),
+ *               or its dpf_table_pack copy with row_begin 0, row_count N
+ *               (packed = 1: tcgen05 contraction; log_i >= 3, >= 5 for ET).
+ *   shares    : DEVICE, n_bins x B x D uint32 (bin-major), overwritten:
+ *               shares[b][c][d] = sum_{j < I, bI + j < N} Eval(k_{b,c}, j) T[bI + j][d].
+ * One launch sequence of dpf_eval_grouped(_packed) with one group per bin.
+ * Asynchronous on `stream`.  Errors: DPF_EINVAL (sizes, alignment, log_i out
+ * of range, more than 2^20 bins), DPF_ENOMEM (workspace), DPF_EUNSUPPORTED
+ * (prf), DPF_ECUDA. */
+size_t dpf_eval_pbr_workspace_bytes(uint32_t B, uint32_t log_i, uint64_t N, uint32_t D, uint32_t prf, int packed);
+int dpf_eval_pbr(const uint8_t *keys_wire, uint32_t B, uint32_t log_i, uint32_t prf, const void *table, int packed,
+                 uint64_t N, uint32_t D, uint32_t *shares, void *workspace, size_t workspace_bytes, void *stream);
+
 /* End-to-end serving call: as dpf_eval_batch_shard, but shares_host is a HOST
  * buffer (pinned for best speed) that receives the B x D answers; the call
  * synchronises `stream` before returning.  The table stays device-resident

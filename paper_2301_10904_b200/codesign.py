@@ -10,6 +10,10 @@ every table's hot and full batches); this module is the client half:
   each hot table and Q_full keys to each full table, padding with dummy
   queries, so the servers learn nothing from the number of keys; rows beyond
   the budget are dropped (the client tolerates dropped queries, P:600, P:658);
+* partial batch retrieval (PBR, reading R21): the table is
+  segmented into bins of I = 2^log_i rows and the client sends one key per
+  bin, so one full-table PRF cost retrieves up to n_bins rows; a bin's second
+  and later wanted rows are dropped, empty bins get dummy keys;
 * reconstruction: the two servers' answers are added mod 2^32.
 
 Pure host logic (numpy); the DPF keys come from libdpfpir's dpf_gen.
@@ -92,3 +96,44 @@ def plan_table(needed_rows: Sequence[int], split: HotSplit, hot_map: dict, q_hot
 def log2_domain(rows: int) -> int:
     """Tree depth for a table of `rows` rows (rows >= 2^n absent, reading R12)."""
     return max(1, int(rows - 1).bit_length())
+
+
+@dataclasses.dataclass
+class PbrPlan:
+    """One client's PBR query to one table: one key per bin."""
+    log_i: int
+    index: np.ndarray    # in-bin index each bin's key targets (dummies included)
+    real: np.ndarray     # bool per bin: a wanted row (else a dummy)
+    rows: np.ndarray     # table row retrieved per bin (-1 for dummies)
+    dropped: np.ndarray  # wanted rows lost to bin collisions (request order)
+
+    @property
+    def n_bins(self) -> int:
+        return len(self.index)
+
+
+def pbr_n_bins(n_rows: int, log_i: int) -> int:
+    """ceil(L / I): the last bin is ragged when I does not divide L."""
+    return -(-n_rows >> log_i)
+
+
+def plan_pbr(needed_rows: Sequence[int], n_rows: int, log_i: int, rng: np.random.Generator) -> PbrPlan:
+    """Bin each wanted row (bin = row >> log_i); per bin keep the first wanted
+    row in request order (repeats of a row count once), drop the others; bins
+    with no wanted row get a uniformly random dummy index."""
+    rows = np.asarray(needed_rows, dtype=np.int64).ravel()
+    nb = pbr_n_bins(n_rows, log_i)
+    _, first = np.unique(rows, return_index=True)
+    uniq = rows[np.sort(first)]                       # distinct rows, request order
+    bins = uniq >> log_i
+    _, keep_at = np.unique(bins, return_index=True)   # first wanted row of each hit bin
+    keep = np.zeros(len(uniq), bool)
+    keep[keep_at] = True
+    index = rng.integers(0, 1 << log_i, size=nb, dtype=np.int64)
+    real = np.zeros(nb, bool)
+    out_rows = np.full(nb, -1, np.int64)
+    kb = bins[keep]
+    index[kb] = uniq[keep] - (kb << log_i)
+    real[kb] = True
+    out_rows[kb] = uniq[keep]
+    return PbrPlan(log_i, index, real, out_rows, uniq[~keep])

@@ -271,7 +271,32 @@ struct Smem {
 // lane + 32*(cg*CPL + c), c < CPL.  y read as broadcast (same word for all
 // lanes), T read coalesced.  No column guard in the loop: columns >= D read
 // padding/next-row words whose products are never flushed.
-template <int KPW, int CPL>
+template <int KPW>
+__device__ __forceinline__ void load_y(const uint32_t *__restrict__ yp, uint32_t (&yv)[KPW]) {
+  if constexpr (KPW % 4 == 0) {
+#pragma unroll
+    for (int k = 0; k < KPW; k += 4) {
+      const uint4 v = *reinterpret_cast<const uint4 *>(yp + k);
+      yv[k] = v.x; yv[k + 1] = v.y; yv[k + 2] = v.z; yv[k + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < KPW; ++k) yv[k] = yp[k];
+  }
+}
+
+// Slots processed per main-loop step: the step's LDS are all issued before
+// its IMADs (no per-slot trip-count guard between them), so small tiles --
+// the streaming regime, B <= 8, where the contraction is a few IMADs per
+// LDS -- are not LDS-latency-bound.  The 16-producer kernels (80-register
+// cap) and large tiles keep one slot per step: their registers are spoken for.
+template <int KPW, int CPL, int NP>
+__host__ __device__ constexpr int consume_unroll() {
+  return NP >= 16 ? (KPW * CPL >= 16 ? 1 : 2)
+                  : KPW * CPL >= 64 ? 1 : KPW * CPL >= 32 ? 2 : KPW * CPL >= 16 ? 4 : 8;
+}
+
+template <int KPW, int CPL, int NP>
 __device__ __forceinline__ void consume_window(const uint32_t *__restrict__ yb, const uint32_t *__restrict__ tb,
                                                uint32_t nslots, uint32_t Kt, uint32_t D, uint32_t key0,
                                                uint32_t colbase, uint32_t s0, uint32_t sstep,
@@ -281,22 +306,34 @@ __device__ __forceinline__ void consume_window(const uint32_t *__restrict__ yb, 
   const uint32_t *yp = yb + key0 + s0 * Kt;
   const uint32_t *tp = tb + colbase + s0 * D;
   const uint32_t ystep = sstep * Kt, tstep = sstep * D;
+  constexpr int U = consume_unroll<KPW, CPL, NP>();
+  uint32_t s = s0;
+  if constexpr (U > 1) {
+    for (; s + (U - 1) * sstep < nslots; s += U * sstep) {
+      uint32_t tv[U][CPL], yv[U][KPW];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) tv[u][c] = tp[u * tstep + 32 * c];
+        load_y<KPW>(yp + u * ystep, yv[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < KPW; ++k)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) acc[k][c] += yv[u][k] * tv[u][c];
+      yp += U * ystep;
+      tp += U * tstep;
+    }
+  }
 #pragma unroll 4
-  for (uint32_t s = s0; s < nslots; s += sstep) {
+  for (; s < nslots; s += sstep) {
     uint32_t tv[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) tv[c] = tp[32 * c];
     uint32_t yv[KPW];
-    if constexpr (KPW % 4 == 0) {
-#pragma unroll
-      for (int k = 0; k < KPW; k += 4) {
-        const uint4 v = *reinterpret_cast<const uint4 *>(yp + k);
-        yv[k] = v.x; yv[k + 1] = v.y; yv[k + 2] = v.z; yv[k + 3] = v.w;
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < KPW; ++k) yv[k] = yp[k];
-    }
+    load_y<KPW>(yp, yv);
 #pragma unroll
     for (int k = 0; k < KPW; ++k)
 #pragma unroll
@@ -450,7 +487,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
     for (int k = 0; k < KPW; ++k)
 #pragma unroll
       for (int c = 0; c < CPL; ++c) acc[k][c] = 0;
-    uint32_t wseq = 0, tseq = 0;
+    uint32_t wseq = 0, ts = 0, tph = 0;  // T ring slot and phase (no division per chunk)
     const uint32_t seg = p.R;  // rows per node per window
     for (uint32_t item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       const GroupDesc g = group_of(p, item);
@@ -459,14 +496,17 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
         const uint32_t stage = wseq & 1;
         named_sync(1 + stage, kFullThreads);
         const uint32_t *yb = ybuf + stage * p.y_stage_words;
-        for (uint32_t ch = 0; ch < p.n_chunks; ++ch, ++tseq) {
-          const uint32_t ts = tseq % p.NST, tuse = tseq / p.NST;
+        for (uint32_t ch = 0; ch < p.n_chunks; ++ch) {
           const uint32_t n0 = ch * p.CN, nn = min(p.CN, p.Ft - n0);
-          mbar_wait(&tfull[ts], tuse & 1);
+          mbar_wait(&tfull[ts], tph);
           if (active)
-            consume_window<KPW, CPL>(yb + n0 * seg * p.Kt, tbuf + ts * p.t_stage_words, nn * seg, p.Kt, p.D, key0,
+            consume_window<KPW, CPL, NP>(yb + n0 * seg * p.Kt, tbuf + ts * p.t_stage_words, nn * seg, p.Kt, p.D, key0,
                                      colbase, sg, p.SG, acc);
           mbar_arrive(&tempty[ts]);  // one warp instruction; each lane orders its own reads
+          if (++ts == p.NST) {
+            ts = 0;
+            tph ^= 1;
+          }
         }
         if (wseq + 2 < total_w) named_arrive(3 + stage, kEmptyThreads);
       }
@@ -492,7 +532,8 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
     // ------------------------------------------------------------ T loader
     // T ring of (window, node chunk) entries: CN nodes x 2W rows, one
     // cp.async.bulk per node segment, decoupled from the y ring.
-    uint32_t tseq = 0;
+    uint32_t ts = 0, tph = 0;  // ring slot, and the parity of its previous use
+    bool wrapped = false;      // every slot used once: wait for the consumers' release
     const uint64_t seg_rows = p.R;
     const uint32_t row_bytes = p.D * 4;
     constexpr uint32_t V = Prf::kEt ? 4u : 0u;
@@ -500,10 +541,15 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
       const GroupDesc g = group_of(p, item);
       const uint32_t ng = (item - g.item_base) / g.n_ktiles;
       for (uint32_t win = 0; win < g.nwin; ++win) {
-        for (uint32_t ch = 0; ch < p.n_chunks; ++ch, ++tseq) {
-          const uint32_t ts = tseq % p.NST, tuse = tseq / p.NST;
-          if (tuse > 0) mbar_wait(&tempty[ts], (tuse - 1) & 1);
-          uint32_t *tb = tbuf + ts * p.t_stage_words;
+        for (uint32_t ch = 0; ch < p.n_chunks; ++ch) {
+          const uint32_t cur = ts;
+          if (wrapped) mbar_wait(&tempty[cur], tph ^ 1);
+          if (++ts == p.NST) {
+            ts = 0;
+            tph ^= 1;
+            wrapped = true;
+          }
+          uint32_t *tb = tbuf + cur * p.t_stage_words;
           const uint32_t n0 = ch * p.CN, n1 = min(p.Ft, n0 + p.CN);
           if (g.nwin == 1) {
             // one window covers whole subtrees: the chunk's rows are contiguous
@@ -516,8 +562,8 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
             const uint64_t a = s0 > g.r0 ? s0 : g.r0, e = s1 < g.r1 ? s1 : g.r1;
             const uint32_t bytes = a < e ? uint32_t(e - a) * row_bytes : 0u;
             if (lane == 0) {
-              mbar_arrive_expect_tx(&tfull[ts], bytes);
-              if (bytes) bulk_g2s(tb + (a - s0) * p.D, g.T + (a - g.r0) * p.D, bytes, &tfull[ts]);
+              mbar_arrive_expect_tx(&tfull[cur], bytes);
+              if (bytes) bulk_g2s(tb + (a - s0) * p.D, g.T + (a - g.r0) * p.D, bytes, &tfull[cur]);
             }
             __syncwarp();
             continue;
@@ -531,7 +577,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
             if (a < e) my_bytes += uint32_t(e - a) * row_bytes;
           }
           const uint32_t total = __reduce_add_sync(0xFFFFFFFFu, my_bytes);
-          if (lane == 0) mbar_arrive_expect_tx(&tfull[ts], total);
+          if (lane == 0) mbar_arrive_expect_tx(&tfull[cur], total);
           __syncwarp();
           for (uint32_t nl = n0 + lane; nl < n1; nl += 32) {
             const uint64_t node = uint64_t(ng) * p.Ft + nl;
@@ -540,7 +586,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
             const uint64_t a = s0 > g.r0 ? s0 : g.r0, e = (s0 + seg_rows) < g.r1 ? (s0 + seg_rows) : g.r1;
             if (a < e)
               bulk_g2s(tb + (uint64_t(nl - n0) * seg_rows + (a - s0)) * p.D, g.T + (a - g.r0) * p.D,
-                       uint32_t(e - a) * row_bytes, &tfull[ts]);
+                       uint32_t(e - a) * row_bytes, &tfull[cur]);
           }
         }
       }
@@ -2177,3 +2223,63 @@ int eval_grouped_impl(const dpf_eval_group *groups, uint32_t n_groups, uint32_t 
 
 }  // namespace
 }  // namespace dpfpir
+
+// ------------------------------------------------------------- PBR (row f2)
+// Partial batch retrieval (reading R21): one group per bin of
+// I = 2^log_i rows, every group a view of the table at row bI (row-major:
+// + bI D words; packed: + bI/8 blocks of 32 Dp bytes, I >= 8 keeps bins on
+// whole 8-row blocks), run through the grouped launch sequence.
+namespace dpfpir {
+namespace {
+
+int make_pbr_groups(const uint8_t *keys, uint32_t B, uint32_t log_i, uint32_t prf, const void *table, int packed,
+                    uint64_t N, uint32_t D, uint32_t *shares, std::vector<dpf_eval_group> &gs) {
+  if (!keys || !table || !shares || B == 0 || N == 0 || D == 0 || log_i < 1 || log_i > DPF_MAX_LOG_N)
+    return DPF_EINVAL;
+  if (packed && log_i < 3) return DPF_EINVAL;
+  const size_t ks = dpf_key_wire_size_prf(log_i, prf);
+  if (ks == 0) return DPF_EINVAL;
+  const uint64_t I = 1ull << log_i;
+  const uint64_t nb = (N + I - 1) >> log_i;
+  if (nb > (1ull << 20)) return DPF_EINVAL;
+  const uint64_t Dp = (D + 127) & ~127u;
+  gs.assign(nb, dpf_eval_group{});
+  for (uint64_t b = 0; b < nb; ++b) {
+    dpf_eval_group &g = gs[b];
+    g.keys_wire = keys + b * B * ks;
+    g.B = B;
+    g.log_n = log_i;
+    g.row_begin = 0;
+    g.row_count = std::min<uint64_t>(I, N - b * I);
+    g.table = packed ? reinterpret_cast<const uint32_t *>(static_cast<const uint8_t *>(table) + (b * I / 8) * 32 * Dp)
+                     : static_cast<const uint32_t *>(table) + b * I * D;
+    g.shares = shares + b * B * D;
+  }
+  return DPF_OK;
+}
+
+}  // namespace
+}  // namespace dpfpir
+
+extern "C" size_t dpf_eval_pbr_workspace_bytes(uint32_t B, uint32_t log_i, uint64_t N, uint32_t D, uint32_t prf,
+                                               int packed) {
+  // plan on placeholder (aligned, non-null) addresses: sizes depend only on shapes
+  std::vector<dpf_eval_group> gs;
+  const uintptr_t fake = 1u << 12;
+  if (dpfpir::make_pbr_groups(reinterpret_cast<const uint8_t *>(fake), B, log_i, prf,
+                              reinterpret_cast<const void *>(fake), packed, N, D, reinterpret_cast<uint32_t *>(fake),
+                              gs) != DPF_OK)
+    return 0;
+  return packed ? dpf_eval_grouped_packed_workspace_bytes(gs.data(), uint32_t(gs.size()), D, prf)
+                : dpf_eval_grouped_workspace_bytes(gs.data(), uint32_t(gs.size()), D, prf);
+}
+
+extern "C" int dpf_eval_pbr(const uint8_t *keys_wire, uint32_t B, uint32_t log_i, uint32_t prf, const void *table,
+                            int packed, uint64_t N, uint32_t D, uint32_t *shares, void *workspace,
+                            size_t workspace_bytes, void *stream) {
+  std::vector<dpf_eval_group> gs;
+  int rc = dpfpir::make_pbr_groups(keys_wire, B, log_i, prf, table, packed, N, D, shares, gs);
+  if (rc != DPF_OK) return rc;
+  return packed ? dpf_eval_grouped_packed(gs.data(), uint32_t(gs.size()), D, prf, workspace, workspace_bytes, stream)
+                : dpf_eval_grouped(gs.data(), uint32_t(gs.size()), D, prf, workspace, workspace_bytes, stream);
+}

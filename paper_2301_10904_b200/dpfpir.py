@@ -107,6 +107,9 @@ def lib() -> ctypes.CDLL:
     L.dpf_eval_grouped_packed_workspace_bytes.argtypes = [vp, u32, u32, u32]
     L.dpf_eval_grouped_packed_workspace_bytes.restype = sz
     L.dpf_eval_grouped_packed.argtypes = [vp, u32, u32, u32, vp, sz, vp]
+    L.dpf_eval_pbr_workspace_bytes.argtypes = [u32, u32, u64, u32, u32, ctypes.c_int]
+    L.dpf_eval_pbr_workspace_bytes.restype = sz
+    L.dpf_eval_pbr.argtypes = [vp, u32, u32, u32, vp, ctypes.c_int, u64, u32, vp, vp, sz, vp]
     L.dpf_last_eval_stats.argtypes = [vp]
     L.dpf_eval_plan.argtypes = [u32, u32, u32, u64, u64, u32, ctypes.c_int, vp]
     L.dpf_kernel_timer_begin.argtypes = [u32]
@@ -125,6 +128,7 @@ EXPORTED_SYMBOLS = ("dpf_gen", "dpf_key_wire_size", "dpf_key_wire_size_prf", "dp
                     "dpf_table_packed_bytes", "dpf_table_pack", "dpf_eval_batch_packed", "dpf_eval_batch_wire_packed",
                     "dpf_eval_grouped_workspace_bytes", "dpf_eval_grouped",
                     "dpf_eval_grouped_packed_workspace_bytes", "dpf_eval_grouped_packed",
+                    "dpf_eval_pbr_workspace_bytes", "dpf_eval_pbr",
                     "dpf_eval_batch_wire_ex", "dpf_ipc_export", "dpf_ipc_open", "dpf_ipc_close",
                     "dpf_server_workspace_bytes", "dpf_server_create", "dpf_server_run", "dpf_server_destroy",
                     "dpf_kernel_timer_read", "dpf_strerror", "dpf_version")
@@ -516,6 +520,40 @@ def eval_grouped_packed(groups, D: int, prf: int = DPF_PRF_CHACHA20, workspace=N
     _check(lib().dpf_eval_grouped_packed(arr, len(groups), D, prf, ws.data_ptr(), ws.numel() * ws.element_size(),
                                          _stream_ptr(stream)), "dpf_eval_grouped_packed")
     return [g[4] for g in groups]
+
+
+def eval_pbr_workspace_bytes(B: int, log_i: int, N: int, D: int, prf: int = DPF_PRF_CHACHA20,
+                             packed: bool = False) -> int:
+    return lib().dpf_eval_pbr_workspace_bytes(B, log_i, N, D, prf, int(packed))
+
+
+def eval_pbr(keys_wire_dev, B: int, log_i: int, table, out=None, workspace=None, stream=None,
+             prf: int = DPF_PRF_CHACHA20):
+    """dpf_eval_pbr (partial batch retrieval): keys_wire_dev uint8
+    [n_bins * B, wire bytes] bin-major (client c's key for bin b at row b*B + c),
+    `table` the whole row-major CUDA table [N, D] or its PackedTable (row_begin 0).
+    Returns shares int32 [n_bins, B, D]."""
+    import torch
+    packed = isinstance(table, PackedTable)
+    if packed:
+        if table.row_begin != 0:
+            raise ValueError("PBR needs the packed copy of the whole table (row_begin 0)")
+        N, D, ptr, dev = table.row_count, table.D, table.data.data_ptr(), table.data.device
+    else:
+        _check_table(table)
+        (N, D), ptr, dev = table.shape, table.data_ptr(), table.device
+    nb = (N + (1 << log_i) - 1) >> log_i
+    if keys_wire_dev.shape[0] != nb * B:
+        raise ValueError("expected %d bin-major keys, got %d" % (nb * B, keys_wire_dev.shape[0]))
+    if out is None:
+        out = torch.empty((nb, B, D), dtype=torch.int32, device=dev)
+    need = eval_pbr_workspace_bytes(B, log_i, N, D, prf, packed)
+    if need == 0:
+        raise DpfError(DPF_EINVAL, "dpf_eval_pbr_workspace_bytes")
+    ws = workspace if workspace is not None else _workspace(need, dev, stream)
+    _check(lib().dpf_eval_pbr(keys_wire_dev.data_ptr(), B, log_i, prf, ptr, int(packed), N, D, out.data_ptr(),
+                              ws.data_ptr(), ws.numel() * ws.element_size(), _stream_ptr(stream)), "dpf_eval_pbr")
+    return out
 
 
 def serve_workspace_bytes(B: int, log_n: int, rows: int, D: int) -> int:

@@ -59,3 +59,19 @@ def test_end_to_end_reconstruction_with_oracle_servers(oracle):
                 got = oracle.reconstruct(a0, a1)
                 for q in np.nonzero(real)[0]:
                     np.testing.assert_array_equal(got[q], T[rows_of[q]])
+
+
+def test_pbr_planner_matches_oracle_rule(oracle):
+    """The product's client PBR planner (vectorised) keeps and drops exactly
+    the rows the oracle's loop (R21) does."""
+    rng = np.random.default_rng(3)
+    for N, log_i, need in ((1 << 12, 8, 30), (1 << 12, 10, 6), (5000, 9, 40), (1 << 10, 10, 3)):
+        for row in synth.codesign_needed(1, N, 20, need):
+            pp = codesign.plan_pbr(row, N, log_i, rng)
+            index, dropped = oracle.pbr_plan(row, N, log_i)
+            assert pp.n_bins == len(index) == codesign.pbr_n_bins(N, log_i)
+            np.testing.assert_array_equal(pp.real, np.array(index) >= 0)
+            np.testing.assert_array_equal(pp.index[pp.real], np.array(index)[pp.real])
+            np.testing.assert_array_equal(pp.dropped, dropped)
+            assert pp.index.min() >= 0 and pp.index.max() < (1 << log_i)
+            np.testing.assert_array_equal(pp.rows[pp.real], (np.nonzero(pp.real)[0] << log_i) + pp.index[pp.real])
