@@ -123,6 +123,14 @@ __device__ __forceinline__ void red_add_u32(uint32_t *addr, uint32_t v, uint32_t
     asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(addr), "r"(v) : "memory");
 }
 
+// Programmatic dependent launch (PDL): the top BFS lets the fused kernel
+// launch as soon as all of its CTAs are running (launch_dependents); the
+// fused kernel sets up its barriers / TMEM / DFS state and then waits for the
+// top BFS grid to complete and its frontier writes (and the answer zeroing)
+// to be visible (griddepcontrol.wait; a no-op without a PDL primary).
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait_primary() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // Wire-format key accessors (include/dpfpir.h).
 __device__ __forceinline__ uint4 key_root(const uint8_t *k) { return __ldg(reinterpret_cast<const uint4 *>(k + 16)); }
 __device__ __forceinline__ uint32_t key_cw_out(const uint8_t *k) {
@@ -156,6 +164,7 @@ __global__ void __launch_bounds__(256) expand_top_split_kernel(const uint8_t *__
                                                                uint64_t r1, uint4 *__restrict__ out, uint64_t cap,
                                                                uint4 *__restrict__ zero, uint64_t zero_vec) {
   __shared__ uint4 buf[2][1u << kTopSmemLevels];
+  pdl_launch_dependents();
   // a7's zeroing of the answers rides along (saves a launch per step)
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < zero_vec; i += uint64_t(gridDim.x) * blockDim.x)
     zero[i] = make_uint4(0, 0, 0, 0);
@@ -366,6 +375,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  pdl_wait_primary();  // the top BFS' frontier and zeroed answers
 
   if (warp < NP) {
     // ------------------------------------------------------------ producers
@@ -1186,6 +1196,15 @@ thread_local Staging g_staging;
 
 // The tcgen05 fused kernel (single CTAs or CTA pairs) for a plan, timed by
 // the optional kernel timer.  Used by single-table and grouped launches.
+// PDL between the top BFS and the fused kernel; DPF_PDL=0 disables (A/B).
+bool use_pdl() {
+  static const bool on = [] {
+    const char *e = getenv("DPF_PDL");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 int launch_tc_kernel(const Plan &pl, const dev::FusedParams &p, cudaStream_t st) {
   const bool timed = g_timer.on && 2 * g_timer.used + 1 < g_timer.ev.size();
   dev::TcParams tp;
@@ -1232,13 +1251,17 @@ int launch_tc_kernel(const Plan &pl, const dev::FusedParams &p, cudaStream_t st)
   cfg.blockDim = dim3(32 * (kTcNP + dev::tc_extra_warps(epip)));
   cfg.dynamicSmemBytes = pl.smem_bytes;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = pl.pair ? 2 : 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  // PDL behind the top BFS (with the kernel timer on, its start event sits
+  // between the two launches: any early start counts in the kernel's time)
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = use_pdl();
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
   if (cudaLaunchKernelEx(&cfg, fn, tp) != cudaSuccess) return DPF_ECUDA;
   if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used++ + 1], st);
@@ -1333,7 +1356,20 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
   if (cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.smem_bytes)) != cudaSuccess)
     return DPF_ECUDA;
   if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used], st);
-  kfn<<<pl.grid, 32 * (pl.kc.NP + kNC + 1), pl.smem_bytes, st>>>(p);
+  {
+    cudaLaunchConfig_t cfg;
+    std::memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3(pl.grid);
+    cfg.blockDim = dim3(32 * (pl.kc.NP + kNC + 1));
+    cfg.dynamicSmemBytes = pl.smem_bytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = use_pdl();
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kfn, p) != cudaSuccess) return DPF_ECUDA;
+  }
   if (timed) cudaEventRecord(g_timer.ev[2 * g_timer.used++ + 1], st);
   ++nk;
   if (cudaGetLastError() != cudaSuccess) return DPF_ECUDA;

@@ -285,6 +285,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
   __syncthreads();
   if constexpr (PAIR) cluster_sync_all();  // both CTAs' barriers initialised before any remote arrive
   tc_fence_after();
+  pdl_wait_primary();  // PDL: the top BFS' frontier and zeroed answers are complete and visible
   // work items: one per CTA, or one per CTA pair
   const uint32_t first = PAIR ? blockIdx.x >> 1 : blockIdx.x;
   const uint32_t stride = PAIR ? gridDim.x >> 1 : gridDim.x;

@@ -31,6 +31,10 @@ ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--check", type=int, default=2, help="inferences whose rows are reconstructed and checked")
 ap.add_argument("--prf", default="chacha20", choices=["chacha20", "chacha20_et"])
 ap.add_argument("--packed", action="store_true", help="limb-packed tables + tcgen05 (dpf_eval_grouped_packed)")
+ap.add_argument("--scheme", default="hot", choices=["hot", "pbr"],
+                help="hot: hot-table split, Q_hot + Q_full keys per table (P:645-659); "
+                     "pbr: partial batch retrieval, one key per bin of each full table (P:595-602)")
+ap.add_argument("--bins", type=int, default=4, help="PBR bins per table (power of two)")
 a = ap.parse_args()
 prf = dpfpir.DPF_PRF_CHACHA20_ET if a.prf == "chacha20_et" else dpfpir.DPF_PRF_CHACHA20
 D = synth.CODESIGN_D
@@ -55,6 +59,25 @@ for Binf in a.batches:
     dropped = 0
     for t, tb in enumerate(tables):
         need = synth.codesign_needed(t, tb["N"], Binf, a.need)
+        if a.scheme == "pbr":
+            # one group per bin: the keys of all inferences for that bin
+            log_i = tb["nF"] - (a.bins.bit_length() - 1)
+            I = 1 << log_i
+            pplans = [codesign.plan_pbr(r, tb["N"], log_i, rng) for r in need]
+            dropped += sum(len(p.dropped) for p in pplans)
+            for b in range(codesign.pbr_n_bins(tb["N"], log_i)):
+                pairs = [dpfpir.gen(log_i, int(p.index[b]), 1, next(seed_iter), prf=prf) for p in pplans]
+                if a.packed:
+                    Dp = (D + 127) // 128 * 128
+                    view = dpfpir.PackedTable(tb["Td"].data[(b * I // 8) * 32 * Dp:((b + 1) * I // 8) * 32 * Dp], 0, I, D)
+                else:
+                    view = tb["Td"][b * I:(b + 1) * I]
+                for party, gl in ((0, groups0), (1, groups1)):
+                    wire = torch.from_numpy(dpfpir.keys_to_wire([p[party] for p in pairs])).cuda()
+                    out = torch.empty((len(pairs), D), dtype=torch.int32, device="cuda")
+                    gl.append((wire, log_i, view, 0, out))
+                real.append((t, "pbr", [(p.real[b], p.rows[b]) for p in pplans]))
+            continue
         plans = [codesign.plan_table(r, tb["split"], tb["hmap"], a.q_hot, a.q_full, rng) for r in need]
         dropped += sum(p.dropped for p in plans)
         for kind, tbl, n, idxs in (("hot", tb["Hd"], tb["nH"], [p.hot_idx for p in plans]),
@@ -102,6 +125,12 @@ for Binf in a.batches:
     ok = True
     for gi, (t, kind, plans) in enumerate(real):
         ans = dpfpir.reconstruct(dpfpir.as_u32(groups0[gi][4]), dpfpir.as_u32(groups1[gi][4]))
+        if kind == "pbr":
+            for inf in range(min(a.check, Binf)):
+                is_real, row = plans[inf]
+                if is_real:
+                    ok &= bool(np.array_equal(ans[inf], tables[t]["T"][row]))
+            continue
         q = a.q_hot if kind == "hot" else a.q_full
         for inf in range(min(a.check, Binf)):
             p = plans[inf]
@@ -112,10 +141,12 @@ for Binf in a.batches:
     # blocks over each table's rows: N - 1 per key (R9), N/8 - 1 with early termination (R20)
     blocks = sum(g[0].shape[0] * ((g[2].shape[0] - 1) if prf == dpfpir.DPF_PRF_CHACHA20 else max(1, g[2].shape[0] // 8 - 1))
                  for g in groups0)
+    n_rows_wanted = Binf * len(tables) * a.need
     ms = res["grouped"]
-    print(json.dumps({"workload": "c5 co-design", "prf": a.prf, "packed": a.packed, "inferences_per_batch": Binf, "keys_per_batch": n_keys,
+    print(json.dumps({"workload": "c5 co-design", "scheme": a.scheme, "bins": a.bins if a.scheme == "pbr" else None,
+                      "prf": a.prf, "packed": a.packed, "inferences_per_batch": Binf, "keys_per_batch": n_keys,
                       "q_hot": a.q_hot, "q_full": a.q_full, "hot_fraction": a.hot, "need_per_table": a.need,
-                      "dropped_rows": dropped, "ms_grouped": round(ms, 4), "ms_separate": round(res["separate"], 4),
+                      "dropped_rows": dropped, "wanted_rows": n_rows_wanted, "ms_grouped": round(ms, 4), "ms_separate": round(res["separate"], 4),
                       "inferences_per_s": round(Binf / (ms * 1e-3), 1), "dpf_queries_per_s": round(n_keys / (ms * 1e-3)),
                       "alu_frac": round(640 * blocks / (ms * 1e-3) / (148 * 64 * 1965e6), 3),
                       "rows_reconstructed_ok": ok, "plan": plan}), flush=True)
