@@ -39,6 +39,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import re
 import os
 import socket
 import statistics
@@ -653,10 +654,13 @@ def roofline_of(args, w, rows, g, G, stats, kernel_ms, ms_per_step, value, use_p
     tree_blocks = (rows - 1 + g) if not v else (2 * (rows >> v) - 1 + g)
     qps_roof = min(alu_peak / (ops_per_block * tree_blocks),
                    w.B / max(bounds["tensor"], bounds["hbm"], 1e-30))
-    traffic = _ncu_traffic(w.name if args.prf == "chacha20" else "%s_%s" % (w.name, args.prf))
+    timed_kernel = dpfpir.kernel_name(stats.get("kernel_id", 0))
+    traffic, traffic_kernel = _ncu_traffic(w.name if args.prf == "chacha20" else "%s_%s" % (w.name, args.prf))
+    if traffic is not None and traffic_kernel != timed_kernel:
+        traffic = None  # the capture is of another kernel instantiation than the one just timed
     return {
         "bound": bound, "achieved": achieved * scale, "peak": peak * scale, "unit": unit,
-        "frac": achieved / peak, "traffic": traffic,
+        "frac": achieved / peak, "traffic": traffic, "traffic_kernel": traffic_kernel, "timed_kernel": timed_kernel,
         "bounds_ms": {k: v_ * 1e3 for k, v_ in bounds.items()},
         "kernel": "fused_eval_tc_kernel" if use_packed else "fused_eval_kernel", "kernel_ms": kern_avg_ms,
         "kernel_share_of_step": kern_avg_ms / ms_per_step,
@@ -682,15 +686,21 @@ def _nvsmi_index(local_rank: int) -> int:
 
 
 def _ncu_traffic(config_name: str):
-    """DRAM bytes per fused launch from the committed ncu --set full capture
-    (profiles/ncu_traffic.json), or None."""
+    """(DRAM bytes per fused launch, captured kernel template) from the
+    committed ncu --set full capture (profiles/ncu_traffic.json), or (None,
+    None).  The caller drops the bytes when the template differs from the
+    kernel the run just timed."""
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d.get(config_name, {}).get("dram_bytes_per_launch")
+            e = json.load(f).get(config_name, {})
     except (OSError, ValueError):
-        return None
+        return None, None
+    kern = e.get("kernel")
+    if kern:  # ncu prints "void ns::fused_eval_tc_kernel<ns::PrfChacha, 16, 3, 4, 1, 0>(ns::TcParams)"
+        kern = re.sub(r"\(.*$", "", kern.replace("void ", "").replace("dpfpir::dev::", "").replace("dpfpir::", "")).strip()
+        kern = kern.replace("true", "1").replace("false", "0")
+    return e.get("dram_bytes_per_launch"), kern
 
 
 if __name__ == "__main__":

@@ -1168,6 +1168,18 @@ size_t layout(const Plan &pl, uint32_t B, size_t kstride, Workspace *ws, void *b
 
 thread_local dpf_eval_stats g_stats{};
 
+// dpf_eval_stats.kernel_id: which fused-kernel instantiation a plan launches
+// (include/dpfpir.h): bit 0 tcgen05, bit 1 CTA pair, bit 2 producer epilogue,
+// bits 4-7 y-ring stages, bits 8-11 PRF, bits 12-17 producer warps, bits
+// 18-23 consumer keys per warp (IMAD), bits 24-31 consumer column words (IMAD).
+uint32_t kernel_id(const Plan &pl) {
+  if (pl.tc) {
+    const uint32_t epip = pl.prf == DPF_PRF_CHACHA20_ET;
+    return 1u | (uint32_t(pl.pair) << 1) | (epip << 2) | (pl.nsy << 4) | (pl.prf << 8) | (16u << 12);
+  }
+  return (pl.prf << 8) | (uint32_t(pl.kc.NP) << 12) | (uint32_t(pl.kc.KPW) << 18) | (uint32_t(pl.kc.CPL) << 24);
+}
+
 // Optional per-launch timing of the fused kernel (bench instrumentation).
 struct KernelTimer {
   std::vector<cudaEvent_t> ev;
@@ -1466,6 +1478,7 @@ int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uin
   g_stats.nodes_per_tile = pl.Ft;
   g_stats.work_items = pl.n_items;
   g_stats.grid = pl.grid;
+  g_stats.kernel_id = kernel_id(pl);
   return DPF_OK;
 }
 
@@ -1518,6 +1531,7 @@ extern "C" int dpf_eval_plan(uint32_t B, uint32_t log_n, uint32_t prf, uint64_t 
   out->nodes_per_tile = pl.Ft;
   out->work_items = pl.n_items;
   out->grid = pl.grid;
+  out->kernel_id = kernel_id(pl);
   return DPF_OK;
 }
 
@@ -2254,6 +2268,7 @@ int eval_grouped_impl(const dpf_eval_group *groups, uint32_t n_groups, uint32_t 
   g_stats.nodes_per_tile = pl.Ft;
   g_stats.work_items = pl.n_items;
   g_stats.grid = pl.grid;
+  g_stats.kernel_id = kernel_id(pl);
   return DPF_OK;
 }
 

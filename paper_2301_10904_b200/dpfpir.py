@@ -47,7 +47,7 @@ class DpfKey(ctypes.Structure):
 class DpfEvalStats(ctypes.Structure):
     _fields_ = [("prf_blocks", ctypes.c_uint64), ("kernels", ctypes.c_uint32), ("frontier_depth", ctypes.c_uint32),
                 ("keys_per_tile", ctypes.c_uint32), ("nodes_per_tile", ctypes.c_uint32),
-                ("work_items", ctypes.c_uint32), ("grid", ctypes.c_uint32)]
+                ("work_items", ctypes.c_uint32), ("grid", ctypes.c_uint32), ("kernel_id", ctypes.c_uint32)]
 
 
 class DpfEvalGroup(ctypes.Structure):
@@ -595,6 +595,18 @@ def last_eval_stats() -> dict:
     s = DpfEvalStats()
     _check(lib().dpf_last_eval_stats(ctypes.byref(s)), "dpf_last_eval_stats")
     return {f: getattr(s, f) for f, _ in DpfEvalStats._fields_}
+
+
+def kernel_name(kernel_id: int) -> str:
+    """The fused-kernel template a plan launches (dpf_eval_stats.kernel_id), in
+    the form ncu prints it (namespaces dropped)."""
+    prf = {DPF_PRF_CHACHA20: "PrfChacha", DPF_PRF_AES128: "PrfAesBs", DPF_PRF_CHACHA20_ET: "PrfChachaEt"}.get(
+        (kernel_id >> 8) & 0xF, "?")
+    np_ = (kernel_id >> 12) & 0x3F
+    if kernel_id & 1:
+        return "fused_eval_tc_kernel<%s, %d, %d, 4, %d, %d>" % (prf, np_, (kernel_id >> 4) & 0xF, (kernel_id >> 1) & 1,
+                                                                 (kernel_id >> 2) & 1)
+    return "fused_eval_kernel<%s, %d, 4, %d, %d>" % (prf, np_, (kernel_id >> 18) & 0x3F, kernel_id >> 24)
 
 
 def eval_plan(B: int, log_n: int, rows: int, D: int, prf: int = DPF_PRF_CHACHA20, row_begin: int = 0,
