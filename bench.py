@@ -654,6 +654,7 @@ def roofline_of(args, w, rows, g, G, stats, kernel_ms, ms_per_step, value, use_p
     tree_blocks = (rows - 1 + g) if not v else (2 * (rows >> v) - 1 + g)
     qps_roof = min(alu_peak / (ops_per_block * tree_blocks),
                    w.B / max(bounds["tensor"], bounds["hbm"], 1e-30))
+    from paper_2301_10904_b200 import dpfpir
     timed_kernel = dpfpir.kernel_name(stats.get("kernel_id", 0))
     traffic, traffic_kernel = _ncu_traffic(w.name if args.prf == "chacha20" else "%s_%s" % (w.name, args.prf))
     if traffic is not None and traffic_kernel != timed_kernel:

@@ -1524,6 +1524,7 @@ extern "C" int dpf_eval_plan(uint32_t B, uint32_t log_n, uint32_t prf, uint64_t 
   const int rc = packed ? make_tc_plan(B, log_n, row_begin, row_count, D, pl, et)
                         : make_plan(B, log_n, row_begin, row_count, D, pl, et);
   if (rc) return rc;
+  pl.prf = prf;
   out->prf_blocks = pl.prf_blocks;
   out->kernels = 0;
   out->frontier_depth = pl.f;

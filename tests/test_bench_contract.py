@@ -112,3 +112,25 @@ def test_aes_circuit_count():
     gates = 10 * 32 * 113 + 9 * 8 * 92 + 11 * 256 + 10 * (4 * 113 + 128) + 16
     assert bench.aes_alu_ops_per_node() == gates / 32
     assert 1600 < bench.ALU_OPS_PER_BLOCK["aes128"] < 1610
+
+
+def test_roofline_of_runs_on_cpu_with_plan_stats():
+    """roofline_of (the bench line's roofline object) from host-only plan
+    stats: it runs without a GPU, names the timed kernel instantiation, and
+    drops the committed ncu traffic when that capture is of another kernel."""
+    import argparse
+    import bench
+    import synth
+    from paper_2301_10904_b200 import dpfpir
+    w = synth.CONFIGS["c3"]
+    stats = dpfpir.eval_plan(w.B, w.log_n, w.N, w.D, packed=True)
+    args = argparse.Namespace(prf="chacha20", config="c3")
+    r = bench.roofline_of(args, w, w.N, 0, 1, stats, [10.0], 10.1, 25000.0, True)
+    assert r["bound"] == "alu" and 0.8 < r["frac"] < 1.0
+    assert r["timed_kernel"] == dpfpir.kernel_name(stats["kernel_id"])
+    assert r["timed_kernel"].startswith("fused_eval_tc_kernel<PrfChacha, 16, ")
+    if r["traffic_kernel"] != r["timed_kernel"]:
+        assert r["traffic"] is None
+    stats["kernel_id"] ^= 2  # claim the other CTA-pair variant: the capture no longer applies
+    r2 = bench.roofline_of(args, w, w.N, 0, 1, stats, [10.0], 10.1, 25000.0, True)
+    assert r2["traffic"] is None
