@@ -239,6 +239,8 @@ struct FusedParams {
   const GroupDesc *groups;   // device array when n_groups > 1 (sorted by item_base)
   uint32_t n_groups, n_items, D;
   uint32_t Kt, Ft, tasks;  // tasks = Kt * Ft <= 32 * NP (lanes >= tasks idle)
+  uint32_t Kr;             // tcgen05: keys per CTA that carry a key (<= Kt = the CTA's MMA columns;
+                           // < Kt for small batches: the other B-operand columns stay zero)
   uint32_t W;              // units per producer thread per window (unit: a leaf pair; ET: a final node)
   uint32_t R;              // table rows per node per window: 2W, or 16W with early termination (R20)
   uint32_t CG, KG, SG;     // consumer col groups / key groups / slot groups
@@ -761,6 +763,7 @@ struct Plan {
   uint32_t tmem_cols, y_stage_bytes, t_stage_bytes;
   uint64_t r0a, packed_rows;
   uint32_t n, m, f, Kt, Ft, tasks, W, CG, KG, SG, n_ktiles, n_items, nwin, grid;
+  uint32_t Kr;  // tcgen05: real keys per CTA (<= Kt)
   uint64_t r0, r1, F, lo_f, cap;
   uint32_t y_stage_words, t_stage_words, CN, n_chunks, NST;
   size_t smem_bytes;
@@ -1045,7 +1048,7 @@ inline uint32_t tc_t_stages(uint32_t) { return 4u; }
 // columns fit the 512 TMEM columns; Ft = 512/Kt frontier nodes per item;
 // W = 4 leaf pairs per node per window (one 8-row packed block).
 int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et,
-                   uint32_t W);
+                   uint32_t W, bool allow_kr = true, bool fallback_padded = true);
 
 // W (leaf pairs per node per window, standard scheme): 8 when the problem is
 // deep enough for subtrees of >= 4 levels (m >= 4 under W = 4), else 4 --
@@ -1071,13 +1074,14 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
     return !(e && atoi(e) == 4);
   }();
   if (!allow8) return rc;
+  // (a wider window must not trade the small-batch key mapping for the padded one)
   Plan p8;
-  if (make_tc_plan_w(B, log_n, r0, rows, D, p8, false, 8) == DPF_OK) pl = p8;
+  if (make_tc_plan_w(B, log_n, r0, rows, D, p8, false, 8, true, pl.Kr == pl.Kt) == DPF_OK) pl = p8;
   return DPF_OK;
 }
 
 int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et,
-                   uint32_t W) {
+                   uint32_t W, bool allow_kr, bool fallback_padded) {
   std::memset(&pl, 0, sizeof pl);
   if (D == 0 || D % 4 || D > 1024 || log_n < 3) return DPF_EINVAL;
   pl.tc = true;
@@ -1105,9 +1109,26 @@ int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint3
   while (Ktp > kmin && Ktp / 2 >= B) Ktp >>= 1;
   pl.Kt = pl.pair ? Ktp / 2 : Ktp;
   pl.nsy = (et && W == 2) ? 2u : tc_y_stages(et);
-  pl.Ft = 32 * kTcNP / pl.Kt;
-  pl.tasks = Ktp * pl.Ft;  // per item (both CTAs of a pair)
-  pl.n_ktiles = (B + Ktp - 1) / Ktp;
+  // Small batches (B < MMA N, single CTA): the MMA keeps N = Kt columns but
+  // only Kr = B of them carry keys -- the producer threads map to (real key,
+  // node), Ft = 512 / Kr nodes per item (a multiple of 4, so a window is
+  // whole 32-leaf K-chunks), and the padding columns stay zero in SMEM.  No
+  // producer lane expands a padding key's tree (before: Kt - B of every Kt
+  // lanes did).  DPF_TC_SMALLB=0 restores the padded mapping (A/B).
+  static const bool smallb = [] {
+    const char *e = getenv("DPF_TC_SMALLB");
+    return !(e && atoi(e) == 0);
+  }();
+  pl.Kr = (!pl.pair && smallb && allow_kr && B < pl.Kt) ? B : pl.Kt;
+  // a Kr-mapped plan whose y ring does not fit falls back to the padded mapping
+  auto fail = [&]() {
+    return (pl.Kr < pl.Kt && fallback_padded) ? make_tc_plan_w(B, log_n, r0, rows, D, pl, et, W, false)
+                                              : DPF_EINVAL;
+  };
+  pl.Ft = pl.Kr == pl.Kt ? 32 * kTcNP / pl.Kt : (32 * kTcNP / pl.Kr) & ~3u;
+  const uint32_t Kr_item = pl.pair ? 2 * pl.Kr : pl.Kr;  // keys per item (both CTAs of a pair)
+  pl.tasks = Kr_item * pl.Ft;
+  pl.n_ktiles = (B + Kr_item - 1) / Kr_item;
   // W units per node per window: W leaf pairs (W/4 8-row packed blocks), or
   // one final node (16 rows) with early termination.
   pl.R = unit_rows(pl) * W;
@@ -1115,10 +1136,16 @@ int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint3
   pl.y_stage_bytes = 4 * pl.Kt * Kw;
   // SMEM: T ring + y ring + the DFS stack (16 B per producer thread per level)
   pl.nst = tc_t_stages(D);
+  // small-batch key mapping with a y ring too large for 3 stages (B = 4, 5:
+  // 64 KB stages): 2 stages
+  if (pl.Kr < pl.Kt && !et &&
+      1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(pl.nsy) * pl.y_stage_bytes + 2 * kTcLevelBytes >
+          227 * 1024)
+    pl.nsy = 2;
   const size_t fixed = 1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(pl.nsy) * pl.y_stage_bytes;
   const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / kTcLevelBytes) + 1);
   const uint32_t m_min = tc_m_min(et, W);  // a subtree holds >= one window
-  if (m_cap < m_min || n < m_min) return DPF_EINVAL;
+  if (m_cap < m_min || n < m_min) return fail();
   // co-resident CTA pairs: a GPC with an odd SM count leaves an SM unpaired
   const uint32_t workers = pl.pair ? max_pairs(fixed + tc_stack_bytes(m_cap)) : uint32_t(num_sms());
   pl.m = choose_m_target(pl, n, m_min, m_cap, workers);
@@ -1131,16 +1158,16 @@ int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint3
   pl.F = ((pl.nr1 - 1) >> pl.m) - pl.lo_f + 1;
   pl.cap = pl.F;
   const uint64_t items = uint64_t(pl.n_ktiles) * ((pl.F + pl.Ft - 1) / pl.Ft);
-  if (items > 0x7FFFFFFFull) return DPF_EINVAL;
+  if (items > 0x7FFFFFFFull) return fail();
   pl.n_items = uint32_t(items);
   pl.W = W;
   pl.nwin = (et ? (1u << pl.m) : (1u << (pl.m - 1))) / W;
-  if (pl.nwin == 0) return DPF_EINVAL;
+  if (pl.nwin == 0) return fail();
   const uint32_t cols = n_dt_cta * 4 * Ktp;
   pl.tmem_cols = 32;
   while (pl.tmem_cols < cols) pl.tmem_cols <<= 1;
   pl.smem_bytes = fixed + tc_stack_bytes(pl.m);
-  if (pl.smem_bytes > 227 * 1024) return DPF_EINVAL;
+  if (pl.smem_bytes > 227 * 1024) return fail();
   pl.grid = pl.pair ? 2 * choose_grid(pl.n_items, pl.n_ktiles, workers) : choose_grid(pl.n_items, pl.n_ktiles);
   pl.prf_blocks = count_blocks(pl, B);
   return DPF_OK;
@@ -1252,6 +1279,8 @@ int launch_tc_kernel(const Plan &pl, const dev::FusedParams &p, cudaStream_t st)
                                 : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, false, true>)
                      : (pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSYEt, 4, true, true>
                                 : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSYEt, 4, false, true>);
+  else if (pl.nsy == 2 && !pl.pair)  // small-batch key mapping, 64 KB y stages
+    fn = &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, 2, 4, false, false>;
   else
     fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, true, false>
                  : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, false, false>;
@@ -1344,6 +1373,7 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
   p.n_items = pl.n_items;
   p.D = D;
   p.Kt = pl.Kt;
+  p.Kr = pl.Kr ? pl.Kr : pl.Kt;
   p.Ft = pl.Ft;
   p.tasks = pl.tasks;
   p.W = pl.W;
@@ -2236,6 +2266,7 @@ int eval_grouped_impl(const dpf_eval_group *groups, uint32_t n_groups, uint32_t 
   p.n_items = pl.n_items;
   p.D = D;
   p.Kt = pl.Kt;
+  p.Kr = pl.Kr ? pl.Kr : pl.Kt;
   p.Ft = pl.Ft;
   p.tasks = pl.tasks;
   p.W = pl.W;

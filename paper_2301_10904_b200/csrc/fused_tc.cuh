@@ -268,6 +268,13 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
+  if (tp.f.Kr < tp.f.Kt) {
+    // small batch: the y ring's padding key columns are read by every MMA and
+    // written by nobody -- zero them once (all stages), visible to the async proxy
+    uint4 *yz = reinterpret_cast<uint4 *>(smem + 1024 + NST * kTcTStageBytes);
+    for (uint32_t i = threadIdx.x; i < NSY * tp.y_stage_bytes / 16; i += blockDim.x) yz[i] = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+  }
   if (warp == NP) {  // consumer warp 0 owns the TMEM allocation (in each CTA of a pair)
     if constexpr (PAIR) {
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
@@ -289,7 +296,9 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
   // work items: one per CTA, or one per CTA pair
   const uint32_t first = PAIR ? blockIdx.x >> 1 : blockIdx.x;
   const uint32_t stride = PAIR ? gridDim.x >> 1 : gridDim.x;
-  const uint32_t Ktp = PAIR ? 2 * p.Kt : p.Kt;  // keys per item
+  const uint32_t Ktp = PAIR ? 2 * p.Kt : p.Kt;  // MMA N: B-operand columns per item
+  const uint32_t Kr = p.Kr;                      // columns per CTA that carry a key (<= Kt)
+  const uint32_t Krp = PAIR ? 2 * Kr : Kr;       // keys per item
   const uint32_t tmem_base = *tmem_slot;
 
   const uint32_t W2 = p.R;             // leaves per node per window (multiple of 8)
@@ -321,7 +330,9 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
         tmem_wait_ld();
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const uint32_t bkey = kt * Ktp + h * 16 + j;
+          // TMEM column c = h*16 + j: CTA half c / Kt, its column kk = c % Kt (a key iff kk < Kr)
+          const uint32_t c = h * 16 + j, kk = c % p.Kt;
+          const uint32_t bkey = kk < Kr ? kt * Krp + (c / p.Kt) * Kr + kk : 0xFFFFFFFFu;
           if (bkey < g.B && d < D) {
             const uint32_t val = v[j] + (x[j] << 16) + (z[j] << 24);  // A0 + 2^8 A1 + 2^16 A2 + 2^24 A3
             const uint32_t neg = key_party(g.keys + uint64_t(bkey) * g.kstride);
@@ -346,16 +357,17 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
     // 2^m - 1 blocks per subtree.  (Measured: this two-site form beats a
     // single-site "one block per iteration" loop and a 4-leaf "quad" form.)
     const uint32_t tix = warp * 32 + lane;
-    const uint32_t kl = tix % p.Kt, nl = tix / p.Kt;
+    const uint32_t kl = tix % Kr, nl = tix / Kr;
+    const bool lane_on = nl < p.Ft;  // small batches: Kr * Ft may leave a few lanes without a (key, node)
     uint32_t wseq = 0, pnf = 0;  // pnf: runs drained (producer epilogue)
     for (uint32_t item = first; item < p.n_items; item += stride) {
       const GroupDesc g = group_of(p, item);
       const uint32_t li = item - g.item_base;
       const uint32_t kt = li % g.n_ktiles, ng = li / g.n_ktiles;
       const uint32_t nq = 1u << (g.m - 1);
-      const uint32_t b = kt * Ktp + rank * p.Kt + kl;
+      const uint32_t b = kt * Krp + rank * Kr + kl;
       const uint64_t node = uint64_t(ng) * p.Ft + nl;
-      const bool valid = b < g.B && node < g.F;
+      const bool valid = lane_on && b < g.B && node < g.F;
       const uint8_t *key = g.keys + uint64_t(valid ? b : 0) * g.kstride;
       const uint32_t cw_out = key_cw_out(key);
       uint4 cur = valid ? g.frontier[uint64_t(b) * g.cap + node] : make_uint4(0, 0, 0, 0);
@@ -397,7 +409,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
                 y[c] = (valid && row >= g.r0 && row < g.r1) ? y[c] : 0u;
               }
             }
-            put_leaf16(yb, ybplane, p.Kt, kl, nl * W2 + 16 * qi, y);
+            if (lane_on) put_leaf16(yb, ybplane, p.Kt, kl, nl * W2 + 16 * qi, y);
             if ((q & 1) && (q >> 1) + 1 < npairs) {
               const uint32_t k = g.m - 1 - (__ffs((q >> 1) + 1) - 1);
               cur = stack[(k - 1) * (32 * NP) + tix];
@@ -429,7 +441,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
             y0 = (valid && row >= g.r0 && row < g.r1) ? y0 : 0u;
             y1 = (valid && row + 1 >= g.r0 && row + 1 < g.r1) ? y1 : 0u;
           }
-          put_leaf_pair(yb, ybplane, p.Kt, kl, nl * W2 + 2 * qi, y0, y1);
+          if (lane_on) put_leaf_pair(yb, ybplane, p.Kt, kl, nl * W2 + 2 * qi, y0, y1);
           if (q + 1 < nq) {  // pop the right sibling at depth m-1-ctz(q+1)
             const uint32_t k = g.m - 1 - (__ffs(q + 1) - 1);
             cur = stack[(k - 1) * (32 * NP) + tix];

@@ -606,3 +606,22 @@ def test_packed_deep_windows_shards(dp, oracle, n, N, r0, rows, D, B):
     Td = to_dev(Tsh)
     got = dp.as_u32(dp.eval_batch_packed(keys, dp.table_pack(Td, r0)))
     np.testing.assert_array_equal(got, oracle.answer_batch(okeys, Tsh, row_begin=r0, threads=16))
+
+
+@pytest.mark.parametrize("n,N,D,B,prf,row_begin", [
+    (14, 1 << 14, 256, 8, 1, 0), (13, 8000, 64, 9, 1, 0), (14, 1 << 14, 128, 15, 1, 0), (12, 4096, 256, 6, 1, 0),
+    (13, 7000, 256, 12, 1, 1000), (14, 1 << 14, 256, 11, 3, 0), (12, 4000, 64, 7, 3, 40), (12, 4096, 128, 4, 1, 0),
+    (12, 4096, 128, 2, 1, 0), (16, 1 << 16, 512, 10, 1, 0),
+])
+def test_packed_tc_small_batch(dp, oracle, n, N, D, B, prf, row_begin):
+    """B < 16 on the tensor path: N = 16 MMA columns, only B of them keys
+    (Kr = B producer key lanes, zero padding columns); falls back to the
+    padded mapping when that y ring does not fit SMEM (B = 2, 4)."""
+    T = synth.table(N, D, n + B)
+    al = synth.alphas(B, N, n + B)
+    seeds = synth.gen_seeds(B, n + B)
+    keys = [dp.gen(n, int(a), 1, s, prf=prf)[i % 2] for i, (a, s) in enumerate(zip(al, seeds))]
+    okeys = [oracle.key_from_wire(dp.key_serialize(k)) for k in keys]
+    Tsh = T[row_begin:]
+    got = dp.as_u32(dp.eval_batch_packed(keys, dp.table_pack(to_dev(Tsh), row_begin)))
+    np.testing.assert_array_equal(got, oracle.answer_batch(okeys, Tsh, row_begin=row_begin, threads=8))
