@@ -1100,13 +1100,23 @@ int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint3
     const char *e = getenv("DPF_TC_PAIR");
     return e ? atoi(e) : -1;
   }();
-  pl.pair = n_dt % 2 == 0 && pair_env != 0 && B > 16;
+  // MMA N of a single CTA / of a pair: TMEM budget, no wider than the batch
+  // (N >= 16, >= 32 for a pair)
+  auto mma_n = [&](uint32_t dt_cta, uint32_t kmin) {
+    uint32_t k = 128;
+    while (4 * dt_cta * k > 512) k >>= 1;
+    while (k > kmin && k / 2 >= B) k >>= 1;
+    return k;
+  };
+  // Pairs only where they widen the MMA (measured: same N -> the cross-CTA
+  // lockstep costs up to 2 %; early termination at Dp >= 512 pairs lose even
+  // with twice the N -- ET D = 1024 13.9 -> 9.6 ms unpaired, B = 32 at D = 256
+  // 0.53 -> 0.32 ms)
+  pl.pair = n_dt % 2 == 0 && pair_env != 0 && B > 16 && mma_n(n_dt / 2, 32) > mma_n(n_dt, 16) &&
+            (!et || n_dt == 2);
+  if (pair_env == 1 && n_dt % 2 == 0 && B > 16) pl.pair = true;  // DPF_TC_PAIR=1 forces pairs (A/B)
   const uint32_t n_dt_cta = pl.pair ? n_dt / 2 : n_dt;
-  uint32_t Ktp = 128;
-  while (4 * n_dt_cta * Ktp > 512) Ktp >>= 1;
-  // small batches: no wider than the batch (MMA N >= 16, >= 32 for a pair)
-  const uint32_t kmin = pl.pair ? 32 : 16;
-  while (Ktp > kmin && Ktp / 2 >= B) Ktp >>= 1;
+  const uint32_t Ktp = pl.pair ? mma_n(n_dt_cta, 32) : mma_n(n_dt_cta, 16);
   pl.Kt = pl.pair ? Ktp / 2 : Ktp;
   pl.nsy = (et && W == 2) ? 2u : tc_y_stages(et);
   // Small batches (B < MMA N, single CTA): the MMA keeps N = Kt columns but
