@@ -69,6 +69,9 @@ L2_BYTES = 126 * 1024 * 1024
 # Parity-failure hook for the bench contract test (flips one answer word
 # before the checks): never set in a measurement.
 INJECT_ENV = "DPF_BENCH_INJECT_MISMATCH"
+# Test-only: run the N > 1 path with every rank on cuda:0 (gloo, host-side
+# collectives) so a one-GPU box exercises it; the line carries "test_mode".
+SHARED_GPU_ENV = "DPF_BENCH_SHARED_GPU"
 
 METRIC = "DPF-PIR queries/sec"
 UNIT = "queries/s"
@@ -343,10 +346,30 @@ def run_ours(args, rank, world, local_rank):
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (no CPU fallback)")
+    # Test mode for the N > 1 code path on a one-GPU box (tests/test_bench_gpu.py):
+    # every rank on cuda:0, a gloo group, collectives through host copies.  The
+    # line says so ("test_mode"); it is never a measurement.
+    shared_gpu = os.environ.get(SHARED_GPU_ENV) == "1"
+    if shared_gpu:
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+
+    def host_coll(t, fn):
+        if not shared_gpu:
+            return fn(t)
+        h = t.cpu()
+        fn(h)
+        t.copy_(h)
+        return t
+
+    def reduce0(t):  # the one exchange step: partial answers summed mod 2^32 at rank 0
+        return host_coll(t, lambda x: shard.reduce_partial_shares(x, dst=0))
     G = world
     w = synth.CONFIGS[args.config]
     r0, rows = shard.row_range(w.N, G, rank)
@@ -385,11 +408,14 @@ def run_ours(args, rank, world, local_rank):
         else:
             dpfpir.eval_batch_wire(wire, w.log_n, T, r0, out=out, workspace=ws, stream=stream, prf=prf)
         if G > 1:
-            shard.reduce_partial_shares(out, dst=0)
+            reduce0(out)
 
     def barrier():
         if G > 1:
-            dist.barrier(device_ids=[local_rank])
+            if shared_gpu:
+                dist.barrier()
+            else:
+                dist.barrier(device_ids=[local_rank])
         torch.cuda.synchronize()
 
     # ---- correctness before timing: both servers' answers reconstruct T[alpha]
@@ -402,14 +428,14 @@ def run_ours(args, rank, world, local_rank):
     out1 = (dpfpir.eval_batch_packed(keys1, Tp, workspace=ws) if use_packed else
             dpfpir.eval_batch_shard(keys1, T, r0, workspace=ws))
     if G > 1:
-        shard.reduce_partial_shares(out1, dst=0)
+        reduce0(out1)
     parity = {}
     if rank == 0:
         recon = dpfpir.reconstruct(share0, dpfpir.as_u32(out1))
         want = np.stack([synth.table_rows(w.N, w.D, w.seed, int(a), int(a) + 1)[0] for a in al])
         parity["reconstruct_all_queries"] = bool(np.array_equal(recon, want))
     if G > 1:
-        parity.update(wrap_check(args, dpfpir, shard, dist, G, rank, dev, use_packed, prf, inject))
+        parity.update(wrap_check(args, dpfpir, shard, reduce0, G, rank, dev, use_packed, prf, inject))
     barrier()
 
     # ---- value: device-resident keys, K steps between barriers
@@ -436,7 +462,7 @@ def run_ours(args, rank, world, local_rank):
     stats = dpfpir.last_eval_stats()
     t = torch.tensor([region_ms if scrub is None else sum(step_ms)] + step_ms, dtype=torch.float64, device=dev)
     if G > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        host_coll(t, lambda x: dist.all_reduce(x, op=dist.ReduceOp.MAX))
     tl = t.cpu().tolist()
     ms_per_step = tl[0] / args.steps
     lat = percentiles(tl[1:])
@@ -459,7 +485,7 @@ def run_ours(args, rank, world, local_rank):
         else:
             dpfpir.eval_batch_shard(keys0, T, r0, out=out, workspace=ws, stream=stream)
         if G > 1:
-            shard.reduce_partial_shares(out, dst=0)
+            reduce0(out)
         if rank == 0:
             host_out.copy_(out, non_blocking=True)
         stream.synchronize()
@@ -476,7 +502,7 @@ def run_ours(args, rank, world, local_rank):
     clocks = sampler.stop()
     te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
     if G > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        host_coll(te, lambda x: dist.all_reduce(x, op=dist.ReduceOp.MAX))
     e2e_value = w.B / (float(te.item()) / e2e_steps * 1e-3)
     if rank == 0:
         e2e_ans = host_out.numpy().view(np.uint32).copy()
@@ -492,7 +518,7 @@ def run_ours(args, rank, world, local_rank):
         cpu, sample_parity = oracle_leg(args, w, wire_host, share0, T_host if G == 1 else None, G)
         parity.update(sample_parity)
     if G > 1:
-        dist.barrier(device_ids=[local_rank])
+        barrier()
 
     rc = 0
     if rank == 0:
@@ -519,19 +545,21 @@ def run_ours(args, rank, world, local_rank):
             "parity": parity,
             "plan": stats,
         }
+        if shared_gpu:
+            line["test_mode"] = "all ranks on cuda:0, gloo, host-side collectives (not a measurement)"
         rc = emit(line, parity)
     if peer is not None:
         peer.close()
     if G > 1:
         flag = torch.tensor([rc], dtype=torch.int32, device=dev)
-        dist.broadcast(flag, src=0)
+        host_coll(flag, lambda x: dist.broadcast(x, src=0))
         rc = int(flag.item())
-        dist.barrier(device_ids=[local_rank])
+        barrier()
         dist.destroy_process_group()
     return rc
 
 
-def wrap_check(args, dpfpir, shard, dist, G, rank, dev, use_packed, prf, inject):
+def wrap_check(args, dpfpir, shard, reduce0, G, rank, dev, use_packed, prf, inject):
     """N > 1: an all-0xFFFFFFFF table of 2^12 rows, row-sharded like the real
     one, 32 keys with random beta: each rank's partial answers are (minus) sums
     of leaf shares, so their int32 sum overflows in about half the words.  The
@@ -561,7 +589,7 @@ def wrap_check(args, dpfpir, shard, dist, G, rank, dev, use_packed, prf, inject)
             dpfpir.eval_batch_packed(kb, Twp, out=outw)
         else:
             dpfpir.eval_batch_shard(kb, Tw, a0, out=outw)
-        shard.reduce_partial_shares(outw, dst=0)
+        reduce0(outw)
     torch.cuda.synchronize()
     if rank != 0:
         return {}

@@ -1267,6 +1267,11 @@ int launch_tc_kernel(const Plan &pl, const dev::FusedParams &p, cudaStream_t st)
   // early termination's T ring turns over 4x faster per block: the loader
   // polls (try_wait) instead of sleeping (measured t5 ET 0.807 -> 0.815)
   tp.loader_spin = spin || pl.prf == DPF_PRF_CHACHA20_ET;
+  static const uint32_t wait_sleep = [] {  // DPF_WAIT_SLEEP=<bits> (tuning; fused_tc.cuh TcParams)
+    const char *e = getenv("DPF_WAIT_SLEEP");
+    return e ? uint32_t(atoi(e)) : 0u;
+  }();
+  tp.wait_sleep = wait_sleep;
   static const uint32_t nomma = [] {
     const char *e = getenv("DPF_DEBUG_NOMMA");
     return uint32_t(e && atoi(e) == 1);

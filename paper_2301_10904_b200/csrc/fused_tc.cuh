@@ -33,7 +33,17 @@ struct TcParams {
   uint32_t loader_spin;  // T loader waits by polling (try_wait) instead of sleeping back-off
   uint32_t debug_nomma;  // tuning only: skip the MMAs (wrong answers; isolates the producer rate)
   uint32_t role_swap;    // MMA / loader warps on the lowest hardware warp ids
+  uint32_t wait_sleep;   // bit 0: producers, bit 1: T loader, bit 2: MMA warp wait on their
+                         // mbarriers with a suspend-time hint (the warp sleeps until the phase
+                         // completes) instead of re-polling try_wait
 };
+
+// mbarrier wait of one role: polling try_wait, or try_wait with a suspend
+// hint (TRYWAIT + NANOSLEEP.SYNCS: woken by the barrier, no issue slots)
+__device__ __forceinline__ void mbar_wait_role(uint64_t *bar, uint32_t parity, bool sleep) {
+  if (sleep) mbar_wait_sleep(bar, parity);
+  else mbar_wait(bar, parity);
+}
 
 constexpr uint32_t kTcTStageBytes = 16384;  // 32 leaves x 128 columns x 4 limbs
 
@@ -383,7 +393,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
         const uint32_t npairs = 1u << (g.m - 1);
         for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
           const uint32_t ys = wseq % NSY, yuse = wseq / NSY;
-          if (yuse > 0) mbar_wait(&yempty[ys], (yuse - 1) & 1);
+          if (yuse > 0) mbar_wait_role(&yempty[ys], (yuse - 1) & 1, tp.wait_sleep & 1);
           uint8_t *yb = ybuf + ys * tp.y_stage_bytes;
           for (uint32_t qi = 0; qi < p.W; ++qi) {
             const uint32_t q = win * p.W + qi;
@@ -422,7 +432,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
       } else {
       for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
         const uint32_t ys = wseq % NSY, yuse = wseq / NSY;
-        if (yuse > 0) mbar_wait(&yempty[ys], (yuse - 1) & 1);
+        if (yuse > 0) mbar_wait_role(&yempty[ys], (yuse - 1) & 1, tp.wait_sleep & 1);
         uint8_t *yb = ybuf + ys * tp.y_stage_bytes;
         for (uint32_t qi = 0; qi < p.W; ++qi) {
           const uint32_t q = win * p.W + qi;
@@ -492,7 +502,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
           for (uint32_t cc = 0; cc < n_cc; ++cc) {
             for (uint32_t dt = 0; dt < n_dt; ++dt, ++tseq) {
               const uint32_t ts = tseq % NST, tuse = tseq / NST;
-              mbar_wait(&tfull[ts], tuse & 1);
+              mbar_wait_role(&tfull[ts], tuse & 1, tp.wait_sleep & 4);
               if (PAIR) mbar_wait_cluster(&tpeer[ts], tuse & 1);
               tc_fence_after();
               // Descriptors by adding (offset >> 4) to the start-address
@@ -573,7 +583,8 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
           for (uint32_t dt = 0; dt < n_dt; ++dt, ++tseq) {
             const uint32_t ts = tseq % NST, tuse = tseq / NST;
             if (tuse > 0) {
-              if (tp.loader_spin) mbar_wait(&tempty[ts], (tuse - 1) & 1);
+              if (tp.wait_sleep & 2) mbar_wait_sleep(&tempty[ts], (tuse - 1) & 1);
+              else if (tp.loader_spin) mbar_wait(&tempty[ts], (tuse - 1) & 1);
               else mbar_wait_backoff(&tempty[ts], (tuse - 1) & 1);
             }
             if (lane == 0) mbar_arrive_expect_tx(&tfull[ts], total);
