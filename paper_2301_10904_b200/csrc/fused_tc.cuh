@@ -372,8 +372,8 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
     uint32_t wseq = 0, pnf = 0;  // pnf: runs drained (producer epilogue)
     for (uint32_t item = first; item < p.n_items; item += stride) {
       const GroupDesc g = group_of(p, item);
-      const uint32_t li = item - g.item_base;
-      const uint32_t kt = li % g.n_ktiles, ng = li / g.n_ktiles;
+      const ItemDec it = decode_item(p, g, item);
+      const uint32_t kt = it.kt, ng = it.ng;
       const uint32_t nq = 1u << (g.m - 1);
       const uint32_t b = kt * Krp + rank * Kr + kl;
       const uint64_t node = uint64_t(ng) * p.Ft + nl;
@@ -384,6 +384,18 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
       const uint64_t row_base = (g.lo_f + node) << (g.m + V);
       const bool inside = valid && row_base >= g.r0 && row_base + (1ull << (g.m + V)) <= g.r1;
       uint32_t dep = 0;
+      if (it.w1 - it.w0 < g.nwin) {
+        // a part of a split item: its subtree hangs below the node at depth
+        // s = log2(split) reached along the part index's bits (s blocks)
+        const uint32_t S = g.nwin / (it.w1 - it.w0), part = it.w0 / (it.w1 - it.w0);
+        const uint32_t sd = __ffs(S) - 1;
+        for (uint32_t l = 0; l < sd; ++l) {
+          uint4 c0, c1;
+          node_children<Prf>(cur, key_cw(key, g.n - g.m + l + 1), c0, c1);
+          cur = ((part >> (sd - 1 - l)) & 1) ? c1 : c0;
+        }
+        dep = sd;
+      }
       if constexpr (Prf::kEt) {
         // R20: one final node (16 leaves) per unit; even units expand the
         // leaf-parent, odd units convert the right child kept from it.
@@ -391,7 +403,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
         load_cwl(key_cw(key, g.n + 1), cwl);
         uint4 pend = make_uint4(0, 0, 0, 0);
         const uint32_t npairs = 1u << (g.m - 1);
-        for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
+        for (uint32_t win = it.w0; win < it.w1; ++win, ++wseq) {
           const uint32_t ys = wseq % NSY, yuse = wseq / NSY;
           if (yuse > 0) mbar_wait_role(&yempty[ys], (yuse - 1) & 1, tp.wait_sleep & 1);
           uint8_t *yb = ybuf + ys * tp.y_stage_bytes;
@@ -430,7 +442,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
           named_arrive(1 + ys, 32 * (NP + 1));
         }
       } else {
-      for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
+      for (uint32_t win = it.w0; win < it.w1; ++win, ++wseq) {
         const uint32_t ys = wseq % NSY, yuse = wseq / NSY;
         if (yuse > 0) mbar_wait_role(&yempty[ys], (yuse - 1) & 1, tp.wait_sleep & 1);
         uint8_t *yb = ybuf + ys * tp.y_stage_bytes;
@@ -486,14 +498,15 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
     bool fresh = true;
     for (uint32_t item = first; item < p.n_items; item += stride) {
       const GroupDesc g = group_of(p, item);
-      const uint32_t kt = (item - g.item_base) % g.n_ktiles;
+      const ItemDec it = decode_item(p, g, item);
+      const uint32_t kt = it.kt;
       const bool last = !run_continues(p, g, kt, item + stride);
       if (q == 0 && rank == 0) {
         if (fresh && nf > 0) {  // epilogue(s) drained the accumulators
           if (PAIR) mbar_wait_cluster(accempty, (nf - 1) & 1);
           else mbar_wait(accempty, (nf - 1) & 1);
         }
-        for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
+        for (uint32_t win = it.w0; win < it.w1; ++win, ++wseq) {
           const uint32_t ys = wseq % NSY;
           named_sync(1 + ys, 32 * (NP + 1));
           if (PAIR) mbar_wait_cluster(&ypeer[ys], (wseq / NSY) & 1);
@@ -511,7 +524,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
               const uint64_t a0 = adesc0 + uint64_t((ts * kTcTStageBytes) >> 4);
               const uint64_t b0 = bdesc0 + uint64_t((yb - ybase + cc * 2u * b_lbo) >> 4);
               const uint32_t d0 = tmem_base + dt * 4 * Ktp;
-              const bool zero_acc = fresh && win == 0 && cc == 0;
+              const bool zero_acc = fresh && win == it.w0 && cc == 0;
               if (!tp.debug_nomma) {
 #pragma unroll
                 for (uint32_t s = 0; s < 4; ++s) {
@@ -528,12 +541,12 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
             }
           }
           umma_commit_elect<PAIR>(&yempty[ys]);                             // y stage reusable (both CTAs)
-          if (last && win + 1 == g.nwin) umma_commit_elect<PAIR>(accfull);  // run's accumulators complete
+          if (last && win + 1 == it.w1) umma_commit_elect<PAIR>(accfull);  // run's accumulators complete
           __syncwarp();
         }
       } else if (q == 0) {
         // PAIR peer: forward this CTA's y-FULL and T-FULL events to the leader
-        for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
+        for (uint32_t win = it.w0; win < it.w1; ++win, ++wseq) {
           const uint32_t ys = wseq % NSY;
           named_sync(1 + ys, 32 * (NP + 1));
           if (lane == 0) mbar_arrive_leader(&ypeer[ys]);
@@ -570,8 +583,9 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
       const GroupDesc g = group_of(p, item);
       const uint64_t pend = g.r0a + g.packed_rows;
       const uint8_t *packed = reinterpret_cast<const uint8_t *>(g.T);
-      const uint32_t ng = (item - g.item_base) / g.n_ktiles;
-      for (uint32_t win = 0; win < g.nwin; ++win) {
+      const ItemDec it = decode_item(p, g, item);
+      const uint32_t ng = it.ng;
+      for (uint32_t win = it.w0; win < it.w1; ++win) {
         for (uint32_t cc = 0; cc < n_cc; ++cc) {
           // lane j < 4: window leaves [32cc + 8j, +8) = rows [s0, s0 + 8) of
           // one node (one packed block): node (32cc + 8j) / W2, offset % W2
