@@ -239,8 +239,6 @@ struct FusedParams {
   const GroupDesc *groups;   // device array when n_groups > 1 (sorted by item_base)
   uint32_t n_groups, n_items, D;
   uint32_t Kt, Ft, tasks;  // tasks = Kt * Ft <= 32 * NP (lanes >= tasks idle)
-  uint32_t n_full, split;  // tail split (single-group tcgen05 launches): items >= n_full are parts of
-                           // 1/split of an item (nwin/split windows); split = 1: none
   uint32_t Kr;             // tcgen05: keys per CTA that carry a key (<= Kt = the CTA's MMA columns;
                            // < Kt for small batches: the other B-operand columns stay zero)
   uint32_t W;              // units per producer thread per window (unit: a leaf pair; ET: a final node)
@@ -268,34 +266,9 @@ __device__ __forceinline__ GroupDesc group_of(const FusedParams &p, uint32_t ite
 // run (the host picks a grid that is a multiple of the key-tile count when
 // that is free, which makes a CTA's key tile constant).  Exact for any
 // grouping: Z_2^32 addition is associative.
-// Work item -> (key tile, node group, windows [w0, w1) of its subtrees).
-// Items below p.n_full are whole subtrees; a single-group tcgen05 launch may
-// split each of its last items into p.split parts of nwin/split windows (a
-// part = the subtree below one node at depth log2(split)), so the last round
-// of the static round-robin lasts one part instead of one item.
-struct ItemDec {
-  uint32_t kt, ng, w0, w1;
-};
-__device__ __forceinline__ ItemDec decode_item(const FusedParams &p, const GroupDesc &g, uint32_t item) {
-  uint32_t li = item - g.item_base, part = 0, S = 1;
-  if (p.split > 1 && item >= p.n_full) {
-    const uint32_t j = item - p.n_full;
-    li = p.n_full + j / p.split;
-    part = j % p.split;
-    S = p.split;
-  }
-  ItemDec d;
-  d.kt = li % g.n_ktiles;
-  d.ng = li / g.n_ktiles;
-  const uint32_t pw = g.nwin / S;
-  d.w0 = part * pw;
-  d.w1 = d.w0 + pw;
-  return d;
-}
-
 __device__ __forceinline__ bool run_continues(const FusedParams &p, const GroupDesc &g, uint32_t kt, uint32_t next) {
   if (next >= p.n_items) return false;
-  if (p.n_groups <= 1) return decode_item(p, g, next).kt == kt;
+  if (p.n_groups <= 1) return (next - g.item_base) % g.n_ktiles == kt;
   const GroupDesc h = group_of(p, next);
   return h.item_base == g.item_base && (next - h.item_base) % h.n_ktiles == kt;
 }
@@ -791,8 +764,6 @@ struct Plan {
   uint64_t r0a, packed_rows;
   uint32_t n, m, f, Kt, Ft, tasks, W, CG, KG, SG, n_ktiles, n_items, nwin, grid;
   uint32_t Kr;  // tcgen05: real keys per CTA (<= Kt)
-  uint32_t n_full, split;  // tail split: items >= n_full are parts of 1/split item (split = 1: none)
-  double balance;          // static round-robin efficiency: (items / workers) / makespan
   uint64_t r0, r1, F, lo_f, cap;
   uint32_t y_stage_words, t_stage_words, CN, n_chunks, NST;
   size_t smem_bytes;
@@ -1072,42 +1043,6 @@ inline uint32_t tc_m_min(bool et, uint32_t W) {
 // (6 and 8 entries measured no faster for early termination either.)
 inline uint32_t tc_t_stages(uint32_t) { return 4u; }
 
-// Static round-robin makespan (in items) of n equal items on G workers when
-// the last n mod G items are split into S parts each.
-double split_makespan(uint64_t n, uint32_t G, uint32_t S) {
-  const uint64_t R = n / G, L = n % G;
-  return double(R) + (L ? double((L * S + G - 1) / G) / S : 0.0);
-}
-uint32_t best_split(uint64_t n, uint32_t G, uint32_t smax) {
-  uint32_t best = 1;
-  double bm = split_makespan(n, G, 1);
-  for (uint32_t S = 2; S <= smax && S <= 16; S <<= 1) {
-    const double m = split_makespan(n, G, S);
-    if (m < bm - 1e-9) {
-      bm = m;
-      best = S;
-    }
-  }
-  return best;
-}
-// Largest part count a plan's items allow: parts of >= 2 windows (a part pays
-// log2(split) path blocks per thread and its own pipeline ramp), standard
-// scheme only -- with early termination the producers drain TMEM at the end
-// of every accumulator run, and a part is a run of its own (measured: c3 ET
-// 0.78 -> 0.66 with parts; deeper subtrees balanced by parts also lost at c2,
-// 0.70 -> 0.67, and were dropped).
-uint32_t split_cap(const Plan &pl, bool et) {
-  return et ? 1u : pl.nwin / 2;
-}
-// DPF_TAIL_SPLIT=0 disables the tail split (A/B).
-bool tail_split_on() {
-  static const bool on = [] {
-    const char *e = getenv("DPF_TAIL_SPLIT");
-    return !(e && atoi(e) == 0);
-  }();
-  return on;
-}
-
 // tcgen05 plan (limb-packed table), D a multiple of 128 up to 1024:
 // Kt = MMA N = 64/32/16 keys so that 4 limb accumulators x D/128 tiles x Kt
 // columns fit the 512 TMEM columns; Ft = 512/Kt frontier nodes per item;
@@ -1140,11 +1075,8 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
   }();
   if (!allow8) return rc;
   // (a wider window must not trade the small-batch key mapping for the padded one)
-  // (nor a worse balance: a window covering whole subtrees cannot be split)
   Plan p8;
-  if (make_tc_plan_w(B, log_n, r0, rows, D, p8, false, 8, true, pl.Kr == pl.Kt) == DPF_OK &&
-      p8.balance >= pl.balance - 0.005)
-    pl = p8;
+  if (make_tc_plan_w(B, log_n, r0, rows, D, p8, false, 8, true, pl.Kr == pl.Kt) == DPF_OK) pl = p8;
   return DPF_OK;
 }
 
@@ -1248,21 +1180,6 @@ int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint3
   if (pl.smem_bytes > 227 * 1024) return fail();
   pl.grid = pl.pair ? 2 * choose_grid(pl.n_items, pl.n_ktiles, workers) : choose_grid(pl.n_items, pl.n_ktiles);
   pl.prf_blocks = count_blocks(pl, B);
-  // tail split of the static round-robin (items of the last, partial round cut into parts)
-  pl.n_full = pl.n_items;
-  pl.split = 1;
-  {
-    const uint32_t G = pl.pair ? pl.grid / 2 : pl.grid;
-    const uint32_t S = tail_split_on() ? best_split(pl.n_items, G, split_cap(pl, et)) : 1u;
-    pl.balance = double(pl.n_items) / G / split_makespan(pl.n_items, G, S);
-    if (S > 1) {
-      const uint32_t L = pl.n_items % G;
-      pl.n_full = pl.n_items - L;
-      pl.split = S;
-      pl.n_items = pl.n_full + L * S;
-      pl.grid = pl.pair ? 2 * std::min<uint32_t>(pl.n_items, G) : std::min<uint32_t>(pl.n_items, G);
-    }
-  }
   return DPF_OK;
 }
 
@@ -1350,11 +1267,6 @@ int launch_tc_kernel(const Plan &pl, const dev::FusedParams &p, cudaStream_t st)
   // early termination's T ring turns over 4x faster per block: the loader
   // polls (try_wait) instead of sleeping (measured t5 ET 0.807 -> 0.815)
   tp.loader_spin = spin || pl.prf == DPF_PRF_CHACHA20_ET;
-  static const uint32_t wait_sleep = [] {  // DPF_WAIT_SLEEP=<bits> (tuning; fused_tc.cuh TcParams)
-    const char *e = getenv("DPF_WAIT_SLEEP");
-    return e ? uint32_t(atoi(e)) : 0u;
-  }();
-  tp.wait_sleep = wait_sleep;
   static const uint32_t nomma = [] {
     const char *e = getenv("DPF_DEBUG_NOMMA");
     return uint32_t(e && atoi(e) == 1);
@@ -1369,16 +1281,23 @@ int launch_tc_kernel(const Plan &pl, const dev::FusedParams &p, cudaStream_t st)
   TcFn fn;
   // early termination: producers drain TMEM (EPIP, 18 warps, 96 registers)
   const bool epip = pl.prf == DPF_PRF_CHACHA20_ET;
-  if (pl.prf == DPF_PRF_AES128)
+  if (pl.prf == DPF_PRF_AES128 && pl.Kr < pl.Kt)
+    fn = pl.nsy == 2 ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, 2, 4, false, false, true>
+                     : &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, false, false, true>;
+  else if (pl.prf == DPF_PRF_AES128)
     fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, true, false>
                  : &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, false, false>;
+  else if (epip && pl.Kr < pl.Kt)  // small-batch key mapping (single CTA)
+    fn = pl.nsy == 2 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, false, true, true>
+                     : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSYEt, 4, false, true, true>;
   else if (epip)
     fn = pl.nsy == 2 ? (pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, true, true>
                                 : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, false, true>)
                      : (pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSYEt, 4, true, true>
                                 : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSYEt, 4, false, true>);
-  else if (pl.nsy == 2 && !pl.pair)  // small-batch key mapping, 64 KB y stages
-    fn = &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, 2, 4, false, false>;
+  else if (pl.Kr < pl.Kt)  // small-batch key mapping (single CTA; 2 y stages of 64 KB for B = 4, 5)
+    fn = pl.nsy == 2 ? &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, 2, 4, false, false, true>
+                     : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, false, false, true>;
   else
     fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, true, false>
                  : &dev::fused_eval_tc_kernel<dev::PrfChacha, kTcNP, kTcNSY, 4, false, false>;
@@ -1472,8 +1391,6 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
   p.D = D;
   p.Kt = pl.Kt;
   p.Kr = pl.Kr ? pl.Kr : pl.Kt;
-  p.n_full = pl.split > 1 ? pl.n_full : pl.n_items;
-  p.split = pl.split > 1 ? pl.split : 1;
   p.Ft = pl.Ft;
   p.tasks = pl.tasks;
   p.W = pl.W;
@@ -2367,8 +2284,6 @@ int eval_grouped_impl(const dpf_eval_group *groups, uint32_t n_groups, uint32_t 
   p.D = D;
   p.Kt = pl.Kt;
   p.Kr = pl.Kr ? pl.Kr : pl.Kt;
-  p.n_full = pl.n_items;  // grouped launches: no tail split (items are numbered group after group)
-  p.split = 1;
   p.Ft = pl.Ft;
   p.tasks = pl.tasks;
   p.W = pl.W;

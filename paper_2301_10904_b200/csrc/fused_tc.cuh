@@ -33,17 +33,7 @@ struct TcParams {
   uint32_t loader_spin;  // T loader waits by polling (try_wait) instead of sleeping back-off
   uint32_t debug_nomma;  // tuning only: skip the MMAs (wrong answers; isolates the producer rate)
   uint32_t role_swap;    // MMA / loader warps on the lowest hardware warp ids
-  uint32_t wait_sleep;   // bit 0: producers, bit 1: T loader, bit 2: MMA warp wait on their
-                         // mbarriers with a suspend-time hint (the warp sleeps until the phase
-                         // completes) instead of re-polling try_wait
 };
-
-// mbarrier wait of one role: polling try_wait, or try_wait with a suspend
-// hint (TRYWAIT + NANOSLEEP.SYNCS: woken by the barrier, no issue slots)
-__device__ __forceinline__ void mbar_wait_role(uint64_t *bar, uint32_t parity, bool sleep) {
-  if (sleep) mbar_wait_sleep(bar, parity);
-  else mbar_wait(bar, parity);
-}
 
 constexpr uint32_t kTcTStageBytes = 16384;  // 32 leaves x 128 columns x 4 limbs
 
@@ -237,7 +227,11 @@ __device__ __forceinline__ void put_leaf16(uint8_t *yb, uint32_t ybplane, uint32
 // peer's MMA warp forwards its y-FULL and T-FULL events to the leader
 // (ypeer / tpeer, remote mbarrier arrives); the leader's commits arrive in
 // both CTAs (multicast); both epilogues release the leader's accempty.
-template <class Prf, int NP, int NSY, int NST, bool PAIR, bool EPIP>
+// SMALLB: the small-batch key mapping (Kr < Kt real keys per CTA, zeroed
+// padding MMA columns).  A separate instantiation: the lane guard it needs in
+// the producer loop perturbs ptxas' register assignment of the ChaCha loop
+// (measured c3 0.918 -> 0.903 when compiled into every kernel).
+template <class Prf, int NP, int NSY, int NST, bool PAIR, bool EPIP, bool SMALLB = false>
 __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eval_tc_kernel(const TcParams tp) {
   constexpr int NC = EPIP ? 1 : 4;          // MMA/epilogue warps
   constexpr int NEPI = EPIP ? NP : 4;       // warps that drain TMEM and release accempty
@@ -278,7 +272,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   const uint32_t rank = PAIR ? cluster_ctarank() : 0u;
-  if (tp.f.Kr < tp.f.Kt) {
+  if (SMALLB) {
     // small batch: the y ring's padding key columns are read by every MMA and
     // written by nobody -- zero them once (all stages), visible to the async proxy
     uint4 *yz = reinterpret_cast<uint4 *>(smem + 1024 + NST * kTcTStageBytes);
@@ -307,7 +301,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
   const uint32_t first = PAIR ? blockIdx.x >> 1 : blockIdx.x;
   const uint32_t stride = PAIR ? gridDim.x >> 1 : gridDim.x;
   const uint32_t Ktp = PAIR ? 2 * p.Kt : p.Kt;  // MMA N: B-operand columns per item
-  const uint32_t Kr = p.Kr;                      // columns per CTA that carry a key (<= Kt)
+  const uint32_t Kr = SMALLB ? p.Kr : p.Kt;      // columns per CTA that carry a key (<= Kt)
   const uint32_t Krp = PAIR ? 2 * Kr : Kr;       // keys per item
   const uint32_t tmem_base = *tmem_slot;
 
@@ -341,8 +335,8 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           // TMEM column c = h*16 + j: CTA half c / Kt, its column kk = c % Kt (a key iff kk < Kr)
-          const uint32_t c = h * 16 + j, kk = c % p.Kt;
-          const uint32_t bkey = kk < Kr ? kt * Krp + (c / p.Kt) * Kr + kk : 0xFFFFFFFFu;
+          const uint32_t c = h * 16 + j, kk = SMALLB ? c % p.Kt : 0u;
+          const uint32_t bkey = !SMALLB ? kt * Ktp + c : kk < Kr ? kt * Krp + (c / p.Kt) * Kr + kk : 0xFFFFFFFFu;
           if (bkey < g.B && d < D) {
             const uint32_t val = v[j] + (x[j] << 16) + (z[j] << 24);  // A0 + 2^8 A1 + 2^16 A2 + 2^24 A3
             const uint32_t neg = key_party(g.keys + uint64_t(bkey) * g.kstride);
@@ -368,12 +362,12 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
     // single-site "one block per iteration" loop and a 4-leaf "quad" form.)
     const uint32_t tix = warp * 32 + lane;
     const uint32_t kl = tix % Kr, nl = tix / Kr;
-    const bool lane_on = nl < p.Ft;  // small batches: Kr * Ft may leave a few lanes without a (key, node)
+    const bool lane_on = !SMALLB || nl < p.Ft;  // small batches: Kr * Ft may leave a few lanes idle
     uint32_t wseq = 0, pnf = 0;  // pnf: runs drained (producer epilogue)
     for (uint32_t item = first; item < p.n_items; item += stride) {
       const GroupDesc g = group_of(p, item);
-      const ItemDec it = decode_item(p, g, item);
-      const uint32_t kt = it.kt, ng = it.ng;
+      const uint32_t li = item - g.item_base;
+      const uint32_t kt = li % g.n_ktiles, ng = li / g.n_ktiles;
       const uint32_t nq = 1u << (g.m - 1);
       const uint32_t b = kt * Krp + rank * Kr + kl;
       const uint64_t node = uint64_t(ng) * p.Ft + nl;
@@ -384,18 +378,6 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
       const uint64_t row_base = (g.lo_f + node) << (g.m + V);
       const bool inside = valid && row_base >= g.r0 && row_base + (1ull << (g.m + V)) <= g.r1;
       uint32_t dep = 0;
-      if (it.w1 - it.w0 < g.nwin) {
-        // a part of a split item: its subtree hangs below the node at depth
-        // s = log2(split) reached along the part index's bits (s blocks)
-        const uint32_t S = g.nwin / (it.w1 - it.w0), part = it.w0 / (it.w1 - it.w0);
-        const uint32_t sd = __ffs(S) - 1;
-        for (uint32_t l = 0; l < sd; ++l) {
-          uint4 c0, c1;
-          node_children<Prf>(cur, key_cw(key, g.n - g.m + l + 1), c0, c1);
-          cur = ((part >> (sd - 1 - l)) & 1) ? c1 : c0;
-        }
-        dep = sd;
-      }
       if constexpr (Prf::kEt) {
         // R20: one final node (16 leaves) per unit; even units expand the
         // leaf-parent, odd units convert the right child kept from it.
@@ -403,9 +385,9 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
         load_cwl(key_cw(key, g.n + 1), cwl);
         uint4 pend = make_uint4(0, 0, 0, 0);
         const uint32_t npairs = 1u << (g.m - 1);
-        for (uint32_t win = it.w0; win < it.w1; ++win, ++wseq) {
+        for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
           const uint32_t ys = wseq % NSY, yuse = wseq / NSY;
-          if (yuse > 0) mbar_wait_role(&yempty[ys], (yuse - 1) & 1, tp.wait_sleep & 1);
+          if (yuse > 0) mbar_wait(&yempty[ys], (yuse - 1) & 1);
           uint8_t *yb = ybuf + ys * tp.y_stage_bytes;
           for (uint32_t qi = 0; qi < p.W; ++qi) {
             const uint32_t q = win * p.W + qi;
@@ -431,7 +413,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
                 y[c] = (valid && row >= g.r0 && row < g.r1) ? y[c] : 0u;
               }
             }
-            if (lane_on) put_leaf16(yb, ybplane, p.Kt, kl, nl * W2 + 16 * qi, y);
+            if (!SMALLB || lane_on) put_leaf16(yb, ybplane, p.Kt, kl, nl * W2 + 16 * qi, y);
             if ((q & 1) && (q >> 1) + 1 < npairs) {
               const uint32_t k = g.m - 1 - (__ffs((q >> 1) + 1) - 1);
               cur = stack[(k - 1) * (32 * NP) + tix];
@@ -442,9 +424,9 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
           named_arrive(1 + ys, 32 * (NP + 1));
         }
       } else {
-      for (uint32_t win = it.w0; win < it.w1; ++win, ++wseq) {
+      for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
         const uint32_t ys = wseq % NSY, yuse = wseq / NSY;
-        if (yuse > 0) mbar_wait_role(&yempty[ys], (yuse - 1) & 1, tp.wait_sleep & 1);
+        if (yuse > 0) mbar_wait(&yempty[ys], (yuse - 1) & 1);
         uint8_t *yb = ybuf + ys * tp.y_stage_bytes;
         for (uint32_t qi = 0; qi < p.W; ++qi) {
           const uint32_t q = win * p.W + qi;
@@ -463,7 +445,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
             y0 = (valid && row >= g.r0 && row < g.r1) ? y0 : 0u;
             y1 = (valid && row + 1 >= g.r0 && row + 1 < g.r1) ? y1 : 0u;
           }
-          if (lane_on) put_leaf_pair(yb, ybplane, p.Kt, kl, nl * W2 + 2 * qi, y0, y1);
+          if (!SMALLB || lane_on) put_leaf_pair(yb, ybplane, p.Kt, kl, nl * W2 + 2 * qi, y0, y1);
           if (q + 1 < nq) {  // pop the right sibling at depth m-1-ctz(q+1)
             const uint32_t k = g.m - 1 - (__ffs(q + 1) - 1);
             cur = stack[(k - 1) * (32 * NP) + tix];
@@ -498,15 +480,14 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
     bool fresh = true;
     for (uint32_t item = first; item < p.n_items; item += stride) {
       const GroupDesc g = group_of(p, item);
-      const ItemDec it = decode_item(p, g, item);
-      const uint32_t kt = it.kt;
+      const uint32_t kt = (item - g.item_base) % g.n_ktiles;
       const bool last = !run_continues(p, g, kt, item + stride);
       if (q == 0 && rank == 0) {
         if (fresh && nf > 0) {  // epilogue(s) drained the accumulators
           if (PAIR) mbar_wait_cluster(accempty, (nf - 1) & 1);
           else mbar_wait(accempty, (nf - 1) & 1);
         }
-        for (uint32_t win = it.w0; win < it.w1; ++win, ++wseq) {
+        for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
           const uint32_t ys = wseq % NSY;
           named_sync(1 + ys, 32 * (NP + 1));
           if (PAIR) mbar_wait_cluster(&ypeer[ys], (wseq / NSY) & 1);
@@ -515,7 +496,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
           for (uint32_t cc = 0; cc < n_cc; ++cc) {
             for (uint32_t dt = 0; dt < n_dt; ++dt, ++tseq) {
               const uint32_t ts = tseq % NST, tuse = tseq / NST;
-              mbar_wait_role(&tfull[ts], tuse & 1, tp.wait_sleep & 4);
+              mbar_wait(&tfull[ts], tuse & 1);
               if (PAIR) mbar_wait_cluster(&tpeer[ts], tuse & 1);
               tc_fence_after();
               // Descriptors by adding (offset >> 4) to the start-address
@@ -524,7 +505,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
               const uint64_t a0 = adesc0 + uint64_t((ts * kTcTStageBytes) >> 4);
               const uint64_t b0 = bdesc0 + uint64_t((yb - ybase + cc * 2u * b_lbo) >> 4);
               const uint32_t d0 = tmem_base + dt * 4 * Ktp;
-              const bool zero_acc = fresh && win == it.w0 && cc == 0;
+              const bool zero_acc = fresh && win == 0 && cc == 0;
               if (!tp.debug_nomma) {
 #pragma unroll
                 for (uint32_t s = 0; s < 4; ++s) {
@@ -541,12 +522,12 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
             }
           }
           umma_commit_elect<PAIR>(&yempty[ys]);                             // y stage reusable (both CTAs)
-          if (last && win + 1 == it.w1) umma_commit_elect<PAIR>(accfull);  // run's accumulators complete
+          if (last && win + 1 == g.nwin) umma_commit_elect<PAIR>(accfull);  // run's accumulators complete
           __syncwarp();
         }
       } else if (q == 0) {
         // PAIR peer: forward this CTA's y-FULL and T-FULL events to the leader
-        for (uint32_t win = it.w0; win < it.w1; ++win, ++wseq) {
+        for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
           const uint32_t ys = wseq % NSY;
           named_sync(1 + ys, 32 * (NP + 1));
           if (lane == 0) mbar_arrive_leader(&ypeer[ys]);
@@ -583,9 +564,8 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
       const GroupDesc g = group_of(p, item);
       const uint64_t pend = g.r0a + g.packed_rows;
       const uint8_t *packed = reinterpret_cast<const uint8_t *>(g.T);
-      const ItemDec it = decode_item(p, g, item);
-      const uint32_t ng = it.ng;
-      for (uint32_t win = it.w0; win < it.w1; ++win) {
+      const uint32_t ng = (item - g.item_base) / g.n_ktiles;
+      for (uint32_t win = 0; win < g.nwin; ++win) {
         for (uint32_t cc = 0; cc < n_cc; ++cc) {
           // lane j < 4: window leaves [32cc + 8j, +8) = rows [s0, s0 + 8) of
           // one node (one packed block): node (32cc + 8j) / W2, offset % W2
@@ -597,8 +577,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
           for (uint32_t dt = 0; dt < n_dt; ++dt, ++tseq) {
             const uint32_t ts = tseq % NST, tuse = tseq / NST;
             if (tuse > 0) {
-              if (tp.wait_sleep & 2) mbar_wait_sleep(&tempty[ts], (tuse - 1) & 1);
-              else if (tp.loader_spin) mbar_wait(&tempty[ts], (tuse - 1) & 1);
+              if (tp.loader_spin) mbar_wait(&tempty[ts], (tuse - 1) & 1);
               else mbar_wait_backoff(&tempty[ts], (tuse - 1) & 1);
             }
             if (lane == 0) mbar_arrive_expect_tx(&tfull[ts], total);
