@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fused -s 2 -c 1 -o /tmp/prof_c3 python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 3 > /dev/null 2>&1
+ncu -i /tmp/prof_c3.ncu-rep --page source --csv --print-source sass > gpurun_out/src_c3.csv 2>&1
