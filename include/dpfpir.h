@@ -66,7 +66,8 @@ enum dpf_status {
   DPF_EKEY = -2,         /* malformed key: magic/version/party/log_n/prf mismatch */
   DPF_ENOMEM = -3,       /* workspace too small */
   DPF_ECUDA = -4,        /* CUDA launch/config error (reported synchronously) */
-  DPF_EUNSUPPORTED = -6  /* unknown PRF id, feature not built, no sm_100 device */
+  DPF_EUNSUPPORTED = -6, /* unknown PRF id, feature not built, no sm_100 device */
+  DPF_EBUSY = -7         /* pipelined server: every slot holds an uncollected batch */
 };
 
 /* One party's DPF key (two codeword matrices C_0, C_1; P:349 root
@@ -198,6 +199,29 @@ int dpf_server_create(uint32_t B, uint32_t log_n, uint32_t prf, const void *tabl
                       dpf_server **out);
 int dpf_server_run(dpf_server *server, const uint8_t *keys_wire_host, uint32_t *shares_host);
 void dpf_server_destroy(dpf_server *server);
+
+/* ---- pipelined serving: up to `depth` batches in flight ----
+ * dpf_server_pipeline_create builds `depth` (1..DPF_SERVER_MAX_DEPTH) slots,
+ * each a captured serving step as above with its own pinned staging, answer
+ * buffer, stream and workspace region (workspace >=
+ * dpf_server_pipeline_workspace_bytes(..., depth)).  dpf_server_submit checks
+ * the headers, copies one batch's host wire keys into the next free slot and
+ * launches its graph without waiting (DPF_EBUSY when all slots hold
+ * uncollected batches); dpf_server_collect waits for the OLDEST batch in
+ * flight and copies its B x D answers to shares_host (DPF_EINVAL if none).
+ * Consecutive batches overlap: one batch's key upload, top BFS and answer
+ * download run beside its predecessor's fused kernel.  dpf_server_create is
+ * the depth-1 case; dpf_server_run = submit + collect (DPF_EBUSY if a batch
+ * is in flight).  destroy waits for batches in flight.  Not thread-safe per
+ * server object. */
+#define DPF_SERVER_MAX_DEPTH 4
+size_t dpf_server_pipeline_workspace_bytes(uint32_t B, uint32_t log_n, uint32_t prf, uint64_t row_count, uint32_t D,
+                                           uint32_t depth);
+int dpf_server_pipeline_create(uint32_t B, uint32_t log_n, uint32_t prf, const void *table, int packed,
+                               uint64_t row_begin, uint64_t row_count, uint32_t D, uint32_t depth, void *workspace,
+                               size_t workspace_bytes, void *stream, dpf_server **out);
+int dpf_server_submit(dpf_server *server, const uint8_t *keys_wire_host);
+int dpf_server_collect(dpf_server *server, uint32_t *shares_host);
 
 /* ---- fused cross-GPU reduction (multi-GPU row sharding) ----
  * The G row shards' partial answers sum to the answer (Z_2^32 is a group).

@@ -1719,11 +1719,17 @@ extern "C" int dpf_serve_batch(const dpf_key *keys, uint32_t B, const uint32_t *
 // replayed with ONE cudaGraphLaunch per batch (the per-call launch overhead of
 // the small configurations is host-side; the graph removes it).
 struct dpf_server {
+  // One slot per batch in flight: pinned staging for the wire keys and the
+  // answers, a private stream, the captured graph, its own workspace region.
+  struct Slot {
+    uint8_t *keys_pinned = nullptr;  // B x kstride (library-owned pinned staging)
+    uint32_t *out_pinned = nullptr;  // B x D
+    cudaStream_t st = nullptr;
+    cudaGraphExec_t exec = nullptr;
+  };
   uint32_t B, log_n, prf, D, kstride;
-  uint8_t *keys_pinned = nullptr;   // B x kstride (library-owned pinned staging)
-  uint32_t *out_pinned = nullptr;   // B x D
-  cudaStream_t st = nullptr;
-  cudaGraphExec_t exec = nullptr;
+  std::vector<Slot> slots;
+  uint32_t head = 0, inflight = 0;  // next slot to submit into; batches submitted, not collected
 };
 
 extern "C" size_t dpf_server_workspace_bytes(uint32_t B, uint32_t log_n, uint32_t prf, uint64_t row_count,
@@ -1734,71 +1740,106 @@ extern "C" size_t dpf_server_workspace_bytes(uint32_t B, uint32_t log_n, uint32_
   return ev + align_up(size_t(B) * kstride, kAlign) + align_up(size_t(B) * D * 4, kAlign);
 }
 
-extern "C" int dpf_server_create(uint32_t B, uint32_t log_n, uint32_t prf, const void *table, int packed,
-                                 uint64_t row_begin, uint64_t row_count, uint32_t D, void *workspace,
-                                 size_t workspace_bytes, void *stream, dpf_server **out) {
+extern "C" size_t dpf_server_pipeline_workspace_bytes(uint32_t B, uint32_t log_n, uint32_t prf, uint64_t row_count,
+                                                      uint32_t D, uint32_t depth) {
+  if (depth < 1 || depth > DPF_SERVER_MAX_DEPTH) return 0;
+  const size_t one = dpf_server_workspace_bytes(B, log_n, prf, row_count, D);
+  return one ? size_t(depth) * align_up(one, kAlign) : 0;
+}
+
+namespace dpfpir {
+namespace {
+void server_free(dpf_server *sv) {
+  for (auto &sl : sv->slots) {
+    if (sl.exec) cudaGraphExecDestroy(sl.exec);
+    if (sl.keys_pinned) cudaFreeHost(sl.keys_pinned);
+    if (sl.out_pinned) cudaFreeHost(sl.out_pinned);
+    if (sl.st) cudaStreamDestroy(sl.st);
+  }
+  delete sv;
+}
+
+// Capture one slot's serving step (H2D keys, eval, D2H answers) on its stream.
+int capture_slot(dpf_server *sv, dpf_server::Slot &sl, const void *table, int packed, uint64_t row_begin,
+                 uint64_t row_count, uint8_t *ws) {
+  const uint32_t B = sv->B, D = sv->D;
+  const size_t ev = dpf_eval_workspace_bytes(B, sv->log_n, row_count, D);
+  uint8_t *keys_dev = ws + ev;
+  uint32_t *out_dev = reinterpret_cast<uint32_t *>(keys_dev + align_up(size_t(B) * sv->kstride, kAlign));
+  const size_t kb = size_t(B) * sv->kstride, ob = size_t(B) * D * 4;
+  if (cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking) != cudaSuccess) {
+    sl.st = nullptr;
+    return DPF_ECUDA;
+  }
+  if (cudaHostAlloc(&sl.keys_pinned, kb, cudaHostAllocDefault) != cudaSuccess) {
+    sl.keys_pinned = nullptr;
+    return DPF_ENOMEM;
+  }
+  if (cudaHostAlloc(&sl.out_pinned, ob, cudaHostAllocDefault) != cudaSuccess) {
+    sl.out_pinned = nullptr;
+    return DPF_ENOMEM;
+  }
+  std::memset(sl.keys_pinned, 0, kb);
+  // warm-up launch outside capture: first-use attribute/occupancy queries happen here
+  int rc = eval_impl(nullptr, B, keys_dev, sv->log_n, sv->prf, static_cast<const uint32_t *>(table), row_begin,
+                     row_count, D, out_dev, ws, ev, sl.st, packed != 0);
+  if (rc == DPF_OK && cudaStreamSynchronize(sl.st) != cudaSuccess) rc = DPF_ECUDA;
+  if (rc != DPF_OK) return rc;
+  cudaGraph_t graph = nullptr;
+  if (cudaStreamBeginCapture(sl.st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return DPF_ECUDA;
+  int r1 = cudaMemcpyAsync(keys_dev, sl.keys_pinned, kb, cudaMemcpyHostToDevice, sl.st) == cudaSuccess ? DPF_OK
+                                                                                                       : DPF_ECUDA;
+  if (r1 == DPF_OK)
+    r1 = eval_impl(nullptr, B, keys_dev, sv->log_n, sv->prf, static_cast<const uint32_t *>(table), row_begin,
+                   row_count, D, out_dev, ws, ev, sl.st, packed != 0);
+  if (r1 == DPF_OK && cudaMemcpyAsync(sl.out_pinned, out_dev, ob, cudaMemcpyDeviceToHost, sl.st) != cudaSuccess)
+    r1 = DPF_ECUDA;
+  const cudaError_t e = cudaStreamEndCapture(sl.st, &graph);
+  rc = r1 != DPF_OK ? r1 : (e == cudaSuccess ? DPF_OK : DPF_ECUDA);
+  if (rc == DPF_OK && cudaGraphInstantiate(&sl.exec, graph, 0) != cudaSuccess) rc = DPF_ECUDA;
+  if (graph) cudaGraphDestroy(graph);
+  return rc;
+}
+}  // namespace
+}  // namespace dpfpir
+
+extern "C" int dpf_server_pipeline_create(uint32_t B, uint32_t log_n, uint32_t prf, const void *table, int packed,
+                                          uint64_t row_begin, uint64_t row_count, uint32_t D, uint32_t depth,
+                                          void *workspace, size_t workspace_bytes, void *stream, dpf_server **out) {
   if (!out || !table || !workspace || B == 0) return DPF_EINVAL;
   *out = nullptr;
-  const size_t need = dpf_server_workspace_bytes(B, log_n, prf, row_count, D);
+  const size_t need = dpf_server_pipeline_workspace_bytes(B, log_n, prf, row_count, D, depth);
   if (need == 0) return DPF_EINVAL;
   if (workspace_bytes < need) return DPF_ENOMEM;
   if (reinterpret_cast<uintptr_t>(workspace) & (kAlign - 1)) return DPF_EINVAL;
-  const size_t ev = dpf_eval_workspace_bytes(B, log_n, row_count, D);
+  const size_t per = align_up(dpf_server_workspace_bytes(B, log_n, prf, row_count, D), kAlign);
   dpf_server *sv = new dpf_server;
   sv->B = B;
   sv->log_n = log_n;
   sv->prf = prf;
   sv->D = D;
   sv->kstride = uint32_t(dpf_key_wire_size_prf(log_n, prf));
-  // the caller's stream orders the table's preparation; the server captures
+  sv->slots.resize(depth);
+  // the caller's stream orders the table's preparation; every slot captures
   // and replays on a private stream (the legacy NULL stream cannot be captured)
-  if (cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&sv->st, cudaStreamNonBlocking) != cudaSuccess) {
-    cudaGetLastError();
-    sv->st = nullptr;
-    dpf_server_destroy(sv);
-    return DPF_ECUDA;
-  }
-  uint8_t *ws = static_cast<uint8_t *>(workspace);
-  uint8_t *keys_dev = ws + ev;
-  uint32_t *out_dev = reinterpret_cast<uint32_t *>(keys_dev + align_up(size_t(B) * sv->kstride, kAlign));
-  const size_t kb = size_t(B) * sv->kstride, ob = size_t(B) * D * 4;
-  int rc = DPF_OK;
-  cudaGraph_t graph = nullptr;
-  if (cudaHostAlloc(&sv->keys_pinned, kb, cudaHostAllocDefault) != cudaSuccess ||
-      cudaHostAlloc(&sv->out_pinned, ob, cudaHostAllocDefault) != cudaSuccess) {
-    rc = DPF_ENOMEM;
-  } else {
-    std::memset(sv->keys_pinned, 0, kb);
-    // warm-up launch outside capture: first-use attribute/occupancy queries happen here
-    rc = eval_impl(nullptr, B, keys_dev, log_n, prf, static_cast<const uint32_t *>(table), row_begin, row_count, D,
-                   out_dev, ws, ev, sv->st, packed != 0);
-    if (rc == DPF_OK && cudaStreamSynchronize(sv->st) != cudaSuccess) rc = DPF_ECUDA;
-  }
-  if (rc == DPF_OK) {
-    if (cudaStreamBeginCapture(sv->st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
-      rc = DPF_ECUDA;
-    } else {
-      int r1 = cudaMemcpyAsync(keys_dev, sv->keys_pinned, kb, cudaMemcpyHostToDevice, sv->st) == cudaSuccess
-                   ? DPF_OK : DPF_ECUDA;
-      if (r1 == DPF_OK)
-        r1 = eval_impl(nullptr, B, keys_dev, log_n, prf, static_cast<const uint32_t *>(table), row_begin, row_count,
-                       D, out_dev, ws, ev, sv->st, packed != 0);
-      if (r1 == DPF_OK && cudaMemcpyAsync(sv->out_pinned, out_dev, ob, cudaMemcpyDeviceToHost, sv->st) != cudaSuccess)
-        r1 = DPF_ECUDA;
-      const cudaError_t e = cudaStreamEndCapture(sv->st, &graph);
-      rc = r1 != DPF_OK ? r1 : (e == cudaSuccess ? DPF_OK : DPF_ECUDA);
-      if (rc == DPF_OK && cudaGraphInstantiate(&sv->exec, graph, 0) != cudaSuccess) rc = DPF_ECUDA;
-    }
-  }
-  if (graph) cudaGraphDestroy(graph);
+  int rc = cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) == cudaSuccess ? DPF_OK : DPF_ECUDA;
+  for (uint32_t i = 0; i < depth && rc == DPF_OK; ++i)
+    rc = capture_slot(sv, sv->slots[i], table, packed, row_begin, row_count,
+                      static_cast<uint8_t *>(workspace) + size_t(i) * per);
   if (rc != DPF_OK) {
     cudaGetLastError();
-    dpf_server_destroy(sv);
+    server_free(sv);
     return rc;
   }
   *out = sv;
   return DPF_OK;
+}
+
+extern "C" int dpf_server_create(uint32_t B, uint32_t log_n, uint32_t prf, const void *table, int packed,
+                                 uint64_t row_begin, uint64_t row_count, uint32_t D, void *workspace,
+                                 size_t workspace_bytes, void *stream, dpf_server **out) {
+  return dpf_server_pipeline_create(B, log_n, prf, table, packed, row_begin, row_count, D, 1, workspace,
+                                    workspace_bytes, stream, out);
 }
 
 // Wire-format header checks of a host key (include/dpfpir.h "Wire format").
@@ -1809,24 +1850,43 @@ static bool wire_header_ok(const uint8_t *k, uint32_t log_n, uint32_t prf) {
   return dpfpir::wire_header_valid(k) && k[5] == prf && k[7] == log_n;
 }
 
-extern "C" int dpf_server_run(dpf_server *sv, const uint8_t *keys_wire_host, uint32_t *shares_host) {
-  if (!sv || !keys_wire_host || !shares_host) return DPF_EINVAL;
+extern "C" int dpf_server_submit(dpf_server *sv, const uint8_t *keys_wire_host) {
+  if (!sv || !keys_wire_host) return DPF_EINVAL;
+  if (sv->inflight == sv->slots.size()) return DPF_EBUSY;
   for (uint32_t b = 0; b < sv->B; ++b)
     if (!wire_header_ok(keys_wire_host + size_t(b) * sv->kstride, sv->log_n, sv->prf)) return DPF_EKEY;
-  std::memcpy(sv->keys_pinned, keys_wire_host, size_t(sv->B) * sv->kstride);
-  if (cudaGraphLaunch(sv->exec, sv->st) != cudaSuccess) return DPF_ECUDA;
-  if (cudaStreamSynchronize(sv->st) != cudaSuccess) return DPF_ECUDA;
-  std::memcpy(shares_host, sv->out_pinned, size_t(sv->B) * sv->D * 4);
+  dpf_server::Slot &sl = sv->slots[sv->head];
+  // the slot is free (its previous batch was collected): its staging can be overwritten
+  std::memcpy(sl.keys_pinned, keys_wire_host, size_t(sv->B) * sv->kstride);
+  if (cudaGraphLaunch(sl.exec, sl.st) != cudaSuccess) return DPF_ECUDA;
+  sv->head = (sv->head + 1) % uint32_t(sv->slots.size());
+  ++sv->inflight;
   return DPF_OK;
+}
+
+extern "C" int dpf_server_collect(dpf_server *sv, uint32_t *shares_host) {
+  if (!sv || !shares_host) return DPF_EINVAL;
+  if (sv->inflight == 0) return DPF_EINVAL;
+  const uint32_t n = uint32_t(sv->slots.size());
+  dpf_server::Slot &sl = sv->slots[(sv->head + n - sv->inflight) % n];  // oldest batch in flight
+  if (cudaStreamSynchronize(sl.st) != cudaSuccess) return DPF_ECUDA;
+  std::memcpy(shares_host, sl.out_pinned, size_t(sv->B) * sv->D * 4);
+  --sv->inflight;
+  return DPF_OK;
+}
+
+extern "C" int dpf_server_run(dpf_server *sv, const uint8_t *keys_wire_host, uint32_t *shares_host) {
+  if (!sv || !keys_wire_host || !shares_host) return DPF_EINVAL;
+  if (sv->inflight) return DPF_EBUSY;  // run is submit + collect of one batch
+  const int rc = dpf_server_submit(sv, keys_wire_host);
+  return rc != DPF_OK ? rc : dpf_server_collect(sv, shares_host);
 }
 
 extern "C" void dpf_server_destroy(dpf_server *sv) {
   if (!sv) return;
-  if (sv->exec) cudaGraphExecDestroy(sv->exec);
-  if (sv->keys_pinned) cudaFreeHost(sv->keys_pinned);
-  if (sv->out_pinned) cudaFreeHost(sv->out_pinned);
-  if (sv->st) cudaStreamDestroy(sv->st);
-  delete sv;
+  for (auto &sl : sv->slots)
+    if (sl.st) cudaStreamSynchronize(sl.st);
+  dpfpir::server_free(sv);
 }
 
 extern "C" int dpf_eval_leaves(const dpf_key *keys, uint32_t B, uint32_t *leaves, void *workspace,

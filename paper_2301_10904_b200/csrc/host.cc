@@ -317,6 +317,7 @@ extern "C" const char *dpf_strerror(int code) {
     case DPF_ENOMEM: return "workspace too small";
     case DPF_ECUDA: return "CUDA error";
     case DPF_EUNSUPPORTED: return "unsupported (PRF not built or no sm_100 device)";
+    case DPF_EBUSY: return "busy (every pipelined-server slot holds an uncollected batch)";
     default: return "unknown status";
   }
 }

@@ -27,7 +27,7 @@ DPF_PRF_CHACHA20 = 1
 DPF_PRF_AES128 = 2
 DPF_PRF_CHACHA20_ET = 3  # early-terminated leaves (R20), log_n >= 5
 DPF_ET_BITS = 4
-DPF_OK, DPF_EINVAL, DPF_EKEY, DPF_ENOMEM, DPF_ECUDA, DPF_EUNSUPPORTED = 0, -1, -2, -3, -4, -6
+DPF_OK, DPF_EINVAL, DPF_EKEY, DPF_ENOMEM, DPF_ECUDA, DPF_EUNSUPPORTED, DPF_EBUSY = 0, -1, -2, -3, -4, -6, -7
 
 
 class DpfError(RuntimeError):
@@ -93,6 +93,12 @@ def lib() -> ctypes.CDLL:
     L.dpf_server_workspace_bytes.restype = sz
     L.dpf_server_create.argtypes = [u32, u32, u32, vp, ctypes.c_int, u64, u64, u32, vp, sz, vp, ctypes.POINTER(vp)]
     L.dpf_server_run.argtypes = [vp, vp, vp]
+    L.dpf_server_pipeline_workspace_bytes.argtypes = [u32, u32, u32, u64, u32, u32]
+    L.dpf_server_pipeline_workspace_bytes.restype = sz
+    L.dpf_server_pipeline_create.argtypes = [u32, u32, u32, vp, ctypes.c_int, u64, u64, u32, u32, vp, sz, vp,
+                                             ctypes.POINTER(vp)]
+    L.dpf_server_submit.argtypes = [vp, vp]
+    L.dpf_server_collect.argtypes = [vp, vp]
     L.dpf_server_destroy.argtypes = [vp]
     L.dpf_server_destroy.restype = None
     L.dpf_eval_leaves.argtypes = [vp, u32, vp, vp, sz, vp]
@@ -131,6 +137,8 @@ EXPORTED_SYMBOLS = ("dpf_gen", "dpf_key_wire_size", "dpf_key_wire_size_prf", "dp
                     "dpf_eval_pbr_workspace_bytes", "dpf_eval_pbr",
                     "dpf_eval_batch_wire_ex", "dpf_ipc_export", "dpf_ipc_open", "dpf_ipc_close",
                     "dpf_server_workspace_bytes", "dpf_server_create", "dpf_server_run", "dpf_server_destroy",
+                    "dpf_server_pipeline_workspace_bytes", "dpf_server_pipeline_create", "dpf_server_submit",
+                    "dpf_server_collect",
                     "dpf_kernel_timer_read", "dpf_strerror", "dpf_version")
 
 
@@ -343,17 +351,20 @@ def ipc_close(ptr: int) -> None:
 
 
 class Server:
-    """dpf_server_*: one serving step of a fixed shape captured as a CUDA graph.
-    run(keys_wire_host uint8 [B, w], out int32 [B, D] host) -> out."""
+    """dpf_server_*: one serving step of a fixed shape captured as a CUDA graph
+    (`depth` > 1: dpf_server_pipeline_create, that many batches in flight).
+    run(keys_wire_host uint8 [B, w], out int32 [B, D] host) -> out;
+    submit(keys_wire_host) / collect(out) for the pipelined form."""
 
-    def __init__(self, B: int, log_n: int, table, row_begin: int = 0, prf: int = DPF_PRF_CHACHA20, stream=None):
+    def __init__(self, B: int, log_n: int, table, row_begin: int = 0, prf: int = DPF_PRF_CHACHA20, stream=None,
+                 depth: int = 1):
         import torch
         packed = isinstance(table, PackedTable)
         rows, D = (table.row_count, table.D) if packed else table.shape
         dev = table.data.device if packed else table.device
-        need = lib().dpf_server_workspace_bytes(B, log_n, prf, rows, D)
+        need = lib().dpf_server_pipeline_workspace_bytes(B, log_n, prf, rows, D, depth)
         if need == 0:
-            raise DpfError(DPF_EINVAL, "dpf_server_workspace_bytes")
+            raise DpfError(DPF_EINVAL, "dpf_server_pipeline_workspace_bytes")
         # private workspace: the captured graph replays on the server's own
         # stream for the object's lifetime, so no other call may share it
         self.ws = torch.empty(need, dtype=torch.uint8, device=dev)
@@ -361,10 +372,12 @@ class Server:
         self.B, self.D, self.wire = B, D, key_wire_size(log_n, prf)
         h = ctypes.c_void_p()
         tptr = table.data.data_ptr() if packed else table.data_ptr()
-        _check(lib().dpf_server_create(B, log_n, prf, tptr, int(packed), row_begin, rows, D, self.ws.data_ptr(),
-                                       self.ws.numel() * self.ws.element_size(), _stream_ptr(stream), ctypes.byref(h)),
-               "dpf_server_create")
+        _check(lib().dpf_server_pipeline_create(B, log_n, prf, tptr, int(packed), row_begin, rows, D, depth,
+                                                self.ws.data_ptr(), self.ws.numel() * self.ws.element_size(),
+                                                _stream_ptr(stream), ctypes.byref(h)),
+               "dpf_server_pipeline_create")
         self.h = h
+        self.depth = depth
 
     def run(self, keys_wire_host: np.ndarray, out: Optional[np.ndarray] = None) -> np.ndarray:
         kw = np.ascontiguousarray(keys_wire_host, dtype=np.uint8)
@@ -373,6 +386,21 @@ class Server:
         if out is None:
             out = np.empty((self.B, self.D), dtype=np.uint32)
         _check(lib().dpf_server_run(self.h, kw.ctypes.data, out.ctypes.data), "dpf_server_run")
+        return out
+
+    def submit(self, keys_wire_host: np.ndarray) -> None:
+        """dpf_server_submit: launch one batch without waiting (the keys are
+        copied into the slot's pinned staging before this returns)."""
+        kw = np.ascontiguousarray(keys_wire_host, dtype=np.uint8)
+        if kw.size != self.B * self.wire:
+            raise ValueError("expected %d keys of %d wire bytes" % (self.B, self.wire))
+        _check(lib().dpf_server_submit(self.h, kw.ctypes.data), "dpf_server_submit")
+
+    def collect(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """dpf_server_collect: wait for the oldest batch in flight, its answers."""
+        if out is None:
+            out = np.empty((self.B, self.D), dtype=np.uint32)
+        _check(lib().dpf_server_collect(self.h, out.ctypes.data), "dpf_server_collect")
         return out
 
     def close(self):

@@ -550,6 +550,43 @@ def test_graph_server_replays_new_keys(dp, oracle, prf, D, packed):
     srv.close()
 
 
+@pytest.mark.parametrize("depth,packed,prf", [(2, True, 1), (3, False, 1), (2, True, 3)])
+def test_pipelined_server_batches_in_flight(dp, oracle, depth, packed, prf):
+    """dpf_server_pipeline_*: up to `depth` batches in flight, collected oldest
+    first, each equal to the oracle; a full pipeline refuses a submit
+    (DPF_EBUSY) and run() refuses while batches are in flight."""
+    n, N, D, B = 12, 3500, 128, 48
+    T = synth.table(N, D, 1500 + depth)
+    Td = to_dev(T)
+    srv = dp.Server(B, n, dp.table_pack(Td) if packed else Td, prf=prf, depth=depth)
+    batches = []
+    for rep in range(3 * depth + 1):
+        al = synth.alphas(B, N, 1600 + rep)
+        keys = [dp.gen(n, int(a), 1, s, prf=prf)[(i + rep) % 2]
+                for i, (a, s) in enumerate(zip(al, synth.gen_seeds(B, 1700 + rep)))]
+        batches.append(keys)
+    want = [oracle.answer_batch([oracle.key_from_wire(dp.key_serialize(k)) for k in keys], T, threads=8)
+            for keys in batches]
+    got, nxt = [], 0
+    for keys in batches:
+        if nxt - len(got) == depth:  # pipeline full
+            with pytest.raises(dp.DpfError):
+                srv.submit(dp.keys_to_wire(keys))
+            got.append(srv.collect())
+        srv.submit(dp.keys_to_wire(keys))
+        nxt += 1
+    with pytest.raises(dp.DpfError):
+        srv.run(dp.keys_to_wire(batches[0]))
+    while len(got) < nxt:
+        got.append(srv.collect())
+    with pytest.raises(dp.DpfError):
+        srv.collect()  # nothing in flight
+    for g, w in zip(got, want):
+        np.testing.assert_array_equal(g, w)
+    np.testing.assert_array_equal(srv.run(dp.keys_to_wire(batches[1])), want[1])
+    srv.close()
+
+
 def test_random_shapes_fuzz(dp, oracle):
     """Seeded random shapes through every entry point family (IMAD and tcgen05
     incl. pairs and padded D, all three schemes, shards with ragged ends, the
