@@ -27,7 +27,10 @@ namespace dpfpir {
 namespace dev {
 
 // Logical right shift.  (Moving these to the FMA pipe as IMAD.HI -- the FMA
-// pipe idles at 7 % here -- measured no faster: IMAD.HI is half-rate.)
+// pipe idles at 7 % here -- measured no faster, also with the multiplier in
+// constant memory so that it stays a multiply (r02: 48 of ~410 ops per round
+// moved, 4,124 vs 4,149 QPS at c3): the rounds are issue-bound as much as
+// ALU-bound, so only fewer instructions help.)
 template <int K>
 __device__ __forceinline__ uint32_t shr_fma(uint32_t x) {
   return x >> K;
