@@ -468,6 +468,10 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
   } else if (warp < NP + NC) {
     // ------------------------------------------------ MMA issuer + epilogue
     const uint32_t q = warp - NP;  // TMEM lane quarter
+    // The MMA issuer: with 4 epilogue warps the one on SMSP 1 (hardware warp
+    // NP + 1), so that SMSP 0 (which also hosts the T loader, NP + 4) is not
+    // the one SMSP with two polling warps next to its 4 producers.
+    constexpr uint32_t MQ = NC == 4 ? 1u : 0u;
     const uint32_t n_cc = Kw / 32;
     const uint32_t idesc = umma_idesc_u8(Ktp, PAIR ? 256u : 128u);
     const uint32_t b_lbo = (p.Kt >> 3) * 128u;  // this CTA's Kt keys of the B operand
@@ -482,7 +486,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
       const GroupDesc g = group_of(p, item);
       const uint32_t kt = (item - g.item_base) % g.n_ktiles;
       const bool last = !run_continues(p, g, kt, item + stride);
-      if (q == 0 && rank == 0) {
+      if (q == MQ && rank == 0) {
         if (fresh && nf > 0) {  // epilogue(s) drained the accumulators
           if (PAIR) mbar_wait_cluster(accempty, (nf - 1) & 1);
           else mbar_wait(accempty, (nf - 1) & 1);
@@ -525,7 +529,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
           if (last && win + 1 == g.nwin) umma_commit_elect<PAIR>(accfull);  // run's accumulators complete
           __syncwarp();
         }
-      } else if (q == 0) {
+      } else if (q == MQ) {
         // PAIR peer: forward this CTA's y-FULL and T-FULL events to the leader
         for (uint32_t win = 0; win < g.nwin; ++win, ++wseq) {
           const uint32_t ys = wseq % NSY;
@@ -548,7 +552,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
       } else {
         // epilogue: all NC warps, TMEM lanes 32q..32q+31 = columns d.  Only the
         // MMA warp polls the commit barrier; the others sleep in bar.sync.
-        if (q == 0) mbar_wait(accfull, nf & 1);
+        if (q == MQ) mbar_wait(accfull, nf & 1);
         ++nf;
         named_sync(NSY + 1, 32 * NC);
         tc_fence_after();
