@@ -45,7 +45,10 @@ constexpr uint32_t kTcTStageBytes = 16384;  // 32 leaves x 128 columns x 4 limbs
 // early termination 0.712 -> 0.761 (c3) / 0.763 -> 0.799 (t5) of the ALU
 // roofline; the standard scheme slightly slower (0.905 -> 0.895 at t5), so
 // it keeps the dedicated warps.
-__host__ __device__ constexpr int tc_extra_warps(bool epip) { return epip ? 2 : 5; }  // MMA (+ epilogue) and loader warps
+// The standard scheme's T loader runs in the epilogue warp on SMSP 3 (it
+// idles between accumulator runs): NP + 4 warps, at most 5 per SMSP, so the
+// per-thread register cap is 96 instead of 80.
+__host__ __device__ constexpr int tc_extra_warps(bool epip) { return epip ? 2 : 4; }  // MMA (+ epilogue) [+ loader]
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -353,6 +356,39 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
     }
   };
 
+  // T loader for one work item: per (window, 32-leaf chunk, d-tile), 4 nodes
+  // x one 4 KB packed block into the T ring (tseq: this warp's ring position).
+  auto load_item = [&](uint32_t item, uint32_t &tseq) {
+    const uint32_t n_cc = Kw / 32;
+    const GroupDesc g = group_of(p, item);
+    const uint64_t pend = g.r0a + g.packed_rows;
+    const uint8_t *packed = reinterpret_cast<const uint8_t *>(g.T);
+    const uint32_t ng = (item - g.item_base) / g.n_ktiles;
+    for (uint32_t win = 0; win < g.nwin; ++win) {
+      for (uint32_t cc = 0; cc < n_cc; ++cc) {
+        // lane j < 4: window leaves [32cc + 8j, +8) = rows [s0, s0 + 8) of
+        // one node (one packed block): node (32cc + 8j) / W2, offset % W2
+        const uint32_t kw0 = 32 * cc + 8 * (lane & 3);
+        const uint64_t node = uint64_t(ng) * p.Ft + kw0 / W2;
+        const uint64_t s0 = ((g.lo_f + node) << (g.m + V)) + uint64_t(W2) * win + kw0 % W2;
+        const bool ok = lane < 4 && node < g.F && s0 >= g.r0a && s0 < pend;
+        const uint32_t total = __popc(__ballot_sync(0xFFFFFFFFu, ok)) * 4096u;
+        for (uint32_t dt = 0; dt < n_dt; ++dt, ++tseq) {
+          const uint32_t ts = tseq % NST, tuse = tseq / NST;
+          if (tuse > 0) {
+            if (tp.loader_spin) mbar_wait(&tempty[ts], (tuse - 1) & 1);
+            else mbar_wait_backoff(&tempty[ts], (tuse - 1) & 1);
+          }
+          if (lane == 0) mbar_arrive_expect_tx(&tfull[ts], total);
+          __syncwarp();
+          if (ok)
+            bulk_g2s(tbuf + ts * kTcTStageBytes + lane * 4096u,
+                     packed + ((s0 - g.r0a) >> 3) * (32ull * Dp) + (dt0 + dt) * 4096ull, 4096u, &tfull[ts]);
+        }
+      }
+    }
+  };
+
   if (warp < NP) {
     // ------------------------------------------------------------ producers
     // Depth-first over the depth-m subtree: descend to the leaf-parent level
@@ -472,6 +508,8 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
     // NP + 1), so that SMSP 0 (which also hosts the T loader, NP + 4) is not
     // the one SMSP with two polling warps next to its 4 producers.
     constexpr uint32_t MQ = NC == 4 ? 1u : 0u;
+    constexpr uint32_t LQ = 3u;  // standard scheme: this epilogue warp (SMSP 3) is also the T loader
+    uint32_t ltseq = 0;          // its T-ring position
     const uint32_t n_cc = Kw / 32;
     const uint32_t idesc = umma_idesc_u8(Ktp, PAIR ? 256u : 128u);
     const uint32_t b_lbo = (p.Kt >> 3) * 128u;  // this CTA's Kt keys of the B operand
@@ -486,6 +524,9 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
       const GroupDesc g = group_of(p, item);
       const uint32_t kt = (item - g.item_base) % g.n_ktiles;
       const bool last = !run_continues(p, g, kt, item + stride);
+      // (the loader runs up to the T ring's depth ahead of the MMAs; at the end
+      // of a run it joins the epilogue once the run's last T entries are issued)
+      if (!EPIP && q == LQ) load_item(item, ltseq);
       if (q == MQ && rank == 0) {
         if (fresh && nf > 0) {  // epilogue(s) drained the accumulators
           if (PAIR) mbar_wait_cluster(accempty, (nf - 1) & 1);
@@ -561,38 +602,9 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
     }
   } else {
     // ------------------------------------------------------------ T loader
-    // Per (window, 32-leaf chunk, d-tile): 4 nodes x one 4 KB packed block.
+    // (early termination: its own warp; the standard scheme: epilogue warp LQ)
     uint32_t tseq = 0;
-    const uint32_t n_cc = Kw / 32;
-    for (uint32_t item = first; item < p.n_items; item += stride) {
-      const GroupDesc g = group_of(p, item);
-      const uint64_t pend = g.r0a + g.packed_rows;
-      const uint8_t *packed = reinterpret_cast<const uint8_t *>(g.T);
-      const uint32_t ng = (item - g.item_base) / g.n_ktiles;
-      for (uint32_t win = 0; win < g.nwin; ++win) {
-        for (uint32_t cc = 0; cc < n_cc; ++cc) {
-          // lane j < 4: window leaves [32cc + 8j, +8) = rows [s0, s0 + 8) of
-          // one node (one packed block): node (32cc + 8j) / W2, offset % W2
-          const uint32_t kw0 = 32 * cc + 8 * (lane & 3);
-          const uint64_t node = uint64_t(ng) * p.Ft + kw0 / W2;
-          const uint64_t s0 = ((g.lo_f + node) << (g.m + V)) + uint64_t(W2) * win + kw0 % W2;
-          const bool ok = lane < 4 && node < g.F && s0 >= g.r0a && s0 < pend;
-          const uint32_t total = __popc(__ballot_sync(0xFFFFFFFFu, ok)) * 4096u;
-          for (uint32_t dt = 0; dt < n_dt; ++dt, ++tseq) {
-            const uint32_t ts = tseq % NST, tuse = tseq / NST;
-            if (tuse > 0) {
-              if (tp.loader_spin) mbar_wait(&tempty[ts], (tuse - 1) & 1);
-              else mbar_wait_backoff(&tempty[ts], (tuse - 1) & 1);
-            }
-            if (lane == 0) mbar_arrive_expect_tx(&tfull[ts], total);
-            __syncwarp();
-            if (ok)
-              bulk_g2s(tbuf + ts * kTcTStageBytes + lane * 4096u,
-                       packed + ((s0 - g.r0a) >> 3) * (32ull * Dp) + (dt0 + dt) * 4096ull, 4096u, &tfull[ts]);
-          }
-        }
-      }
-    }
+    for (uint32_t item = first; item < p.n_items; item += stride) load_item(item, tseq);
   }
   tc_fence_before();
   __syncthreads();
