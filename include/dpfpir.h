@@ -383,7 +383,8 @@ typedef struct dpf_eval_stats {
   uint32_t work_items;    /* fused-kernel work items */
   uint32_t grid;          /* fused-kernel CTAs */
   uint32_t kernel_id;     /* the fused-kernel instantiation: bit 0 tcgen05, bit 1 CTA pair, bit 2 producer
-                             epilogue, bits 4-7 y-ring stages, bits 8-11 PRF, bits 12-17 producer warps,
+                             epilogue, bit 3 small-batch key mapping, bits 4-7 y-ring stages, bits 8-11 PRF,
+                             bits 12-17 producer warps,
                              bits 18-23 / 24-31 IMAD consumer keys per warp / column words per lane */
 } dpf_eval_stats;
 int dpf_last_eval_stats(dpf_eval_stats *out);

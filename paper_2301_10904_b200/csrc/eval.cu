@@ -1207,12 +1207,15 @@ thread_local dpf_eval_stats g_stats{};
 
 // dpf_eval_stats.kernel_id: which fused-kernel instantiation a plan launches
 // (include/dpfpir.h): bit 0 tcgen05, bit 1 CTA pair, bit 2 producer epilogue,
-// bits 4-7 y-ring stages, bits 8-11 PRF, bits 12-17 producer warps, bits
-// 18-23 consumer keys per warp (IMAD), bits 24-31 consumer column words (IMAD).
+// bit 3 small-batch key mapping, bits 4-7 y-ring stages, bits 8-11 PRF, bits
+// 12-17 producer warps, bits 18-23 consumer keys per warp (IMAD), bits 24-31
+// consumer column words (IMAD).
 uint32_t kernel_id(const Plan &pl) {
   if (pl.tc) {
     const uint32_t epip = pl.prf == DPF_PRF_CHACHA20_ET;
-    return 1u | (uint32_t(pl.pair) << 1) | (epip << 2) | (pl.nsy << 4) | (pl.prf << 8) | (16u << 12);
+    const uint32_t smallb = pl.Kr && pl.Kr < pl.Kt;
+    return 1u | (uint32_t(pl.pair) << 1) | (epip << 2) | (smallb << 3) | (pl.nsy << 4) | (pl.prf << 8) |
+           (16u << 12);
   }
   return (pl.prf << 8) | (uint32_t(pl.kc.NP) << 12) | (uint32_t(pl.kc.KPW) << 18) | (uint32_t(pl.kc.CPL) << 24);
 }

@@ -632,8 +632,8 @@ def kernel_name(kernel_id: int) -> str:
         (kernel_id >> 8) & 0xF, "?")
     np_ = (kernel_id >> 12) & 0x3F
     if kernel_id & 1:
-        return "fused_eval_tc_kernel<%s, %d, %d, 4, %d, %d>" % (prf, np_, (kernel_id >> 4) & 0xF, (kernel_id >> 1) & 1,
-                                                                 (kernel_id >> 2) & 1)
+        return "fused_eval_tc_kernel<%s, %d, %d, 4, %d, %d, %d>" % (
+            prf, np_, (kernel_id >> 4) & 0xF, (kernel_id >> 1) & 1, (kernel_id >> 2) & 1, (kernel_id >> 3) & 1)
     return "fused_eval_kernel<%s, %d, 4, %d, %d>" % (prf, np_, (kernel_id >> 18) & 0x3F, kernel_id >> 24)
 
 
