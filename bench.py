@@ -56,10 +56,11 @@ sys.path.insert(0, ROOT)
 import synth  # noqa: E402
 
 # ALU-pipe ops per PRF unit.  ChaCha20 = 320 XOR + 320
-# rotate per block (80 quarter rounds; the adds run on the FMA pipe).  AES-128:
-# the circuit count of one tree node (two encryptions sharing one key
-# schedule), derived in DESIGN.md §7 from the gate counts of the published
-# circuits, independent of this implementation's instruction stream.
+# rotate per block (80 quarter rounds; the adds run on the FMA pipe).  AES-128
+# runs table-driven (S-box/T-table lookups in shared memory), so its bound is
+# the lookup count per tree node (aes_lookups_per_node) at one conflict-free
+# 32-lane LDS per clock per SM; the bitsliced circuit count
+# (aes_alu_ops_per_node) is kept as the table-free alternative's floor.
 ALU_OPS_PER_BLOCK = {"chacha20": 640, "chacha20_et": 640}
 # leaf rows per tree leaf: early termination (R20) ends the tree at final
 # nodes of 16 rows, each converted by one more ChaCha20 block (counter 1).
@@ -95,7 +96,20 @@ def aes_alu_ops_per_node() -> float:
     return gates / 32.0
 
 
-ALU_OPS_PER_BLOCK["aes128"] = aes_alu_ops_per_node()
+def aes_lookups_per_node() -> int:
+    """S-box evaluations of one AES-128 tree node (R8/R9: blocks 0^120||0 and
+    0^120||1 under the node seed, one shared key schedule), each one table
+    read in any table-driven AES (FIPS-197 5.1.1 SubBytes; the T-table form
+    folds ShiftRows/MixColumns into the same read, 5.1.2-5.1.3):
+      SubBytes    10 rounds x 16 bytes x 2 blocks, except that in round 1 the
+                  two states differ only in byte 15 (the plaintexts 0^120||c),
+                  so 16 + 1 distinct S-box inputs there
+      KeyExpand   10 rounds x 4 (SubWord)
+    = 17 + 9 x 32 + 40 = 345."""
+    return (16 + 1) + 9 * 32 + 10 * 4
+
+
+AES_LOOKUPS_PER_NODE = aes_lookups_per_node()
 
 
 def prf_code(dpfpir, name):
@@ -667,8 +681,11 @@ def oracle_leg(args, w, wire_host, share0, T_full, G):
 def roofline_of(args, w, rows, g, G, stats, kernel_ms, ms_per_step, value, use_packed):
     """The dominant (fused) kernel against whichever resource binds it:
     algorithmic work per launch / that resource's peak, the largest of
-      alu    = ALU-pipe ops of the PRF blocks (640 per ChaCha20 block; the
-               AES circuit count per node)            / 148 x 64 lanes x clock
+      alu    = ALU-pipe ops of the PRF blocks (640 per ChaCha20 block)
+                                                      / 148 x 64 lanes x clock
+      smem   = AES-128: table lookups of the PRF nodes (345 per node)
+                                                      / 148 x 32 lanes x clock
+               (one conflict-free LDS.32 per clock per SM)
       tensor = 10 u8 limb MACs x 2 ops per (key, row, column) of the
                contraction (tcgen05 path)             / 2 x the measured bf16
                dense peak (int8 = fp8 rate = 2 x bf16, B200_PROFILING.md)
@@ -681,16 +698,20 @@ def roofline_of(args, w, rows, g, G, stats, kernel_ms, ms_per_step, value, use_p
     # plus one Convert block per final node with early termination
     fused_blocks = w.B * ((rows >> v) >> m) * ((1 << m) - 1 + ((1 << m) if v else 0))
     kern_avg_ms = sum(kernel_ms) / len(kernel_ms)
-    alu_peak = 148 * 64 * pk["sm_max_mhz"] * 1e6  # ALU-pipe lane-ops/s
-    ops_per_block = ALU_OPS_PER_BLOCK[args.prf]
+    aes = args.prf == "aes128"
+    # the PRF's binding unit: ALU-pipe ops (ChaCha20) or SMEM table lookups (AES)
+    prf_res = "smem" if aes else "alu"
+    alu_peak = 148 * (32 if aes else 64) * pk["sm_max_mhz"] * 1e6  # lanes/s of that unit
+    ops_per_block = AES_LOOKUPS_PER_NODE if aes else ALU_OPS_PER_BLOCK[args.prf]
     alu_work = ops_per_block * fused_blocks
     tensor_peak = 2.0 * pk["bf16_tflops"] * 1e12
     tensor_work = 2.0 * 10 * w.B * rows * w.D if use_packed else 0.0
     hbm_peak = pk["hbm_gbs"] * 1e9
     hbm_work = 4.0 * rows * w.D
-    bounds = {"alu": alu_work / alu_peak, "tensor": tensor_work / tensor_peak, "hbm": hbm_work / hbm_peak}
+    bounds = {prf_res: alu_work / alu_peak, "tensor": tensor_work / tensor_peak, "hbm": hbm_work / hbm_peak}
     bound = max(bounds, key=bounds.get)
-    work, peak, unit = {"alu": (alu_work, alu_peak, "Tops/s"), "tensor": (tensor_work, tensor_peak, "TOPS (int8)"),
+    work, peak, unit = {prf_res: (alu_work, alu_peak, "T lookups/s" if aes else "Tops/s"),
+                        "tensor": (tensor_work, tensor_peak, "TOPS (int8)"),
                         "hbm": (hbm_work, hbm_peak, "GB/s")}[bound]
     scale = 1e-9 if bound == "hbm" else 1e-12
     achieved = work / (kern_avg_ms * 1e-3)
@@ -708,10 +729,12 @@ def roofline_of(args, w, rows, g, G, stats, kernel_ms, ms_per_step, value, use_p
         "bounds_ms": {k: v_ * 1e3 for k, v_ in bounds.items()},
         "kernel": "fused_eval_tc_kernel" if use_packed else "fused_eval_kernel", "kernel_ms": kern_avg_ms,
         "kernel_share_of_step": kern_avg_ms / ms_per_step,
-        "ops": ("%g ALU-pipe ops per %s x %d per launch" %
-                (ops_per_block, "AES-128 node (circuit count, DESIGN.md §7)" if args.prf == "aes128" else
-                 "ChaCha20 block (LOP3 xor + SHF rotate)", fused_blocks)),
-        "peak_basis": {"alu": "148 SMs x 64 ALU lanes/clk x %.0f MHz" % pk["sm_max_mhz"],
+        "ops": ("%d SMEM table lookups per AES-128 node (S-box evaluations, DESIGN.md §7) x %d per launch" %
+                (ops_per_block, fused_blocks) if aes else
+                "%g ALU-pipe ops per ChaCha20 block (LOP3 xor + SHF rotate) x %d per launch" %
+                (ops_per_block, fused_blocks)),
+        "peak_basis": {prf_res: ("148 SMs x 32 LDS lanes/clk x %.0f MHz" if aes else
+                                 "148 SMs x 64 ALU lanes/clk x %.0f MHz") % pk["sm_max_mhz"],
                        "tensor": "2 x %.1f TFLOP/s bf16 (%s)" % (pk["bf16_tflops"], pk["source"]),
                        "hbm": "%.0f GB/s (%s)" % (pk["hbm_gbs"], pk["source"])},
         "qps_at_roofline": qps_roof, "frac_qps": value / qps_roof,

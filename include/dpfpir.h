@@ -44,8 +44,9 @@ extern "C" {
 #define DPF_KEY_VERSION 1
 
 /* PRF of the tree: ChaCha20 (Table 5; the default hot-path
- * PRF) or AES-128 (the paper's baseline PRF, Table 4), both table-free
- * on the device (AES bitsliced).  PRF_s(c): ChaCha20 keyed by s || 0^128,
+ * PRF) or AES-128 (the paper's baseline PRF, Table 4; on the device
+ * through lane-replicated T-tables in shared memory, one conflict-free lookup
+ * per S-box evaluation, so no data-dependent timing).  PRF_s(c): ChaCha20 keyed by s || 0^128,
  * bytes [16c, 16c+16) of block 0; AES-128 keyed by s on block 0^120 || c. */
 enum dpf_prf { DPF_PRF_CHACHA20 = 1, DPF_PRF_AES128 = 2, DPF_PRF_CHACHA20_ET = 3 };
 
@@ -171,8 +172,7 @@ int dpf_eval_batch_shard(const dpf_key *keys, uint32_t B, const uint32_t *table_
  * base), e.g. received by the server straight into HBM; `prf` (enum dpf_prf)
  * must be the keys' PRF.  The keys are NOT re-validated (device memory is not read by
  * the host): callers validate at dpf_key_deserialize time.  No host->device
- * traffic; fully asynchronous (AES keys are bitsliced into a private copy in
- * the workspace). */
+ * traffic; fully asynchronous; the keys are read in place (never modified). */
 int dpf_eval_batch_wire(const uint8_t *keys_wire_dev, uint32_t B, uint32_t log_n, uint32_t prf,
                         const uint32_t *table_shard,
                         uint64_t row_begin, uint64_t row_count, uint32_t D, uint32_t *partial_shares,
@@ -315,7 +315,7 @@ size_t dpf_eval_grouped_workspace_bytes(const dpf_eval_group *groups, uint32_t n
 
 /* Evaluate n_groups groups (host array of descriptors; the device buffers
  * they point to stay caller-owned) with one zeroing, one top-BFS and one
- * fused launch (+ one key-bitslicing launch per group for AES).  Asynchronous
+ * fused launch (deep frontiers: + one launch per level beyond 10).  Asynchronous
  * on `stream`.  Errors: DPF_EINVAL, DPF_ENOMEM, DPF_EUNSUPPORTED, DPF_ECUDA. */
 int dpf_eval_grouped(const dpf_eval_group *groups, uint32_t n_groups, uint32_t D, uint32_t prf, void *workspace,
                      size_t workspace_bytes, void *stream);

@@ -1,197 +1,197 @@
-// aes_dev.cuh -- table-free bitsliced AES-128 tree PRF for sm_100a.
+// aes_dev.cuh -- AES-128 tree PRF for sm_100a: lane-replicated T-tables in
+// shared memory.
 //
 // PRF_s(c) = AES-128 with key s on the block 0^120 || c (reading R8 for AES;
 // FIPS-197; the paper's baseline PRF, Table 4).  Each internal
-// node costs one key schedule and two encryptions (R9).
+// node costs one key schedule and two encryptions (R9).  Seeds stay plain
+// 16-byte values (LE words = FIPS-197 state columns: word j = bytes 4j..4j+3,
+// row r = byte r), exactly as in the ChaCha20 path: roots, codewords, the
+// frontier and the DFS stack need no conversion.
 //
-// Representation ("BS seed"): a 16-byte seed is kept bitsliced as 8 planes of
-// 16 bits -- plane p holds bit p of byte i at bit i (i = r + 4c, FIPS-197
-// state order) -- packed two planes per word into a uint4:
-//     word k = plane 2k | plane (2k+1) << 16.
-// A BS seed is 16 bytes like a plain seed, so the DFS stack, the frontier and
-// the key layout are unchanged; roots and codewords are bitsliced once per
-// batch by aes_bitslice_keys_kernel.  lsb(s) (R5) is bit 0 of byte 0 = bit 0
-// of word 0 in both representations.
+// Round function (FIPS-197 5.1, the standard T-table form): column j of the
+// next state is
+//     T0[a_j.b0] ^ T1[a_{j+1}.b1] ^ T2[a_{j+2}.b2] ^ T3[a_{j+3}.b3] ^ k_j
+// with T0[x] = (2S(x), S(x), S(x), 3S(x)) (bytes 0..3) and Tt = rotl(T0, 8t).
+// Only T0 and T1 are stored; T2, T3 = rot16(T0, T1), so one byte permute per
+// column:  T0[.] ^ T1[.] ^ rot16(T0[.] ^ T1[.] ^ rot16(k_j)).  The final round
+// takes S(x) from byte 1 of T0[x] (bytes 2, 3 of T1[x]); the key schedule's
+// SubWord likewise.
 //
-// The two encryptions of a node run together: in a 32-bit plane word the low
-// half is block c = 0, the high half block c = 1.  SubBytes is the generated
-// tower-field circuit (aes_sbox_bs.cuh, verified on all 256 inputs); ShiftRows
-// and MixColumns are rotations inside the 16-bit halves (one AES column = one
-// nibble).  No memory lookups: constant-time, table-free.
+// Layout (64 KB at the start of the kernel's dynamic shared memory): entry e
+// of table t holds 32 copies, one per lane:  address e*256 + t*128 + 4*lane.
+// Every lane reads its own bank whatever the index, so each lookup is one
+// conflict-free LDS and the timing does not depend on the (secret) seed bytes.
+// The address is ONE byte permute: (byte k of x) << 8 | (lane*4 + 128 t),
+// taken from x and a per-lane constant, added to the dynamic-SMEM base by the
+// LDS itself ([R + UR]).  Per node: 345 table lookups (16 per block-round, 1
+// for the second block's round 1, whose plaintext differs from the first only
+// in byte 15, 4 per key-schedule round).
+//
+// Replaces the bitsliced table-free formulation of round 1 (4,075 ALU ops per
+// node; 4,172 QPS at c3): ~725 ALU ops + 345 LDS per node.
 #pragma once
 #include <cstdint>
-
-#include "aes_sbox_bs.cuh"
 
 namespace dpfpir {
 namespace dev {
 
-// Logical right shift.  (Moving these to the FMA pipe as IMAD.HI -- the FMA
-// pipe idles at 7 % here -- measured no faster, also with the multiplier in
-// constant memory so that it stays a multiply (r02: 48 of ~410 ops per round
-// moved, 4,124 vs 4,149 QPS at c3): the rounds are issue-bound as much as
-// ALU-bound, so only fewer instructions help.)
-template <int K>
-__device__ __forceinline__ uint32_t shr_fma(uint32_t x) {
-  return x >> K;
-}
+constexpr uint32_t kAesSmemBytes = 65536;  // T0 and T1, 32 lane copies each
 
-// rotate every nibble down by k rows: new bit (r, c) = old bit ((r + k) % 4, c)
-template <int K>
-__device__ __forceinline__ uint32_t nib_rot(uint32_t x) {
-  constexpr uint32_t lo = (K == 1) ? 0x77777777u : (K == 2) ? 0x33333333u : 0x11111111u;
-  return (shr_fma<K>(x) & lo) | ((x << (4 - K)) & ~lo);
-}
-
-// rotate each 16-bit half right by 4*K bits: new column c = old column c + K
-template <int K>
-__device__ __forceinline__ uint32_t half_rot(uint32_t x) {
-  if constexpr (K == 2) {
-    return __byte_perm(x, x, 0x2301);
-  } else {
-    constexpr uint32_t m = (K == 1) ? 0x0FFF0FFFu : 0x000F000Fu;
-    return (shr_fma<4 * K>(x) & m) | ((x << (16 - 4 * K)) & ~m);
-  }
-}
-
-// ShiftRows (FIPS-197 5.1.2): new (r, c) = old (r, c + r); row r = bits r, r+4, r+8, r+12.
-__device__ __forceinline__ uint32_t shift_rows(uint32_t x) {
-  const uint32_t r1 = half_rot<1>(x), r2 = half_rot<2>(x), r3 = half_rot<3>(x);
-  uint32_t o = (x & 0x11111111u) | (r1 & ~0x11111111u);
-  o = (o & 0x33333333u) | (r2 & ~0x33333333u);
-  return (o & 0x77777777u) | (r3 & ~0x77777777u);
-}
-
-// MixColumns (FIPS-197 5.1.3) on 8 planes: out = 2a + 3a' + a'' + a''' with
-// a^(k) the byte k rows below; = xtime(u) + a' + rot2(u), u = a + a'.
-__device__ __forceinline__ void mix_columns(uint32_t (&x)[8]) {
-  uint32_t r1[8], u[8];
-#pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    r1[p] = nib_rot<1>(x[p]);
-    u[p] = x[p] ^ r1[p];
-  }
-  // xtime(u): bit p <- bit p-1, and bit 7 feeds bits 0, 1, 3, 4 (x^8 = x^4 + x^3 + x + 1)
-  uint32_t xt[8];
-  xt[0] = u[7];
-  xt[1] = u[0] ^ u[7];
-  xt[2] = u[1];
-  xt[3] = u[2] ^ u[7];
-  xt[4] = u[3] ^ u[7];
-  xt[5] = u[4];
-  xt[6] = u[5];
-  xt[7] = u[6];
-#pragma unroll
-  for (int p = 0; p < 8; ++p) x[p] = xt[p] ^ r1[p] ^ nib_rot<2>(u[p]);
-}
-
-// Rcon (FIPS-197 5.2) of rounds 1..10 as per-plane masks: Rcon enters row 0
-// of every column of the new round key, i.e. bits 0, 4, 8, 12 of both halves.
-__constant__ uint32_t c_rcon_mask[10][8] = {
-#define DPF_RC(v) {(v)&1 ? 0x11111111u : 0u, (v)&2 ? 0x11111111u : 0u, (v)&4 ? 0x11111111u : 0u, \
-                   (v)&8 ? 0x11111111u : 0u, (v)&16 ? 0x11111111u : 0u, (v)&32 ? 0x11111111u : 0u, \
-                   (v)&64 ? 0x11111111u : 0u, (v)&128 ? 0x11111111u : 0u}
-    DPF_RC(0x01), DPF_RC(0x02), DPF_RC(0x04), DPF_RC(0x08), DPF_RC(0x10),
-    DPF_RC(0x20), DPF_RC(0x40), DPF_RC(0x80), DPF_RC(0x1B), DPF_RC(0x36)
-#undef DPF_RC
+// ---- T0 from the S-box, computed at compile time (FIPS-197 5.1.1: S(x) =
+// affine(x^-1) in GF(2^8) mod x^8 + x^4 + x^3 + x + 1).
+struct AesT0 {
+  uint32_t t[256];
 };
-
-// Next round key (FIPS-197 5.2) on duplicated 16-bit planes (both halves
-// equal): column j' = (col 0 ^ ... ^ col j) ^ t,
-// t = SubWord(RotWord(col 3)) ^ Rcon.
-__device__ __forceinline__ void next_round_key(uint32_t (&k)[8], int round) {
-  uint32_t s[8];
-#pragma unroll
-  for (int p = 0; p < 8; ++p) s[p] = k[p];
-  aes_sbox_bs(s);
-#pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    // RotWord: t row r = S(col 3, row r+1); col 3 = bits 12..15 of each half
-    const uint32_t t = (shr_fma<13>(s[p]) & 0x00070007u) | (shr_fma<9>(s[p]) & 0x00080008u);
-    uint32_t q = k[p] ^ ((k[p] << 4) & 0xFFF0FFF0u);  // inclusive prefix XOR over columns
-    q ^= (q << 8) & 0xFF00FF00u;
-    k[p] = q ^ (t * 0x1111u) ^ c_rcon_mask[round - 1][p];
+constexpr uint8_t aes_gf_mul(uint8_t a, uint8_t b) {
+  uint8_t r = 0;
+  for (int i = 0; i < 8; ++i) {
+    if (b & 1) r = uint8_t(r ^ a);
+    const bool hi = (a & 0x80) != 0;
+    a = uint8_t(a << 1);
+    if (hi) a = uint8_t(a ^ 0x1B);
+    b = uint8_t(b >> 1);
   }
+  return r;
 }
-
-// Both children of BS seed s: AES_s(0^128) and AES_s(0^120 || 1), as BS seeds.
-__device__ __forceinline__ void aes_children_bs(const uint4 s, uint4 &c0, uint4 &c1) {
-  uint32_t k[8], x[8];
-  const uint32_t w[4] = {s.x, s.y, s.z, s.w};
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    k[2 * q] = __byte_perm(w[q], 0, 0x1010);      // plane 2q duplicated into both halves
-    k[2 * q + 1] = __byte_perm(w[q], 0, 0x3232);  // plane 2q+1 duplicated
-  }
-#pragma unroll
-  for (int p = 0; p < 8; ++p) x[p] = k[p];  // AddRoundKey(0) on plaintexts 0 and 1
-  x[0] ^= 0x80000000u;                      // block 1: byte 15 = 0x01 -> plane 0, bit 15 of the high half
-#pragma unroll 1
-  for (int round = 1; round <= 10; ++round) {
-    aes_sbox_bs(x);
-#pragma unroll
-    for (int p = 0; p < 8; ++p) x[p] = shift_rows(x[p]);
-    if (round != 10) mix_columns(x);
-    next_round_key(k, round);
-#pragma unroll
-    for (int p = 0; p < 8; ++p) x[p] ^= k[p];
-  }
-  c0 = make_uint4(__byte_perm(x[0], x[1], 0x5410), __byte_perm(x[2], x[3], 0x5410),
-                  __byte_perm(x[4], x[5], 0x5410), __byte_perm(x[6], x[7], 0x5410));
-  c1 = make_uint4(__byte_perm(x[0], x[1], 0x7632), __byte_perm(x[2], x[3], 0x7632),
-                  __byte_perm(x[4], x[5], 0x7632), __byte_perm(x[6], x[7], 0x7632));
-}
-
-// plain 16-byte seed (LE words) -> BS seed
-__device__ __forceinline__ uint4 bs_from_bytes(uint4 s) {
-  const uint32_t w[4] = {s.x, s.y, s.z, s.w};
-  uint32_t plane[8];
-#pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    uint32_t acc = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      // bits p, 8+p, 16+p, 24+p of word q -> bits 4q .. 4q+3
-      const uint32_t t = (w[q] >> p) & 0x01010101u;
-      acc |= (((t * 0x00204081u) >> 21) & 0xFu) << (4 * q);
+constexpr uint8_t aes_sbox_ct(uint8_t x) {
+  uint8_t inv = 0;  // x^254 = x^-1 (0 -> 0)
+  if (x) {
+    uint8_t p = x;
+    inv = 1;
+    for (int e = 254; e; e >>= 1) {
+      if (e & 1) inv = aes_gf_mul(inv, p);
+      p = aes_gf_mul(p, p);
     }
-    plane[p] = acc;
   }
-  return make_uint4(plane[0] | (plane[1] << 16), plane[2] | (plane[3] << 16), plane[4] | (plane[5] << 16),
-                    plane[6] | (plane[7] << 16));
+  uint8_t s = inv;
+  for (int i = 1; i <= 4; ++i) s = uint8_t(s ^ uint8_t((inv << i) | (inv >> (8 - i))));
+  return uint8_t(s ^ 0x63);
+}
+constexpr AesT0 make_aes_t0() {
+  AesT0 r{};
+  for (int x = 0; x < 256; ++x) {
+    const uint8_t s = aes_sbox_ct(uint8_t(x));
+    const uint8_t s2 = aes_gf_mul(s, 2), s3 = uint8_t(s2 ^ s);
+    r.t[x] = uint32_t(s2) | uint32_t(s) << 8 | uint32_t(s) << 16 | uint32_t(s3) << 24;
+  }
+  return r;
+}
+static_assert(aes_sbox_ct(0x00) == 0x63 && aes_sbox_ct(0x53) == 0xED && aes_sbox_ct(0xFF) == 0x16,
+              "FIPS-197 S-box (Fig. 7)");
+__constant__ AesT0 c_aes_t0 = make_aes_t0();
+// Rcon of rounds 1..10 (FIPS-197 5.2)
+__constant__ uint32_t c_aes_rcon[10] = {0x01, 0x02, 0x04, 0x08, 0x10, 0x20, 0x40, 0x80, 0x1B, 0x36};
+
+// the kernels' dynamic shared memory (every extern __shared__ array aliases it)
+extern __shared__ __align__(128) uint8_t dpf_dyn_smem[];
+
+// Fill the lane-replicated tables; the caller synchronises the CTA before use.
+__device__ __forceinline__ void aes_tt_fill() {
+  uint4 *w = reinterpret_cast<uint4 *>(dpf_dyn_smem);
+  for (uint32_t i = threadIdx.x; i < kAesSmemBytes / 16; i += blockDim.x) {
+    const uint32_t e = i >> 4, t = (i >> 3) & 1;  // 16 uint4 per entry: 8 for T0, 8 for T1
+    const uint32_t v = c_aes_t0.t[e];
+    const uint32_t x = t ? __funnelshift_l(v, v, 8) : v;
+    w[i] = make_uint4(x, x, x, x);
+  }
 }
 
-// bytes 4..7 of a BS seed as a little-endian u32 (w1 of reading R6)
-__device__ __forceinline__ uint32_t bs_word1(uint4 s) {
-  const uint32_t w[4] = {s.x, s.y, s.z, s.w};
-  uint32_t out = 0;
+// Table word for byte K of x from table base l (= lane*4 for T0, +128 for T1)
+template <int K>
+__device__ __forceinline__ uint32_t aes_tl(uint32_t x, uint32_t l) {
+  const uint32_t off = __byte_perm(x, l, 0x5504u | (uint32_t(K) << 4));  // byte0 = l, byte1 = x.bK, bytes 2,3 = 0
+  return *reinterpret_cast<const uint32_t *>(dpf_dyn_smem + off);
+}
+__device__ __forceinline__ uint32_t rot16(uint32_t x) { return __byte_perm(x, 0, 0x1032); }
+
+// one full round on state a (columns a[0..3]) with kr = rot16(round key)
+__device__ __forceinline__ void aes_round(const uint32_t (&a)[4], uint32_t (&o)[4], const uint32_t (&kr)[4],
+                                          uint32_t l0, uint32_t l1) {
 #pragma unroll
-  for (int p = 0; p < 8; ++p) {
-    const uint32_t nib = (w[p >> 1] >> (16 * (p & 1) + 4)) & 0xFu;  // bytes 4..7 of plane p
-    out |= ((nib * 0x00204081u) & 0x01010101u) << p;
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t u = aes_tl<2>(a[(j + 2) & 3], l0) ^ aes_tl<3>(a[(j + 3) & 3], l1) ^ kr[j];
+    o[j] = aes_tl<0>(a[j], l0) ^ aes_tl<1>(a[(j + 1) & 3], l1) ^ rot16(u);
   }
-  return out;
 }
 
-struct PrfAesBs {
+// final round (no MixColumns): column j = S(a_j.b0), S(a_{j+1}.b1), S(a_{j+2}.b2), S(a_{j+3}.b3) ^ k_j
+__device__ __forceinline__ void aes_final_round(const uint32_t (&a)[4], uint32_t (&o)[4], const uint32_t (&k)[4],
+                                                uint32_t l0, uint32_t l1) {
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t v0 = aes_tl<0>(a[j], l0), v1 = aes_tl<1>(a[(j + 1) & 3], l0);  // S at byte 1 of T0
+    const uint32_t v2 = aes_tl<2>(a[(j + 2) & 3], l1), v3 = aes_tl<3>(a[(j + 3) & 3], l1);  // S at bytes 2, 3 of T1
+    const uint32_t lo = __byte_perm(v0, v1, 0x0051), hi = __byte_perm(v2, v3, 0x7200);
+    o[j] = __byte_perm(lo, hi, 0x7610) ^ k[j];
+  }
+}
+
+// next round key (FIPS-197 5.2): k0 ^= SubWord(RotWord(k3)) ^ Rcon; k_j ^= k_{j-1}
+__device__ __forceinline__ void aes_next_key(uint32_t (&k)[4], uint32_t rcon, uint32_t l0, uint32_t l1) {
+  // RotWord in LE words: bytes (b1, b2, b3, b0)
+  const uint32_t w1 = aes_tl<1>(k[3], l0), w2 = aes_tl<2>(k[3], l0);  // S at byte 1 (T0)
+  const uint32_t w3 = aes_tl<3>(k[3], l1), w0 = aes_tl<0>(k[3], l1);  // S at bytes 2, 3 (T1)
+  const uint32_t lo = __byte_perm(w1, w2, 0x0051), hi = __byte_perm(w3, w0, 0x7200);
+  k[0] ^= __byte_perm(lo, hi, 0x7610) ^ rcon;
+  k[1] ^= k[0];
+  k[2] ^= k[1];
+  k[3] ^= k[2];
+}
+
+// Both children of seed s: AES_s(0^128) and AES_s(0^120 || 1).
+__device__ __forceinline__ void aes_children_tt(const uint4 s, uint4 &c0, uint4 &c1) {
+  const uint32_t l0 = (threadIdx.x & 31u) << 2, l1 = l0 | 128u;
+  uint32_t k[4] = {s.x, s.y, s.z, s.w};
+  uint32_t a[4], b[4], kr[4];
+  // round 0: AddRoundKey on the plaintexts (block 1: byte 15 = 1 = byte 3 of column 3)
+  const uint32_t a3b = k[3] ^ 0x01000000u;
+  // round 1: only column 0 reads byte 15 (ShiftRows: row 3 of column 3 -> column 0)
+  aes_next_key(k, 1u, l0, l1);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) kr[j] = rot16(k[j]);
+  {
+    const uint32_t s0 = s.x, s1 = s.y, s2 = s.z, s3 = s.w;
+    const uint32_t p = aes_tl<0>(s0, l0) ^ aes_tl<1>(s1, l1);
+    const uint32_t q = aes_tl<2>(s2, l0) ^ kr[0];
+    a[0] = p ^ rot16(q ^ aes_tl<3>(s3, l1));
+    b[0] = p ^ rot16(q ^ aes_tl<3>(a3b, l1));
+    const uint32_t st[4] = {s0, s1, s2, s3};
+#pragma unroll
+    for (int j = 1; j < 4; ++j) {
+      const uint32_t u = aes_tl<2>(st[(j + 2) & 3], l0) ^ aes_tl<3>(st[(j + 3) & 3], l1) ^ kr[j];
+      a[j] = b[j] = aes_tl<0>(st[j], l0) ^ aes_tl<1>(st[(j + 1) & 3], l1) ^ rot16(u);
+    }
+  }
+#pragma unroll 1
+  for (uint32_t r = 2; r <= 9; ++r) {
+    aes_next_key(k, c_aes_rcon[r - 1], l0, l1);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) kr[j] = rot16(k[j]);
+    uint32_t ta[4], tb[4];
+    aes_round(a, ta, kr, l0, l1);
+    aes_round(b, tb, kr, l0, l1);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      a[j] = ta[j];
+      b[j] = tb[j];
+    }
+  }
+  aes_next_key(k, 0x36u, l0, l1);
+  uint32_t oa[4], ob[4];
+  aes_final_round(a, oa, k, l0, l1);
+  aes_final_round(b, ob, k, l0, l1);
+  c0 = make_uint4(oa[0], oa[1], oa[2], oa[3]);
+  c1 = make_uint4(ob[0], ob[1], ob[2], ob[3]);
+}
+
+struct PrfAesTt {
   static constexpr uint32_t id = 2;  // DPF_PRF_AES128
   static constexpr bool kEt = false;
-  static __device__ __forceinline__ void children(const uint4 s, uint4 &c0, uint4 &c1) { aes_children_bs(s, c0, c1); }
-  static __device__ __forceinline__ uint32_t word1(const uint4 s) { return bs_word1(s); }
+  static constexpr uint32_t kSmemBytes = kAesSmemBytes;  // at the start of dynamic SMEM
+  static __device__ __forceinline__ void init_smem() { aes_tt_fill(); }
+  static __device__ __forceinline__ void children(const uint4 s, uint4 &c0, uint4 &c1) { aes_children_tt(s, c0, c1); }
+  static __device__ __forceinline__ uint32_t word1(const uint4 s) { return s.y; }  // bytes 4..7 (R6)
 };
-
-// Prepare AES keys in the device key array: bitslice root and codewords in
-// place (wire layout kept: root at +16, cw column d at +32 + 64 (d-1)).
-__global__ void aes_bitslice_keys_kernel(uint8_t *__restrict__ keys, uint32_t kstride, uint32_t B, uint32_t n) {
-  const uint32_t per_key = 1 + 4 * n;  // root + 4 codewords per level
-  const uint64_t total = uint64_t(B) * per_key;
-  for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
-       i += uint64_t(gridDim.x) * blockDim.x) {
-    const uint32_t b = uint32_t(i / per_key), e = uint32_t(i % per_key);
-    uint4 *p = reinterpret_cast<uint4 *>(keys + uint64_t(b) * kstride + (e == 0 ? 16 : 32 + 16 * (e - 1)));
-    *p = bs_from_bytes(*p);
-  }
-}
 
 }  // namespace dev
 }  // namespace dpfpir

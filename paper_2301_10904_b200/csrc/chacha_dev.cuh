@@ -62,13 +62,17 @@ __device__ __forceinline__ uint4 xor4(uint4 a, uint4 b) {
   return make_uint4(a.x ^ b.x, a.y ^ b.y, a.z ^ b.z, a.w ^ b.w);
 }
 
-// PRF policies.  ChaCha20 works on plain seeds; AES-128 (aes_dev.cuh) on
-// bitsliced seeds.  Both keep lsb(s) (R5) at bit 0 of word 0.
+// PRF policies.  Both ChaCha20 and AES-128 (aes_dev.cuh) work on plain
+// seeds, lsb(s) (R5) at bit 0 of word 0.  kSmemBytes: shared memory the PRF
+// needs at the start of the kernel's dynamic SMEM (AES: its T-tables), filled
+// by init_smem() before the kernel's first CTA barrier.
 // kEt: early-terminated leaves (R20): the tree stops kEtBits levels above the
 // rows and each final node yields 2^kEtBits leaves from one Convert block.
 struct PrfChacha {
   static constexpr uint32_t id = 1;  // DPF_PRF_CHACHA20
   static constexpr bool kEt = false;
+  static constexpr uint32_t kSmemBytes = 0;
+  static __device__ __forceinline__ void init_smem() {}
   static __device__ __forceinline__ void children(const uint4 s, uint4 &c0, uint4 &c1) { chacha_children(s, c0, c1); }
   static __device__ __forceinline__ uint32_t word1(const uint4 s) { return s.y; }  // bytes 4..7 (R6)
 };
@@ -76,6 +80,8 @@ struct PrfChachaEt {
   static constexpr uint32_t id = 3;  // DPF_PRF_CHACHA20_ET
   static constexpr bool kEt = true;
   static constexpr uint32_t kEtBits = 4;
+  static constexpr uint32_t kSmemBytes = 0;
+  static __device__ __forceinline__ void init_smem() {}
   static __device__ __forceinline__ void children(const uint4 s, uint4 &c0, uint4 &c1) { chacha_children(s, c0, c1); }
   static __device__ __forceinline__ uint32_t word1(const uint4 s) { return s.y; }  // unused (no per-seed leaves)
 };

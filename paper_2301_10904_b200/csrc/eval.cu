@@ -165,6 +165,10 @@ __global__ void __launch_bounds__(256) expand_top_split_kernel(const uint8_t *__
                                                                uint4 *__restrict__ zero, uint64_t zero_vec) {
   __shared__ uint4 buf[2][1u << kTopSmemLevels];
   pdl_launch_dependents();
+  if constexpr (Prf::kSmemBytes != 0) {  // AES: T-tables in dynamic SMEM
+    Prf::init_smem();
+    __syncthreads();
+  }
   // a7's zeroing of the answers rides along (saves a launch per step)
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < zero_vec; i += uint64_t(gridDim.x) * blockDim.x)
     zero[i] = make_uint4(0, 0, 0, 0);
@@ -356,7 +360,8 @@ __device__ __forceinline__ void consume_window(const uint32_t *__restrict__ yb, 
 
 template <class Prf, int NP, int NC, int KPW, int CPL>
 __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const FusedParams p) {
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem_all[];
+  uint8_t *smem = smem_all + Prf::kSmemBytes;            // after the PRF's tables (AES)
   uint64_t *tfull = reinterpret_cast<uint64_t *>(smem);  // T ring [NST]: bulk-copy completion
   uint64_t *tempty = tfull + 8;                          // T ring [NST]: consumers done (count NC)
   constexpr uint32_t kFullThreads = 32 * (NP + NC), kEmptyThreads = 32 * (NP + NC);
@@ -376,6 +381,7 @@ __global__ void __launch_bounds__(32 * (NP + NC + 1), 1) fused_eval_kernel(const
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  Prf::init_smem();
   __syncthreads();
   pdl_wait_primary();  // the top BFS' frontier and zeroed answers
 
@@ -643,6 +649,7 @@ __global__ void __launch_bounds__(256) expand_top_grouped_kernel(const GroupDesc
   // level a lands where the remaining levels' ping-pong ends on `frontier`
   uint4 *out = (((f - a) & 1) ? g.frontier_alt : const_cast<uint4 *>(g.frontier)) + uint64_t(b) * g.cap;
   if (threadIdx.x == 0) buf[0][0] = key_root(key);
+  Prf::init_smem();
   __syncthreads();
   for (uint32_t k = 1; k <= a; ++k) {
     const uint64_t plo = r0 >> (n - (k - 1)), phi = (r1 - 1) >> (n - (k - 1));
@@ -668,6 +675,10 @@ __global__ void expand_level_grouped_kernel(const GroupDesc *__restrict__ groups
   const GroupDesc &g = groups[blockIdx.y];
   const uint32_t n = g.n, f = g.n - g.m;
   if (k > f) return;
+  if constexpr (Prf::kSmemBytes != 0) {  // (uniform per CTA: k, f)
+    Prf::init_smem();
+    __syncthreads();
+  }
   const uint64_t plo = g.nr0 >> (n - (k - 1)), phi = (g.nr1 - 1) >> (n - (k - 1));
   const uint64_t lo = g.nr0 >> (n - k), hi = (g.nr1 - 1) >> (n - k);
   const uint64_t np = phi - plo + 1, total = np * g.B;
@@ -688,6 +699,10 @@ __global__ void expand_level_grouped_kernel(const GroupDesc *__restrict__ groups
 template <class Prf>
 __global__ void eval_leaves_kernel(const uint8_t *__restrict__ keys, uint32_t kstride, uint32_t B, uint32_t n,
                                    uint32_t *__restrict__ leaves) {
+  if constexpr (Prf::kSmemBytes != 0) {
+    Prf::init_smem();
+    __syncthreads();
+  }
   const uint64_t N = 1ull << n;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < N * B;
        i += uint64_t(gridDim.x) * blockDim.x) {
@@ -727,6 +742,12 @@ constexpr uint32_t kTopSmemLevelsHost = 10;  // == dev::kTopSmemLevels
 constexpr uint32_t kTEntryBytes = 32 * 1024;   // IMAD kernel T-ring entry
 
 inline size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+// opt a kernel into more than 48 KB of dynamic shared memory
+template <class K>
+bool allow_dyn_smem(K *fn, size_t bytes) {
+  return bytes <= 48 * 1024 ||
+         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)) == cudaSuccess;
+}
 inline uint32_t pow2ceil(uint32_t v) {
   uint32_t r = 1;
   while (r < v) r <<= 1;
@@ -736,7 +757,7 @@ inline uint32_t pow2ceil(uint32_t v) {
 struct KernelChoice {
   int NP, KPW, CPL;
   void (*fn)(const dev::FusedParams);      // ChaCha20
-  void (*fn_aes)(const dev::FusedParams);  // AES-128 (bitsliced)
+  void (*fn_aes)(const dev::FusedParams);  // AES-128 (T-tables in SMEM)
   void (*fn_et)(const dev::FusedParams);   // ChaCha20, early-terminated leaves (R20)
   void (*get(uint32_t prf) const)(const dev::FusedParams) {
     return prf == DPF_PRF_AES128 ? fn_aes : prf == DPF_PRF_CHACHA20_ET ? fn_et : fn;
@@ -746,7 +767,7 @@ struct KernelChoice {
 template <int NP, int KPW, int CPL>
 KernelChoice choice() {
   return {NP, KPW, CPL, &dev::fused_eval_kernel<dev::PrfChacha, NP, kNC, KPW, CPL>,
-          &dev::fused_eval_kernel<dev::PrfAesBs, NP, kNC, KPW, CPL>,
+          &dev::fused_eval_kernel<dev::PrfAesTt, NP, kNC, KPW, CPL>,
           &dev::fused_eval_kernel<dev::PrfChachaEt, NP, kNC, KPW, CPL>};
 }
 
@@ -767,6 +788,7 @@ struct Plan {
   uint64_t r0, r1, F, lo_f, cap;
   uint32_t y_stage_words, t_stage_words, CN, n_chunks, NST;
   size_t smem_bytes;
+  size_t xsm;  // PRF shared memory at the start of the dynamic SMEM (AES T-tables), inside smem_bytes
   KernelChoice kc;
   uint64_t prf_blocks;
 };
@@ -895,6 +917,12 @@ uint32_t choose_grid(uint32_t n_items, uint32_t n_ktiles, uint32_t sms = 0) {
 // Rows per window unit: a leaf pair, or one final node with early termination.
 inline uint32_t unit_rows(const Plan &pl) { return pl.v ? (1u << pl.v) : 2u; }
 
+// dynamic SMEM per CTA left for the kernel's own regions (227 KB opt-in max
+// minus the PRF's tables)
+inline size_t smem_cap(const Plan &pl) { return 227 * 1024 - pl.xsm; }
+// the PRF's shared memory (dev::Prf*::kSmemBytes)
+inline size_t prf_smem(uint32_t prf) { return prf == DPF_PRF_AES128 ? dev::PrfAesTt::kSmemBytes : 0; }
+
 bool set_windows(Plan &pl, uint32_t W, uint32_t D, size_t stack_bytes) {
   pl.W = W;
   pl.R = unit_rows(pl) * W;
@@ -910,9 +938,9 @@ bool set_windows(Plan &pl, uint32_t W, uint32_t D, size_t stack_bytes) {
   pl.n_chunks = (pl.Ft + CN - 1) / CN;
   pl.t_stage_words = uint32_t(align_up(size_t(CN) * pl.R * D + pad, 32));
   const size_t fixed = 128 + 4 * 2 * size_t(pl.y_stage_words) + stack_bytes;
-  if (fixed + 2 * 4 * size_t(pl.t_stage_words) > 227 * 1024) return false;
-  pl.NST = uint32_t(std::min<size_t>(8, (227 * 1024 - fixed) / (4 * size_t(pl.t_stage_words))));
-  pl.smem_bytes = fixed + 4 * size_t(pl.NST) * pl.t_stage_words;
+  if (fixed + 2 * 4 * size_t(pl.t_stage_words) > smem_cap(pl)) return false;
+  pl.NST = uint32_t(std::min<size_t>(8, (smem_cap(pl) - fixed) / (4 * size_t(pl.t_stage_words))));
+  pl.smem_bytes = pl.xsm + fixed + 4 * size_t(pl.NST) * pl.t_stage_words;
   return true;
 }
 
@@ -935,8 +963,10 @@ uint64_t count_blocks(const Plan &pl, uint32_t B) {
   return uint64_t(B) * top + uint64_t(pl.n_items) * pl.tasks * per;
 }
 
-int make_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et = false) {
+int make_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et = false,
+              size_t xsm = 0) {
   std::memset(&pl, 0, sizeof pl);
+  pl.xsm = xsm;
   set_ranges(pl, log_n, r0, rows, et);
   const uint32_t n = pl.n;
   // Key tile: lanes <-> keys (Kt <= 32), remaining lanes <-> frontier nodes.
@@ -1048,13 +1078,14 @@ inline uint32_t tc_t_stages(uint32_t) { return 4u; }
 // columns fit the 512 TMEM columns; Ft = 512/Kt frontier nodes per item;
 // W = 4 leaf pairs per node per window (one 8-row packed block).
 int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et,
-                   uint32_t W, bool allow_kr = true, bool fallback_padded = true);
+                   uint32_t W, bool allow_kr = true, bool fallback_padded = true, size_t xsm = 0);
 
 // W (leaf pairs per node per window, standard scheme): 8 when the problem is
 // deep enough for subtrees of >= 4 levels (m >= 4 under W = 4), else 4 --
 // half the y-ring handshakes per block (measured c3 0.896 -> 0.912, t5 0.914
 // -> 0.925).  Early termination: one final node per window.
-int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et = false) {
+int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et = false,
+                 size_t xsm = 0) {
   if (et) {
     // Early termination: two final nodes per window with a 2-deep y ring
     // (half the y handshakes; measured c3 0.778 -> 0.784, t5 0.803 -> 0.815
@@ -1064,10 +1095,10 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
       const char *e = getenv("DPF_ET_W");
       return !(e && atoi(e) == 1);
     }();
-    if (allow2 && make_tc_plan_w(B, log_n, r0, rows, D, pl, true, 2) == DPF_OK) return DPF_OK;
-    return make_tc_plan_w(B, log_n, r0, rows, D, pl, true, 1);
+    if (allow2 && make_tc_plan_w(B, log_n, r0, rows, D, pl, true, 2, true, true, xsm) == DPF_OK) return DPF_OK;
+    return make_tc_plan_w(B, log_n, r0, rows, D, pl, true, 1, true, true, xsm);
   }
-  int rc = make_tc_plan_w(B, log_n, r0, rows, D, pl, false, 4);
+  int rc = make_tc_plan_w(B, log_n, r0, rows, D, pl, false, 4, true, true, xsm);
   if (rc != DPF_OK || pl.m < 4) return rc;
   static const bool allow8 = [] {  // DPF_TC_W=4 pins the 4-leaf-pair window (tuning)
     const char *e = getenv("DPF_TC_W");
@@ -1076,13 +1107,14 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
   if (!allow8) return rc;
   // (a wider window must not trade the small-batch key mapping for the padded one)
   Plan p8;
-  if (make_tc_plan_w(B, log_n, r0, rows, D, p8, false, 8, true, pl.Kr == pl.Kt) == DPF_OK) pl = p8;
+  if (make_tc_plan_w(B, log_n, r0, rows, D, p8, false, 8, true, pl.Kr == pl.Kt, xsm) == DPF_OK) pl = p8;
   return DPF_OK;
 }
 
 int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_t D, Plan &pl, bool et,
-                   uint32_t W, bool allow_kr, bool fallback_padded) {
+                   uint32_t W, bool allow_kr, bool fallback_padded, size_t xsm) {
   std::memset(&pl, 0, sizeof pl);
+  pl.xsm = xsm;
   if (D == 0 || D % 4 || D > 1024 || log_n < 3) return DPF_EINVAL;
   pl.tc = true;
   set_ranges(pl, log_n, r0, rows, et);
@@ -1132,7 +1164,7 @@ int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint3
   pl.Kr = (!pl.pair && smallb && allow_kr && B < pl.Kt) ? B : pl.Kt;
   // a Kr-mapped plan whose y ring does not fit falls back to the padded mapping
   auto fail = [&]() {
-    return (pl.Kr < pl.Kt && fallback_padded) ? make_tc_plan_w(B, log_n, r0, rows, D, pl, et, W, false)
+    return (pl.Kr < pl.Kt && fallback_padded) ? make_tc_plan_w(B, log_n, r0, rows, D, pl, et, W, false, true, xsm)
                                               : DPF_EINVAL;
   };
   pl.Ft = pl.Kr == pl.Kt ? 32 * kTcNP / pl.Kt : (32 * kTcNP / pl.Kr) & ~3u;
@@ -1150,14 +1182,15 @@ int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint3
   // 64 KB stages): 2 stages
   if (pl.Kr < pl.Kt && !et &&
       1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(pl.nsy) * pl.y_stage_bytes + 2 * kTcLevelBytes >
-          227 * 1024)
+          smem_cap(pl))
     pl.nsy = 2;
   const size_t fixed = 1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(pl.nsy) * pl.y_stage_bytes;
-  const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / kTcLevelBytes) + 1);
+  if (fixed > smem_cap(pl)) return fail();
+  const uint32_t m_cap = std::min<uint32_t>(14, uint32_t((smem_cap(pl) - fixed) / kTcLevelBytes) + 1);
   const uint32_t m_min = tc_m_min(et, W);  // a subtree holds >= one window
   if (m_cap < m_min || n < m_min) return fail();
   // co-resident CTA pairs: a GPC with an odd SM count leaves an SM unpaired
-  const uint32_t workers = pl.pair ? max_pairs(fixed + tc_stack_bytes(m_cap)) : uint32_t(num_sms());
+  const uint32_t workers = pl.pair ? max_pairs(pl.xsm + fixed + tc_stack_bytes(m_cap)) : uint32_t(num_sms());
   pl.m = choose_m_target(pl, n, m_min, m_cap, workers);
   if (const char *e = getenv("DPF_FORCE_M")) {  // tuning override
     const uint32_t fm = uint32_t(atoi(e));
@@ -1176,7 +1209,7 @@ int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint3
   const uint32_t cols = n_dt_cta * 4 * Ktp;
   pl.tmem_cols = 32;
   while (pl.tmem_cols < cols) pl.tmem_cols <<= 1;
-  pl.smem_bytes = fixed + tc_stack_bytes(pl.m);
+  pl.smem_bytes = pl.xsm + fixed + tc_stack_bytes(pl.m);
   if (pl.smem_bytes > 227 * 1024) return fail();
   pl.grid = pl.pair ? 2 * choose_grid(pl.n_items, pl.n_ktiles, workers) : choose_grid(pl.n_items, pl.n_ktiles);
   pl.prf_blocks = count_blocks(pl, B);
@@ -1285,11 +1318,11 @@ int launch_tc_kernel(const Plan &pl, const dev::FusedParams &p, cudaStream_t st)
   // early termination: producers drain TMEM (EPIP, 18 warps, 96 registers)
   const bool epip = pl.prf == DPF_PRF_CHACHA20_ET;
   if (pl.prf == DPF_PRF_AES128 && pl.Kr < pl.Kt)
-    fn = pl.nsy == 2 ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, 2, 4, false, false, true>
-                     : &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, false, false, true>;
+    fn = pl.nsy == 2 ? &dev::fused_eval_tc_kernel<dev::PrfAesTt, kTcNP, 2, 4, false, false, true>
+                     : &dev::fused_eval_tc_kernel<dev::PrfAesTt, kTcNP, kTcNSY, 4, false, false, true>;
   else if (pl.prf == DPF_PRF_AES128)
-    fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, true, false>
-                 : &dev::fused_eval_tc_kernel<dev::PrfAesBs, kTcNP, kTcNSY, 4, false, false>;
+    fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfAesTt, kTcNP, kTcNSY, 4, true, false>
+                 : &dev::fused_eval_tc_kernel<dev::PrfAesTt, kTcNP, kTcNSY, 4, false, false>;
   else if (epip && pl.Kr < pl.Kt)  // small-batch key mapping (single CTA)
     fn = pl.nsy == 2 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, false, true, true>
                      : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSYEt, 4, false, true, true>;
@@ -1355,10 +1388,11 @@ int launch_eval(const Plan &pl, const uint8_t *keys_dev, uint32_t kstride, uint3
     const uint64_t cnt_s = ((pl.nr1 - 1) >> (pl.n - s)) - (pl.nr0 >> (pl.n - s)) + 1;
     const uint64_t grid = uint64_t(B) * cnt_s;
     if (grid > 0x7FFFFFFFull) return DPF_EINVAL;
-    if (pl.prf == DPF_PRF_AES128)
-      dev::expand_top_split_kernel<dev::PrfAesBs><<<uint32_t(grid), 256, 0, st>>>(
+    if (pl.prf == DPF_PRF_AES128) {
+      if (!allow_dyn_smem(&dev::expand_top_split_kernel<dev::PrfAesTt>, dev::kAesSmemBytes)) return DPF_ECUDA;
+      dev::expand_top_split_kernel<dev::PrfAesTt><<<uint32_t(grid), 256, dev::kAesSmemBytes, st>>>(
           keys_dev, kstride, pl.n, s, pl.f, pl.nr0, pl.nr1, ws.front[0], pl.cap, zero_ptr, zero_vec);
-    else
+    } else
       dev::expand_top_split_kernel<dev::PrfChacha><<<uint32_t(grid), 256, 0, st>>>(
           keys_dev, kstride, pl.n, s, pl.f, pl.nr0, pl.nr1, ws.front[0], pl.cap, zero_ptr, zero_vec);
     ++nk;
@@ -1472,7 +1506,8 @@ int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uin
   if (rc) return rc;
   Plan pl;
   const bool et = prf == DPF_PRF_CHACHA20_ET;
-  rc = packed ? make_tc_plan(B, n, row_begin, rows, D, pl, et) : make_plan(B, n, row_begin, rows, D, pl, et);
+  rc = packed ? make_tc_plan(B, n, row_begin, rows, D, pl, et, prf_smem(prf))
+              : make_plan(B, n, row_begin, rows, D, pl, et, prf_smem(prf));
   if (rc) return rc;
   pl.prf = prf;
   const uint32_t kstride = uint32_t(dpf_key_wire_size_prf(n, prf));
@@ -1504,23 +1539,9 @@ int eval_impl(const dpf_key *keys, uint32_t B, const uint8_t *keys_wire_dev, uin
     if (cudaEventRecord(sg.done[slot], st) != cudaSuccess) return DPF_ECUDA;
     kd = ws.keys;
   }
-  uint32_t prep = 0;
-  if (prf == DPF_PRF_AES128) {
-    // the AES path works on bitsliced seeds: bitslice roots and codewords once
-    // (a private copy: caller-owned device keys are never modified)
-    if (kd != ws.keys &&
-        cudaMemcpyAsync(ws.keys, kd, size_t(B) * kstride, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-      return DPF_ECUDA;
-    const uint64_t items = uint64_t(B) * (1 + 4 * n);
-    dev::aes_bitslice_keys_kernel<<<uint32_t(std::min<uint64_t>((items + 255) / 256, 148ull * 8)), 256, 0, st>>>(
-        ws.keys, kstride, B, n);
-    kd = ws.keys;
-    prep = 1;
-  }
   uint32_t nk = 0;
   rc = launch_eval(pl, kd, kstride, B, table, D, out, ws, st, &nk, flags);
   if (rc) return rc;
-  nk += prep;
   g_stats.prf_blocks = pl.prf_blocks;
   g_stats.kernels = nk;
   g_stats.frontier_depth = pl.f;
@@ -1546,15 +1567,17 @@ extern "C" size_t dpf_eval_workspace_bytes(uint32_t B, uint32_t log_n, uint64_t 
   // contraction paths (IMAD, tcgen05).
   pl.cap += 1;
   size_t bytes = layout(pl, B, dpf_key_wire_size(log_n), nullptr, nullptr);
-  for (int et = 0; et < 2; ++et) {
+  // every PRF (AES: less SMEM for the DFS stack -> possibly a deeper frontier)
+  for (uint32_t prf : {uint32_t(DPF_PRF_CHACHA20), uint32_t(DPF_PRF_AES128), uint32_t(DPF_PRF_CHACHA20_ET)}) {
+    const bool et = prf == DPF_PRF_CHACHA20_ET;
     if (et && log_n <= DPF_ET_BITS) break;
-    const size_t kst = et ? dpf_key_wire_size_prf(log_n, DPF_PRF_CHACHA20_ET) : dpf_key_wire_size(log_n);
+    const size_t kst = dpf_key_wire_size_prf(log_n, prf);
     Plan q;
-    if (et && make_plan(B, log_n, 0, row_count, D, q, true) == DPF_OK) {
+    if (make_plan(B, log_n, 0, row_count, D, q, et, prf_smem(prf)) == DPF_OK) {
       q.cap += 1;
       bytes = std::max(bytes, layout(q, B, kst, nullptr, nullptr));
     }
-    if (make_tc_plan(B, log_n, 0, row_count, D, q, et != 0) == DPF_OK) {
+    if (make_tc_plan(B, log_n, 0, row_count, D, q, et, prf_smem(prf)) == DPF_OK) {
       q.cap += 1;
       bytes = std::max(bytes, layout(q, B, kst, nullptr, nullptr));
     }
@@ -1571,8 +1594,8 @@ extern "C" int dpf_eval_plan(uint32_t B, uint32_t log_n, uint32_t prf, uint64_t 
   const uint64_t dom = 1ull << log_n;
   if (row_begin >= dom || row_count > dom - row_begin) return DPF_EINVAL;
   Plan pl;
-  const int rc = packed ? make_tc_plan(B, log_n, row_begin, row_count, D, pl, et)
-                        : make_plan(B, log_n, row_begin, row_count, D, pl, et);
+  const int rc = packed ? make_tc_plan(B, log_n, row_begin, row_count, D, pl, et, prf_smem(prf))
+                        : make_plan(B, log_n, row_begin, row_count, D, pl, et, prf_smem(prf));
   if (rc) return rc;
   pl.prf = prf;
   out->prf_blocks = pl.prf_blocks;
@@ -1910,8 +1933,8 @@ extern "C" int dpf_eval_leaves(const dpf_key *keys, uint32_t B, uint32_t *leaves
   const uint32_t grid = uint32_t(std::min<uint64_t>((total + 255) / 256, 148ull * 8));
   uint8_t *kd = static_cast<uint8_t *>(workspace);
   if (keys[0].prf == DPF_PRF_AES128) {
-    dev::aes_bitslice_keys_kernel<<<uint32_t((B * (1 + 4 * n) + 255) / 256), 256, 0, st>>>(kd, kstride, B, n);
-    dev::eval_leaves_kernel<dev::PrfAesBs><<<grid, 256, 0, st>>>(kd, kstride, B, n, leaves);
+    if (!allow_dyn_smem(&dev::eval_leaves_kernel<dev::PrfAesTt>, dev::kAesSmemBytes)) return DPF_ECUDA;
+    dev::eval_leaves_kernel<dev::PrfAesTt><<<grid, 256, dev::kAesSmemBytes, st>>>(kd, kstride, B, n, leaves);
   } else if (keys[0].prf == DPF_PRF_CHACHA20_ET) {
     dev::eval_leaves_kernel<dev::PrfChachaEt><<<grid, 256, 0, st>>>(kd, kstride, B, n, leaves);
   } else {
@@ -1961,7 +1984,7 @@ struct GroupedPlan {
   Plan cfg;  // shared kernel configuration (Kt, Ft, W, tiles, SMEM)
   std::vector<dev::GroupDesc> desc;
   std::vector<uint32_t> order;  // launch order (largest subtrees first)
-  size_t front_bytes, keys_bytes, desc_bytes, total_bytes;
+  size_t front_bytes, keys_bytes, desc_bytes, total_bytes;  // keys_bytes: 0 (keys stay in place)
 };
 
 // Shared configuration for all groups (same D and PRF): key tile from the
@@ -2005,7 +2028,7 @@ int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t
     }
   }
   // reuse the single-group planner for the shared part (tile, Ft, SMEM rules)
-  int rc = make_plan(best_kt, 20, 0, 1u << 20, D, pl, et);
+  int rc = make_plan(best_kt, 20, 0, 1u << 20, D, pl, et, prf_smem(prf));
   if (rc) return rc;
   pl.prf = prf;
   (void)Bmax;
@@ -2091,7 +2114,6 @@ int make_grouped_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint32_t
     items += uint64_t(d.n_ktiles) * ((d.F + pl.Ft - 1) / pl.Ft);
     keys += d.B;
     gp.front_bytes += 2 * align_up(size_t(d.B) * d.cap * 16, kAlign);
-    gp.keys_bytes += align_up(size_t(d.B) * d.kstride, kAlign);
     uint64_t top = 0;
     for (uint32_t k = 0; k < d.n - d.m; ++k) top += ((d.nr1 - 1) >> (d.n - k)) - (d.nr0 >> (d.n - k)) + 1;
     const uint64_t per = ((1ull << d.m) - 1) + (et ? (1ull << d.m) : 0);  // + Convert blocks (R20)
@@ -2129,7 +2151,9 @@ int make_grouped_tc_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint3
   }
   // shared MMA N: probe the single-table planner's TMEM rule with B = N
   Plan probe;
-  if (make_tc_plan(1u << 30, 20, 0, 1u << 20, D, probe, et) != DPF_OK) return DPF_EINVAL;
+  // (a batch far above any MMA N, small enough that the item count stays
+  // in range at the shallow subtrees the AES tables leave room for)
+  if (make_tc_plan(1u << 12, 20, 0, 1u << 20, D, probe, et, prf_smem(prf)) != DPF_OK) return DPF_EINVAL;
   const uint32_t nmax = probe.pair ? 2 * probe.Kt : probe.Kt, nmin = probe.pair ? 32 : 16;
   uint32_t best = nmax;
   double best_cost = -1;
@@ -2143,14 +2167,15 @@ int make_grouped_tc_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint3
   }
   Plan &pl = gp.cfg;
   // the shared window: W = 4 leaf pairs (tiny groups need shallow subtrees)
-  int rc = make_tc_plan_w(best, 20, 0, 1u << 20, D, pl, et, et ? 1 : 4);
+  int rc = make_tc_plan_w(best, 20, 0, 1u << 20, D, pl, et, et ? 1 : 4, true, true, prf_smem(prf));
   if (rc) return rc;
   pl.prf = prf;
   const uint32_t m_min = tc_m_min(et, pl.W);
   const uint32_t Ktp = pl.pair ? 2 * pl.Kt : pl.Kt;
   const size_t fixed = 1024 + size_t(pl.nst) * dev::kTcTStageBytes + size_t(pl.nsy) * pl.y_stage_bytes;
-  uint32_t m_cap = std::min<uint32_t>(14, uint32_t((227 * 1024 - fixed) / kTcLevelBytes) + 1);
-  const uint32_t workers = pl.pair ? max_pairs(fixed + tc_stack_bytes(m_cap)) : uint32_t(num_sms());
+  if (fixed > smem_cap(pl)) return DPF_EINVAL;
+  uint32_t m_cap = std::min<uint32_t>(14, uint32_t((smem_cap(pl) - fixed) / kTcLevelBytes) + 1);
+  const uint32_t workers = pl.pair ? max_pairs(pl.xsm + fixed + tc_stack_bytes(m_cap)) : uint32_t(num_sms());
   {
     double units = 0;
     for (uint32_t i = 0; i < G; ++i) units += double((gs[i].B + Ktp - 1) / Ktp) * double(gs[i].row_count >> v);
@@ -2191,7 +2216,7 @@ int make_grouped_tc_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint3
     d.nwin = (et ? (1u << m) : (1u << (m - 1))) / pl.W;
     m_max = std::max(m_max, m);
   }
-  pl.smem_bytes = fixed + tc_stack_bytes(m_max);
+  pl.smem_bytes = pl.xsm + fixed + tc_stack_bytes(m_max);
   gp.order.resize(G);
   for (uint32_t i = 0; i < G; ++i) gp.order[i] = i;
   std::stable_sort(gp.order.begin(), gp.order.end(),
@@ -2207,7 +2232,6 @@ int make_grouped_tc_plan(const dpf_eval_group *gs, uint32_t G, uint32_t D, uint3
     items += it;
     keys += d.B;
     gp.front_bytes += 2 * align_up(size_t(d.B) * d.cap * 16, kAlign);
-    gp.keys_bytes += align_up(size_t(d.B) * d.kstride, kAlign);
     uint64_t top = 0;
     for (uint32_t k = 0; k < d.n - d.m; ++k) top += ((d.nr1 - 1) >> (d.n - k)) - (d.nr0 >> (d.n - k)) + 1;
     const uint64_t per = ((1ull << d.m) - 1) + (et ? (1ull << d.m) : 0);
@@ -2272,9 +2296,8 @@ int eval_grouped_impl(const dpf_eval_group *groups, uint32_t n_groups, uint32_t 
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   uint8_t *base = static_cast<uint8_t *>(workspace);
   uint8_t *front = base, *kbuf = base + gp.front_bytes, *dbuf = kbuf + gp.keys_bytes;
-  // device-side keys: ChaCha uses the caller's wire keys in place; AES gets a
-  // bitsliced private copy
-  size_t foff = 0, koff = 0;
+  // device-side keys: the caller's wire keys, in place (every PRF)
+  size_t foff = 0;
   for (uint32_t oi : gp.order) {
     dev::GroupDesc &d = gp.desc[oi];
     const dpf_eval_group &g = groups[oi];
@@ -2282,18 +2305,7 @@ int eval_grouped_impl(const dpf_eval_group *groups, uint32_t n_groups, uint32_t 
     foff += align_up(size_t(d.B) * d.cap * 16, kAlign);
     d.frontier_alt = reinterpret_cast<uint4 *>(front + foff);
     foff += align_up(size_t(d.B) * d.cap * 16, kAlign);
-    if (prf == DPF_PRF_AES128) {
-      uint8_t *kd = kbuf + koff;
-      if (cudaMemcpyAsync(kd, g.keys_wire, size_t(d.B) * d.kstride, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
-        return DPF_ECUDA;
-      const uint64_t n_items = uint64_t(d.B) * (1 + 4 * d.n);
-      dev::aes_bitslice_keys_kernel<<<uint32_t(std::min<uint64_t>((n_items + 255) / 256, 148ull * 8)), 256, 0, st>>>(
-          kd, d.kstride, d.B, d.n);
-      d.keys = kd;
-    } else {
-      d.keys = g.keys_wire;
-    }
-    koff += align_up(size_t(d.B) * d.kstride, kAlign);
+    d.keys = g.keys_wire;
   }
   // descriptors in launch order (sorted by item_base) -> pinned staging -> device
   std::vector<dev::GroupDesc> sorted;
@@ -2317,23 +2329,26 @@ int eval_grouped_impl(const dpf_eval_group *groups, uint32_t n_groups, uint32_t 
   if (cudaMemcpyAsync(dbuf, sg.buf[slot], db, cudaMemcpyHostToDevice, st) != cudaSuccess) return DPF_ECUDA;
   if (cudaEventRecord(sg.done[slot], st) != cudaSuccess) return DPF_ECUDA;
   const dev::GroupDesc *ddesc = reinterpret_cast<const dev::GroupDesc *>(dbuf);
-  uint32_t nk = prf == DPF_PRF_AES128 ? n_groups : 0;
+  uint32_t nk = 0;
   // a7 zeroing, a2 top BFS, then the fused kernel over all groups' items
   dev::zero_shares_grouped_kernel<<<dim3(64, std::min<uint32_t>(n_groups, 1024)), 256, 0, st>>>(ddesc, n_groups, D);
   uint64_t total_keys = 0;
   for (const auto &d : sorted) total_keys += d.B;
-  if (prf == DPF_PRF_AES128)
-    dev::expand_top_grouped_kernel<dev::PrfAesBs><<<uint32_t(total_keys), 256, 0, st>>>(ddesc, n_groups);
-  else
+  if (prf == DPF_PRF_AES128) {
+    if (!allow_dyn_smem(&dev::expand_top_grouped_kernel<dev::PrfAesTt>, dev::kAesSmemBytes)) return DPF_ECUDA;
+    dev::expand_top_grouped_kernel<dev::PrfAesTt><<<uint32_t(total_keys), 256, dev::kAesSmemBytes, st>>>(ddesc,
+                                                                                                         n_groups);
+  } else
     dev::expand_top_grouped_kernel<dev::PrfChacha><<<uint32_t(total_keys), 256, 0, st>>>(ddesc, n_groups);
   nk += 2;
   uint32_t f_max = 0;
   for (const auto &d : sorted) f_max = std::max(f_max, d.n - d.m);
   for (uint32_t k = kTopSmemLevelsHost + 1; k <= f_max; ++k) {  // deeper frontiers: one launch per level
     const dim3 grid(148 * 4, n_groups);
-    if (prf == DPF_PRF_AES128)
-      dev::expand_level_grouped_kernel<dev::PrfAesBs><<<grid, 256, 0, st>>>(ddesc, k);
-    else
+    if (prf == DPF_PRF_AES128) {
+      if (!allow_dyn_smem(&dev::expand_level_grouped_kernel<dev::PrfAesTt>, dev::kAesSmemBytes)) return DPF_ECUDA;
+      dev::expand_level_grouped_kernel<dev::PrfAesTt><<<grid, 256, dev::kAesSmemBytes, st>>>(ddesc, k);
+    } else
       dev::expand_level_grouped_kernel<dev::PrfChacha><<<grid, 256, 0, st>>>(ddesc, k);
     ++nk;
   }

@@ -239,7 +239,8 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
   constexpr int NC = EPIP ? 1 : 4;          // MMA/epilogue warps
   constexpr int NEPI = EPIP ? NP : 4;       // warps that drain TMEM and release accempty
   const FusedParams &p = tp.f;
-  extern __shared__ __align__(128) uint8_t smem[];
+  extern __shared__ __align__(128) uint8_t smem_all[];
+  uint8_t *smem = smem_all + Prf::kSmemBytes;            // after the PRF's tables (AES)
   uint64_t *tfull = reinterpret_cast<uint64_t *>(smem);  // [NST], count 1 + tx bytes
   uint64_t *tempty = tfull + NST;                        // [NST], count 1 (tcgen05.commit)
   uint64_t *yempty = tempty + NST;                       // [NSY], count 1 (tcgen05.commit)
@@ -295,6 +296,7 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
   }
+  Prf::init_smem();
   tc_fence_before();
   __syncthreads();
   if constexpr (PAIR) cluster_sync_all();  // both CTAs' barriers initialised before any remote arrive

@@ -111,7 +111,26 @@ def test_aes_circuit_count():
     import bench
     gates = 10 * 32 * 113 + 9 * 8 * 92 + 11 * 256 + 10 * (4 * 113 + 128) + 16
     assert bench.aes_alu_ops_per_node() == gates / 32
-    assert 1600 < bench.ALU_OPS_PER_BLOCK["aes128"] < 1610
+
+
+def test_aes_lookup_count():
+    """S-box evaluations of one tree node by brute force over the
+    byte positions: a lookup per (round, block, byte) whose S-box input is not
+    already computed for the other block, plus 4 per key-schedule round.  In
+    round 1 the two states (key XOR 0^120||c) differ only in byte 15; from
+    round 2 on every byte differs (MixColumns spreads it)."""
+    import bench
+    n = 0
+    for rnd in range(1, 11):
+        seen = set()
+        for blk in range(2):
+            for byte in range(16):
+                key = (byte, blk if (rnd > 1 or byte == 15) else 0)
+                if key not in seen:
+                    seen.add(key)
+                    n += 1
+        n += 4
+    assert n == bench.AES_LOOKUPS_PER_NODE == 345
 
 
 def test_roofline_of_runs_on_cpu_with_plan_stats():
