@@ -27,8 +27,10 @@
 // for the second block's round 1, whose plaintext differs from the first only
 // in byte 15, 4 per key-schedule round).
 //
-// Replaces the bitsliced table-free formulation of round 1 (4,075 ALU ops per
-// node; 4,172 QPS at c3): ~725 ALU ops + 345 LDS per node.
+// The key schedule runs on rot16(k), the form the rounds XOR in (no per-round
+// key rotation); rounds 2..9 are a loop unrolled by 2.  Per node (SASS):
+// ~690 ALU ops + 345 LDS.  Replaces the bitsliced table-free formulation of
+// round 1 (4,075 ALU ops per node; 4,172 QPS at c3; now 21.6k).
 #pragma once
 #include <cstdint>
 
@@ -79,8 +81,9 @@ constexpr AesT0 make_aes_t0() {
 static_assert(aes_sbox_ct(0x00) == 0x63 && aes_sbox_ct(0x53) == 0xED && aes_sbox_ct(0xFF) == 0x16,
               "FIPS-197 S-box (Fig. 7)");
 __constant__ AesT0 c_aes_t0 = make_aes_t0();
-// Rcon of rounds 1..10 (FIPS-197 5.2)
-__constant__ uint32_t c_aes_rcon[10] = {0x01, 0x02, 0x04, 0x08, 0x10, 0x20, 0x40, 0x80, 0x1B, 0x36};
+// Rcon of rounds 1..10 (FIPS-197 5.2), rot16 (the key schedule runs on rot16(k))
+__constant__ uint32_t c_aes_rcon_r16[10] = {0x01u << 16, 0x02u << 16, 0x04u << 16, 0x08u << 16, 0x10u << 16,
+                                            0x20u << 16, 0x40u << 16, 0x80u << 16, 0x1Bu << 16, 0x36u << 16};
 
 // the kernels' dynamic shared memory (every extern __shared__ array aliases it)
 extern __shared__ __align__(128) uint8_t dpf_dyn_smem[];
@@ -126,29 +129,30 @@ __device__ __forceinline__ void aes_final_round(const uint32_t (&a)[4], uint32_t
   }
 }
 
-// next round key (FIPS-197 5.2): k0 ^= SubWord(RotWord(k3)) ^ Rcon; k_j ^= k_{j-1}
-__device__ __forceinline__ void aes_next_key(uint32_t (&k)[4], uint32_t rcon, uint32_t l0, uint32_t l1) {
-  // RotWord in LE words: bytes (b1, b2, b3, b0)
-  const uint32_t w1 = aes_tl<1>(k[3], l0), w2 = aes_tl<2>(k[3], l0);  // S at byte 1 (T0)
-  const uint32_t w3 = aes_tl<3>(k[3], l1), w0 = aes_tl<0>(k[3], l1);  // S at bytes 2, 3 (T1)
+// Next round key (FIPS-197 5.2: k0 ^= SubWord(RotWord(k3)) ^ Rcon, k_j ^= k_{j-1}),
+// kept in the rot16 domain: kr_j = rot16(k_j), the form every full round XORs
+// in (so no per-round rotation of the key).  Byte b of k3 is byte (b + 2) & 3
+// of kr3; rot16(t) assembles with a swapped selector.
+__device__ __forceinline__ void aes_next_key_r16(uint32_t (&kr)[4], uint32_t rcon_r16, uint32_t l0, uint32_t l1) {
+  // RotWord in LE words: t = S(k3.b1), S(k3.b2), S(k3.b3), S(k3.b0)
+  const uint32_t w1 = aes_tl<3>(kr[3], l0), w2 = aes_tl<0>(kr[3], l0);  // k3.b1, k3.b2: S at byte 1 (T0)
+  const uint32_t w3 = aes_tl<1>(kr[3], l1), w0 = aes_tl<2>(kr[3], l1);  // k3.b3, k3.b0: S at bytes 2, 3 (T1)
   const uint32_t lo = __byte_perm(w1, w2, 0x0051), hi = __byte_perm(w3, w0, 0x7200);
-  k[0] ^= __byte_perm(lo, hi, 0x7610) ^ rcon;
-  k[1] ^= k[0];
-  k[2] ^= k[1];
-  k[3] ^= k[2];
+  kr[0] ^= __byte_perm(lo, hi, 0x1076) ^ rcon_r16;  // rot16(t) ^ rot16(Rcon)
+  kr[1] ^= kr[0];
+  kr[2] ^= kr[1];
+  kr[3] ^= kr[2];
 }
 
 // Both children of seed s: AES_s(0^128) and AES_s(0^120 || 1).
 __device__ __forceinline__ void aes_children_tt(const uint4 s, uint4 &c0, uint4 &c1) {
   const uint32_t l0 = (threadIdx.x & 31u) << 2, l1 = l0 | 128u;
-  uint32_t k[4] = {s.x, s.y, s.z, s.w};
-  uint32_t a[4], b[4], kr[4];
+  uint32_t kr[4] = {rot16(s.x), rot16(s.y), rot16(s.z), rot16(s.w)};
+  uint32_t a[4], b[4];
   // round 0: AddRoundKey on the plaintexts (block 1: byte 15 = 1 = byte 3 of column 3)
-  const uint32_t a3b = k[3] ^ 0x01000000u;
+  const uint32_t a3b = s.w ^ 0x01000000u;
   // round 1: only column 0 reads byte 15 (ShiftRows: row 3 of column 3 -> column 0)
-  aes_next_key(k, 1u, l0, l1);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) kr[j] = rot16(k[j]);
+  aes_next_key_r16(kr, 0x01u << 16, l0, l1);
   {
     const uint32_t s0 = s.x, s1 = s.y, s2 = s.z, s3 = s.w;
     const uint32_t p = aes_tl<0>(s0, l0) ^ aes_tl<1>(s1, l1);
@@ -162,11 +166,9 @@ __device__ __forceinline__ void aes_children_tt(const uint4 s, uint4 &c0, uint4 
       a[j] = b[j] = aes_tl<0>(st[j], l0) ^ aes_tl<1>(st[(j + 1) & 3], l1) ^ rot16(u);
     }
   }
-#pragma unroll 1
+#pragma unroll 2
   for (uint32_t r = 2; r <= 9; ++r) {
-    aes_next_key(k, c_aes_rcon[r - 1], l0, l1);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) kr[j] = rot16(k[j]);
+    aes_next_key_r16(kr, c_aes_rcon_r16[r - 1], l0, l1);
     uint32_t ta[4], tb[4];
     aes_round(a, ta, kr, l0, l1);
     aes_round(b, tb, kr, l0, l1);
@@ -176,8 +178,10 @@ __device__ __forceinline__ void aes_children_tt(const uint4 s, uint4 &c0, uint4 
       b[j] = tb[j];
     }
   }
-  aes_next_key(k, 0x36u, l0, l1);
-  uint32_t oa[4], ob[4];
+  aes_next_key_r16(kr, 0x36u << 16, l0, l1);
+  uint32_t k[4], oa[4], ob[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) k[j] = rot16(kr[j]);
   aes_final_round(a, oa, k, l0, l1);
   aes_final_round(b, ob, k, l0, l1);
   c0 = make_uint4(oa[0], oa[1], oa[2], oa[3]);

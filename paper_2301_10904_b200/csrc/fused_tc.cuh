@@ -285,6 +285,12 @@ __global__ void __launch_bounds__(32 * (NP + tc_extra_warps(EPIP)), 1) fused_eva
   }
   if (warp == NP) {  // consumer warp 0 owns the TMEM allocation (in each CTA of a pair)
     if constexpr (PAIR) {
+      // (both CTAs name the same slot offset: distinct per-rank slots fault
+      // with a misaligned address.  compute-sanitizer racecheck reports the
+      // paired allocation's completion write into this slot -- no kernel PC --
+      // against this CTA's own alloc; the slot is read only after
+      // __syncthreads + barrier.cluster, tools/experiments/x_sanitize.sh
+      // separates those reports from any other hazard)
       asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                    "r"(tp.tmem_cols)
                    : "memory");
