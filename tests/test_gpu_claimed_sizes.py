@@ -5,7 +5,7 @@
     query (beta T[alpha] inside the shard, 0 outside);
   * the 26-table co-design workload c5 (D = 32, hot/full split, 52 groups) in
     one dpf_eval_grouped launch sequence, every key against the oracle;
-  * c3 on the tensor path with 16 keys against the oracle.
+  * c3 on the tensor path with 16 keys against the oracle (ChaCha20 and AES-128).
 Every comparison is element-wise (assert_array_equal): one wrong word fails."""
 import numpy as np
 import pytest
@@ -92,14 +92,20 @@ def test_c5_codesign_26_tables(dp, oracle):
         np.testing.assert_array_equal(s0, oracle.answer_batch(ok, tbl, threads=8))
 
 
-def test_c3_tensor_path_16_keys(dp, oracle):
+@pytest.mark.parametrize("prf_name", ["chacha20", "aes128"])
+def test_c3_tensor_path_16_keys(dp, oracle, prf_name):
+    """c3 in bench.py's launch configuration (limb-packed table, CTA pairs, the
+    full 256-key batch), 16 keys spread over the batch against the oracle; for
+    AES-128 the T-table kernels (64 KB tables beside the rings and a shallower
+    DFS stack) at the size the AES bench line claims."""
+    prf = {"chacha20": dp.DPF_PRF_CHACHA20, "aes128": dp.DPF_PRF_AES128}[prf_name]
     w = synth.CONFIGS["c3"]
     T = synth.table(w.N, w.D, w.seed)
     al = synth.alphas(w.B, w.N, w.seed)
-    pairs = [dp.gen(w.log_n, int(a), 1, s) for a, s in zip(al, synth.gen_seeds(w.B, w.seed))]
+    pairs = [dp.gen(w.log_n, int(a), 1, s, prf=prf) for a, s in zip(al, synth.gen_seeds(w.B, w.seed))]
     pk = dp.table_pack(to_dev(T))
     wire = torch.from_numpy(dp.keys_to_wire([p[0] for p in pairs])).cuda()
-    sh0 = dp.as_u32(dp.eval_batch_wire_packed(wire, w.log_n, pk))
+    sh0 = dp.as_u32(dp.eval_batch_wire_packed(wire, w.log_n, pk, prf=prf))
     st = dp.last_eval_stats()
     assert st["keys_per_tile"] == 128  # the bench's CTA-pair configuration
     sample = list(range(0, w.B, 16))
