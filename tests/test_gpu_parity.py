@@ -528,7 +528,8 @@ def test_grouped_packed_tc(dp, oracle, prf, D):
         np.testing.assert_array_equal(dp.as_u32(g[4]), want)
 
 
-@pytest.mark.parametrize("prf,D,packed", [(1, 64, False), (1, 256, True), (3, 128, True), (2, 64, False), (3, 64, False)])
+@pytest.mark.parametrize("prf,D,packed", [(1, 64, False), (1, 256, True), (3, 128, True), (2, 64, False), (3, 64, False),
+                                           (2, 256, True)])
 def test_graph_server_replays_new_keys(dp, oracle, prf, D, packed):
     """dpf_server_*: the captured serving graph answers fresh host keys on every
     replay (H2D of the staging buffer inside the graph) and checks headers."""
@@ -550,7 +551,7 @@ def test_graph_server_replays_new_keys(dp, oracle, prf, D, packed):
     srv.close()
 
 
-@pytest.mark.parametrize("depth,packed,prf", [(2, True, 1), (3, False, 1), (2, True, 3)])
+@pytest.mark.parametrize("depth,packed,prf", [(2, True, 1), (3, False, 1), (2, True, 3), (2, True, 2)])
 def test_pipelined_server_batches_in_flight(dp, oracle, depth, packed, prf):
     """dpf_server_pipeline_*: up to `depth` batches in flight, collected oldest
     first, each equal to the oracle; a full pipeline refuses a submit
