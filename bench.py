@@ -97,16 +97,18 @@ def aes_alu_ops_per_node() -> float:
 
 
 def aes_lookups_per_node() -> int:
-    """S-box evaluations of one AES-128 tree node (R8/R9: blocks 0^120||0 and
-    0^120||1 under the node seed, one shared key schedule), each one table
-    read in any table-driven AES (FIPS-197 5.1.1 SubBytes; the T-table form
-    folds ShiftRows/MixColumns into the same read, 5.1.2-5.1.3):
-      SubBytes    10 rounds x 16 bytes x 2 blocks, except that in round 1 the
-                  two states differ only in byte 15 (the plaintexts 0^120||c),
-                  so 16 + 1 distinct S-box inputs there
+    """Distinct S-box evaluations of one AES-128 tree node (R8/R9: blocks
+    0^120||0 and 0^120||1 under the node seed, one shared key schedule), each
+    one table read in any table-driven AES (FIPS-197 5.1.1 SubBytes; the
+    T-table form folds ShiftRows/MixColumns into the same read, 5.1.2-5.1.3):
+      SubBytes    16 bytes x 2 blocks per round, minus the inputs the two
+                  blocks share: in round 1 their states (key XOR plaintext)
+                  differ in byte 15 only (16 + 1 distinct), in round 2 in
+                  column 0 only -- round 1's output column 0 (16 + 4); from
+                  round 3 on MixColumns has spread the difference (32 each)
       KeyExpand   10 rounds x 4 (SubWord)
-    = 17 + 9 x 32 + 40 = 345."""
-    return (16 + 1) + 9 * 32 + 10 * 4
+    = 17 + 20 + 8 x 32 + 40 = 333."""
+    return (16 + 1) + (16 + 4) + 8 * 32 + 10 * 4
 
 
 AES_LOOKUPS_PER_NODE = aes_lookups_per_node()
@@ -683,7 +685,7 @@ def roofline_of(args, w, rows, g, G, stats, kernel_ms, ms_per_step, value, use_p
     algorithmic work per launch / that resource's peak, the largest of
       alu    = ALU-pipe ops of the PRF blocks (640 per ChaCha20 block)
                                                       / 148 x 64 lanes x clock
-      smem   = AES-128: table lookups of the PRF nodes (345 per node)
+      smem   = AES-128: table lookups of the PRF nodes (333 per node)
                                                       / 148 x 32 lanes x clock
                (one conflict-free LDS.32 per clock per SM)
       tensor = 10 u8 limb MACs x 2 ops per (key, row, column) of the

@@ -23,13 +23,14 @@
 // conflict-free LDS and the timing does not depend on the (secret) seed bytes.
 // The address is ONE byte permute: (byte k of x) << 8 | (lane*4 + 128 t),
 // taken from x and a per-lane constant, added to the dynamic-SMEM base by the
-// LDS itself ([R + UR]).  Per node: 345 table lookups (16 per block-round, 1
-// for the second block's round 1, whose plaintext differs from the first only
-// in byte 15, 4 per key-schedule round).
+// LDS itself ([R + UR]).  Per node: 333 table lookups (16 per block-round,
+// minus those the second block shares with the first: its round-1 state
+// differs in byte 15 only, its round-2 state in column 0 only; 4 per
+// key-schedule round).
 //
 // The key schedule runs on rot16(k), the form the rounds XOR in (no per-round
-// key rotation); rounds 2..9 are a loop unrolled by 2.  Per node (SASS):
-// ~690 ALU ops + 345 LDS.  Replaces the bitsliced table-free formulation of
+// key rotation).  Rounds 1 and 2 share lookups between the two blocks (their
+// states differ in byte 15, then in column 0 only): 333 lookups per node.  Replaces the bitsliced table-free formulation of
 // round 1 (4,075 ALU ops per node; 4,172 QPS at c3; now 21.6k).
 #pragma once
 #include <cstdint>
@@ -166,8 +167,33 @@ __device__ __forceinline__ void aes_children_tt(const uint4 s, uint4 &c0, uint4 
       a[j] = b[j] = aes_tl<0>(st[j], l0) ^ aes_tl<1>(st[(j + 1) & 3], l1) ^ rot16(u);
     }
   }
+  // round 2: the two states still differ in column 0 only (round 1's column
+  // 0), so each output column has ONE lookup that differs between the blocks
+  // (column j reads column 0 at byte (4 - j) & 3): 20 lookups instead of 32.
+  aes_next_key_r16(kr, 0x02u << 16, l0, l1);
+  {
+    const uint32_t b0 = b[0];
+    // j = 0: column 0 at byte 0 (T0, outside the rot16 group)
+    const uint32_t r0 = rot16(aes_tl<2>(a[2], l0) ^ aes_tl<3>(a[3], l1) ^ kr[0]);
+    const uint32_t t01 = aes_tl<1>(a[1], l1);
+    const uint32_t e0a = aes_tl<0>(a[0], l0) ^ t01 ^ r0, e0b = aes_tl<0>(b0, l0) ^ t01 ^ r0;
+    // j = 1: column 0 at byte 3 (T1, inside the rot16 group)
+    const uint32_t v1 = aes_tl<0>(a[1], l0) ^ aes_tl<1>(a[2], l1);
+    const uint32_t q1 = aes_tl<2>(a[3], l0) ^ kr[1];
+    const uint32_t e1a = v1 ^ rot16(q1 ^ aes_tl<3>(a[0], l1)), e1b = v1 ^ rot16(q1 ^ aes_tl<3>(b0, l1));
+    // j = 2: column 0 at byte 2 (T0, inside the rot16 group)
+    const uint32_t v2 = aes_tl<0>(a[2], l0) ^ aes_tl<1>(a[3], l1);
+    const uint32_t q2 = aes_tl<3>(a[1], l1) ^ kr[2];
+    const uint32_t e2a = v2 ^ rot16(q2 ^ aes_tl<2>(a[0], l0)), e2b = v2 ^ rot16(q2 ^ aes_tl<2>(b0, l0));
+    // j = 3: column 0 at byte 1 (T1, outside the rot16 group)
+    const uint32_t r3 = rot16(aes_tl<2>(a[1], l0) ^ aes_tl<3>(a[2], l1) ^ kr[3]);
+    const uint32_t t30 = aes_tl<0>(a[3], l0);
+    const uint32_t e3a = t30 ^ aes_tl<1>(a[0], l1) ^ r3, e3b = t30 ^ aes_tl<1>(b0, l1) ^ r3;
+    a[0] = e0a; a[1] = e1a; a[2] = e2a; a[3] = e3a;
+    b[0] = e0b; b[1] = e1b; b[2] = e2b; b[3] = e3b;
+  }
 #pragma unroll 2
-  for (uint32_t r = 2; r <= 9; ++r) {
+  for (uint32_t r = 3; r <= 9; ++r) {
     aes_next_key_r16(kr, c_aes_rcon_r16[r - 1], l0, l1);
     uint32_t ta[4], tb[4];
     aes_round(a, ta, kr, l0, l1);

@@ -628,7 +628,7 @@ def last_eval_stats() -> dict:
 def kernel_name(kernel_id: int) -> str:
     """The fused-kernel template a plan launches (dpf_eval_stats.kernel_id), in
     the form ncu prints it (namespaces dropped)."""
-    prf = {DPF_PRF_CHACHA20: "PrfChacha", DPF_PRF_AES128: "PrfAesBs", DPF_PRF_CHACHA20_ET: "PrfChachaEt"}.get(
+    prf = {DPF_PRF_CHACHA20: "PrfChacha", DPF_PRF_AES128: "PrfAesTt", DPF_PRF_CHACHA20_ET: "PrfChachaEt"}.get(
         (kernel_id >> 8) & 0xF, "?")
     np_ = (kernel_id >> 12) & 0x3F
     if kernel_id & 1:

@@ -123,7 +123,9 @@ def test_workspace_bytes(lib):
     assert dpfpir.eval_workspace_bytes(256, 20, 1 << 20, 255) == 0   # D % 4
     assert dpfpir.eval_workspace_bytes(256, 20, 1 << 20, 2048) == 0  # D > 1024
     ws = dpfpir.eval_workspace_bytes(256, 20, 1 << 20, 256)
-    assert 256 * (32 + 64 * 20) < ws < 64 << 20
+    # sized for every PRF: the AES T-tables take 64 KB of SMEM from the DFS
+    # stack, so its plan keeps a one-level-deeper frontier (f = 13 at c3)
+    assert 256 * (32 + 64 * 20) < ws < 96 << 20
 
 
 def test_eval_rejects_bad_args_without_gpu(lib):

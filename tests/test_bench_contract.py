@@ -114,23 +114,22 @@ def test_aes_circuit_count():
 
 
 def test_aes_lookup_count():
-    """S-box evaluations of one tree node by brute force over the
-    byte positions: a lookup per (round, block, byte) whose S-box input is not
-    already computed for the other block, plus 4 per key-schedule round.  In
-    round 1 the two states (key XOR 0^120||c) differ only in byte 15; from
-    round 2 on every byte differs (MixColumns spreads it)."""
+    """distinct S-box inputs of one tree node, counted over the
+    byte positions from which state bytes the two blocks' states can differ:
+    round 1 (key XOR 0^120||c): byte 15 only; round 2: the bytes that round 1
+    computed from byte 15 -- ShiftRows moves byte 15 (row 3, column 3) to
+    column 0 and MixColumns spreads it over column 0's 4 bytes; round >= 3:
+    every byte.  A lookup per (round, distinct input) plus 4 per key-schedule
+    round."""
     import bench
+    diff = {15}  # state bytes (index r + 4c) that differ between the two blocks
     n = 0
     for rnd in range(1, 11):
-        seen = set()
-        for blk in range(2):
-            for byte in range(16):
-                key = (byte, blk if (rnd > 1 or byte == 15) else 0)
-                if key not in seen:
-                    seen.add(key)
-                    n += 1
-        n += 4
-    assert n == bench.AES_LOOKUPS_PER_NODE == 345
+        n += 16 + len(diff) + 4
+        # next round's differing bytes: ShiftRows new (r, c) = old (r, c + r); MixColumns mixes a column
+        moved = {r + 4 * ((c - r) % 4) for r, c in ((i % 4, i // 4) for i in diff)}
+        diff = {r + 4 * c for c in {i // 4 for i in moved} for r in range(4)}
+    assert n == bench.AES_LOOKUPS_PER_NODE == 333
 
 
 def test_roofline_of_runs_on_cpu_with_plan_stats():
