@@ -29,14 +29,14 @@ ap.add_argument("--q-full", type=int, default=1)
 ap.add_argument("--need", type=int, default=3)
 ap.add_argument("--steps", type=int, default=5)
 ap.add_argument("--check", type=int, default=2, help="inferences whose rows are reconstructed and checked")
-ap.add_argument("--prf", default="chacha20", choices=["chacha20", "chacha20_et"])
+ap.add_argument("--prf", default="chacha20", choices=["chacha20", "chacha20_et", "aes128"])
 ap.add_argument("--packed", action="store_true", help="limb-packed tables + tcgen05 (dpf_eval_grouped_packed)")
 ap.add_argument("--scheme", default="hot", choices=["hot", "pbr"],
                 help="hot: hot-table split, Q_hot + Q_full keys per table (P:645-659); "
                      "pbr: partial batch retrieval, one key per bin of each full table (P:595-602)")
 ap.add_argument("--bins", type=int, default=4, help="PBR bins per table (power of two)")
 a = ap.parse_args()
-prf = dpfpir.DPF_PRF_CHACHA20_ET if a.prf == "chacha20_et" else dpfpir.DPF_PRF_CHACHA20
+prf = {"chacha20": dpfpir.DPF_PRF_CHACHA20, "chacha20_et": dpfpir.DPF_PRF_CHACHA20_ET, "aes128": dpfpir.DPF_PRF_AES128}[a.prf]
 D = synth.CODESIGN_D
 rng = np.random.default_rng(0)
 tables = []
@@ -139,7 +139,7 @@ for Binf in a.batches:
             for j in np.nonzero(mask)[0]:
                 ok &= bool(np.array_equal(ans[inf * q + j], tables[t]["T"][rows[j]]))
     # blocks over each table's rows: N - 1 per key (R9), N/8 - 1 with early termination (R20)
-    blocks = sum(g[0].shape[0] * ((g[2].shape[0] - 1) if prf == dpfpir.DPF_PRF_CHACHA20 else max(1, g[2].shape[0] // 8 - 1))
+    blocks = sum(g[0].shape[0] * ((g[2].shape[0] - 1) if prf != dpfpir.DPF_PRF_CHACHA20_ET else max(1, g[2].shape[0] // 8 - 1))
                  for g in groups0)
     n_rows_wanted = Binf * len(tables) * a.need
     ms = res["grouped"]
@@ -148,5 +148,9 @@ for Binf in a.batches:
                       "q_hot": a.q_hot, "q_full": a.q_full, "hot_fraction": a.hot, "need_per_table": a.need,
                       "dropped_rows": dropped, "wanted_rows": n_rows_wanted, "ms_grouped": round(ms, 4), "ms_separate": round(res["separate"], 4),
                       "inferences_per_s": round(Binf / (ms * 1e-3), 1), "dpf_queries_per_s": round(n_keys / (ms * 1e-3)),
-                      "alu_frac": round(640 * blocks / (ms * 1e-3) / (148 * 64 * 1965e6), 3),
+                      # ALU roofline (640 ops per ChaCha20 block); AES-128: the SMEM-lookup roofline
+                      # (333 table lookups per node, bench.aes_lookups_per_node, 32 lanes/clk/SM)
+                      "alu_frac" if prf != dpfpir.DPF_PRF_AES128 else "smem_frac":
+                          round((640 * blocks / (148 * 64 * 1965e6) if prf != dpfpir.DPF_PRF_AES128 else
+                                 333 * blocks / (148 * 32 * 1965e6)) / (ms * 1e-3), 3),
                       "rows_reconstructed_ok": ok, "plan": plan}), flush=True)
