@@ -680,6 +680,22 @@ def oracle_leg(args, w, wire_host, share0, T_full, G):
     return cpu, parity
 
 
+def tc_smem_operand_bytes(rows: int, D: int, B: int, keys_per_tile: int, pair: bool) -> float:
+    """Shared-memory traffic of the tcgen05 limb contraction for one table pass
+    per key tile (DESIGN.md §8 "Entry-size sweep"): per key tile of N =
+    keys_per_tile keys, 32-row K-chunk and 128-column d-tile, the 10 limb MMAs
+    each read the A tile (128 x 32 B) and this CTA's B columns (N, or N/2 for
+    a CTA pair, x 32 B), and the T ring takes the 16 KB limb-packed entry once.
+    N is fixed by the 512 TMEM columns (4 limb accumulators x d-tiles x N),
+    so at large D the table re-streams once per N keys; this bound (at
+    128 B/clk/SM) is what binds early termination above 1 KiB entries."""
+    n_kt = -(-B // keys_per_tile)
+    n_cc = -(-rows // 32)
+    n_dt = -(-D // 128)
+    n_cta = keys_per_tile // 2 if pair else keys_per_tile
+    return float(n_kt) * n_cc * n_dt * (10 * (4096 + 32 * n_cta) + 16384)
+
+
 def roofline_of(args, w, rows, g, G, stats, kernel_ms, ms_per_step, value, use_packed):
     """The dominant (fused) kernel against whichever resource binds it:
     algorithmic work per launch / that resource's peak, the largest of
@@ -710,16 +726,22 @@ def roofline_of(args, w, rows, g, G, stats, kernel_ms, ms_per_step, value, use_p
     tensor_work = 2.0 * 10 * w.B * rows * w.D if use_packed else 0.0
     hbm_peak = pk["hbm_gbs"] * 1e9
     hbm_work = 4.0 * rows * w.D
+    smem_peak = 148 * 128 * pk["sm_max_mhz"] * 1e6  # B/s
+    smem_work = (tc_smem_operand_bytes(rows, w.D, w.B, stats["keys_per_tile"], bool((stats.get("kernel_id", 0) >> 1) & 1))
+                 if use_packed else 0.0)
     bounds = {prf_res: alu_work / alu_peak, "tensor": tensor_work / tensor_peak, "hbm": hbm_work / hbm_peak}
+    if use_packed:
+        bounds["smem_operands"] = smem_work / smem_peak
     bound = max(bounds, key=bounds.get)
     work, peak, unit = {prf_res: (alu_work, alu_peak, "T lookups/s" if aes else "Tops/s"),
+                        "smem_operands": (smem_work, smem_peak, "GB/s"),
                         "tensor": (tensor_work, tensor_peak, "TOPS (int8)"),
                         "hbm": (hbm_work, hbm_peak, "GB/s")}[bound]
-    scale = 1e-9 if bound == "hbm" else 1e-12
+    scale = 1e-9 if bound in ("hbm", "smem_operands") else 1e-12
     achieved = work / (kern_avg_ms * 1e-3)
     tree_blocks = (rows - 1 + g) if not v else (2 * (rows >> v) - 1 + g)
     qps_roof = min(alu_peak / (ops_per_block * tree_blocks),
-                   w.B / max(bounds["tensor"], bounds["hbm"], 1e-30))
+                   w.B / max(bounds["tensor"], bounds["hbm"], bounds.get("smem_operands", 0.0), 1e-30))
     from paper_2301_10904_b200 import dpfpir
     timed_kernel = dpfpir.kernel_name(stats.get("kernel_id", 0))
     traffic, traffic_kernel = _ncu_traffic(w.name if args.prf == "chacha20" else "%s_%s" % (w.name, args.prf))
@@ -737,6 +759,8 @@ def roofline_of(args, w, rows, g, G, stats, kernel_ms, ms_per_step, value, use_p
                 (ops_per_block, fused_blocks)),
         "peak_basis": {prf_res: ("148 SMs x 32 LDS lanes/clk x %.0f MHz" if aes else
                                  "148 SMs x 64 ALU lanes/clk x %.0f MHz") % pk["sm_max_mhz"],
+                       "smem_operands": "148 SMs x 128 B/clk x %.0f MHz (B300_MICROARCH.md smem crossbar)" %
+                                        pk["sm_max_mhz"],
                        "tensor": "2 x %.1f TFLOP/s bf16 (%s)" % (pk["bf16_tflops"], pk["source"]),
                        "hbm": "%.0f GB/s (%s)" % (pk["hbm_gbs"], pk["source"])},
         "qps_at_roofline": qps_roof, "frac_qps": value / qps_roof,

@@ -14,6 +14,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import synth  # noqa: E402
 from paper_2301_10904_b200 import dpfpir  # noqa: E402
+import bench  # noqa: E402  (tc_smem_operand_bytes)
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--B", type=int, default=256)
@@ -30,6 +31,7 @@ keys = [dpfpir.gen(n, int(a), 1, s, prf=prf)[0] for a, s in zip(al, synth.gen_se
 blocks_per_key = (N - 1) if prf == dpfpir.DPF_PRF_CHACHA20 else (N // 8 - 1)  # R9 / R20
 wire = torch.from_numpy(dpfpir.keys_to_wire(keys)).cuda()
 peak = 148 * 64 * 1965e6
+smem_peak = 148 * 128 * 1965e6  # B/s: 128 B/clk/SM
 for D in args.D:
     T = torch.from_numpy(synth.table(N, D, 7).view(np.int32)).cuda()
     ws = torch.empty(dpfpir.eval_workspace_bytes(B, n, N, D), dtype=torch.uint8, device="cuda")
@@ -53,8 +55,17 @@ for D in args.D:
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / args.steps
         st = dpfpir.last_eval_stats()
+        # binding roofline: ALU (640 ops per block) or, on the tensor path, the
+        # SMEM operand traffic of the limb MMAs at the TMEM-limited MMA N
+        bounds = {"alu": 640 * B * blocks_per_key / peak}
+        if pk is not None:
+            bounds["smem_operands"] = bench.tc_smem_operand_bytes(N, D, B, st["keys_per_tile"],
+                                                                  bool((st["kernel_id"] >> 1) & 1)) / smem_peak
+        bound = max(bounds, key=bounds.get)
         print(json.dumps({"D": D, "entry_bytes": 4 * D, "path": name, "B": B, "log_n": n, "ms": round(ms, 3),
                           "qps": round(B / (ms * 1e-3)), "prf": args.prf,
-                          "step_frac_alu": round(640 * B * blocks_per_key / (ms * 1e-3) / peak, 3),
+                          "step_frac_alu": round(bounds["alu"] / (ms * 1e-3), 3),
+                          "bound": bound, "bounds_ms": {k: round(v * 1e3, 3) for k, v in bounds.items()},
+                          "step_frac_binding": round(bounds[bound] / (ms * 1e-3), 3),
                           "keys_per_tile": st["keys_per_tile"], "frontier_depth": st["frontier_depth"]}), flush=True)
     del T, ws
