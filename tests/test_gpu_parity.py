@@ -242,6 +242,8 @@ def test_aes_leaves_match_oracle(dp, oracle):
 @pytest.mark.parametrize("n,N,D,B,packed", [
     (10, 1000, 16, 3, False), (12, 4096, 64, 37, False), (13, 5000, 32, 64, False), (9, 512, 4, 1, False),
     (12, 4096, 256, 40, True), (11, 2048, 128, 64, True), (12, 3000, 384, 33, True),
+    # small batches on the tensor path (B < MMA N: the Kr key mapping with the AES tables beside it)
+    (12, 4096, 256, 5, True), (11, 2048, 128, 1, True), (10, 1000, 64, 12, True), (13, 8000, 512, 2, True),
 ])
 def test_aes_parity(dp, oracle, n, N, D, B, packed):
     T = synth.table(N, D, 600 + n)
@@ -249,6 +251,18 @@ def test_aes_parity(dp, oracle, n, N, D, B, packed):
     Td = to_dev(T)
     got = dp.as_u32(dp.eval_batch_packed(keys, dp.table_pack(Td)) if packed else dp.eval_batch(keys, Td))
     np.testing.assert_array_equal(got, oracle.answer_batch(okeys, T, threads=8))
+
+
+@pytest.mark.parametrize("n,N,r0,rows,D,B", [(13, 8000, 1000, 5000, 256, 40), (12, 4096, 37, 3001, 128, 17),
+                                             (11, 2048, 2040, 8, 64, 3)])
+def test_aes_packed_shards(dp, oracle, n, N, r0, rows, D, B):
+    """AES-128 on the tensor path over row shards with unaligned starts and
+    ragged ends (the packed table built from the shard at row_begin r0)."""
+    T = synth.table(N, D, 650 + n)
+    keys, okeys = make_aes_keys(dp, oracle, n, synth.alphas(B, N, 650 + n), 660 + n)
+    Tsh = T[r0:r0 + rows]
+    got = dp.as_u32(dp.eval_batch_packed(keys, dp.table_pack(to_dev(Tsh), r0)))
+    np.testing.assert_array_equal(got, oracle.answer_batch(okeys, Tsh, row_begin=r0, threads=8))
 
 
 def test_aes_wire_shard_and_reconstruct(dp, oracle):
