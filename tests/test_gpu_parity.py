@@ -244,6 +244,8 @@ def test_aes_leaves_match_oracle(dp, oracle):
     (12, 4096, 256, 40, True), (11, 2048, 128, 64, True), (12, 3000, 384, 33, True),
     # small batches on the tensor path (B < MMA N: the Kr key mapping with the AES tables beside it)
     (12, 4096, 256, 5, True), (11, 2048, 128, 1, True), (10, 1000, 64, 12, True), (13, 8000, 512, 2, True),
+    # large entries: d-tiles beside the 64 KB of tables (CTA pairs at D = 512, N = 16 at D = 1024)
+    (10, 1024, 512, 70, True), (11, 2000, 1024, 40, True),
 ])
 def test_aes_parity(dp, oracle, n, N, D, B, packed):
     T = synth.table(N, D, 600 + n)
