@@ -62,10 +62,15 @@ for D in args.D:
             bounds["smem_operands"] = bench.tc_smem_operand_bytes(N, D, B, st["keys_per_tile"],
                                                                   bool((st["kernel_id"] >> 1) & 1)) / smem_peak
         bound = max(bounds, key=bounds.get)
+        # table bytes streamed into SMEM per step: once per key tile (N keys, TMEM-limited)
+        tstream = (4.0 * N * (((D + 127) // 128 * 128) if pk is not None else D) *
+                   -(-B // st["keys_per_tile"]))
         print(json.dumps({"D": D, "entry_bytes": 4 * D, "path": name, "B": B, "log_n": n, "ms": round(ms, 3),
                           "qps": round(B / (ms * 1e-3)), "prf": args.prf,
                           "step_frac_alu": round(bounds["alu"] / (ms * 1e-3), 3),
                           "bound": bound, "bounds_ms": {k: round(v * 1e3, 3) for k, v in bounds.items()},
                           "step_frac_binding": round(bounds[bound] / (ms * 1e-3), 3),
+                          "table_stream_gb": round(tstream * 1e-9, 2),
+                          "table_stream_tbs": round(tstream / (ms * 1e-3) * 1e-12, 2),
                           "keys_per_tile": st["keys_per_tile"], "frontier_depth": st["frontier_depth"]}), flush=True)
     del T, ws

@@ -40,7 +40,7 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 
 // grid-stride over entries of S bytes; entry e of CTA c = global entry c + e * grid
 __global__ void k_bulk(const uint8_t *__restrict__ src, uint64_t n_entries, uint32_t S, uint32_t NST, uint32_t NCP,
-                       uint32_t *sink) {
+                       uint32_t *sink, uint64_t wrap = ~0ull) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t *full = reinterpret_cast<uint64_t *>(smem), *empty = full + 16;
   uint8_t *buf = smem + 256;
@@ -59,7 +59,7 @@ __global__ void k_bulk(const uint8_t *__restrict__ src, uint64_t n_entries, uint
       if (lane == 0) mbar_expect_tx(&full[s], S);
       __syncwarp();
       const uint32_t part = S / NCP;
-      if (lane < NCP) bulk_g2s(buf + s * S + lane * part, src + e * S + lane * part, part, &full[s]);
+      if (lane < NCP) bulk_g2s(buf + s * S + lane * part, src + (e % wrap) * S + lane * part, part, &full[s]);
     }
   } else if (warp == 1) {  // consumer: touch one word, release
     uint32_t seq = 0;
@@ -83,8 +83,37 @@ __global__ void k_ldg(const uint4 *__restrict__ src, uint64_t n, uint32_t *sink)
   if (acc == 0x12345678u) sink[0] = acc;
 }
 
-int main() {
+int main(int argc, char **argv) {
   const uint64_t bytes = 1ull << 30;
+  if (argc > 1) {
+    // "l2 <MiB>": stream 1 GiB out of an L2-resident region of <MiB> (the
+    // table re-streams of the large-entry tensor path come mostly from L2)
+    const uint64_t region = uint64_t(atoi(argv[2])) << 20;
+    uint8_t *src; uint32_t *sink;
+    CK(cudaMalloc(&src, region)); CK(cudaMalloc(&sink, 16)); CK(cudaMemset(src, 1, region));
+    int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+    CK(cudaFuncSetAttribute(k_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    for (uint32_t S : {16384u}) {
+      for (uint32_t NST : {2u, 4u, 8u, 12u}) {
+        for (uint32_t NCP : {1u, 4u}) {
+          const uint64_t ne = bytes / S, wrap = region / S;
+          float best = 1e9;
+          for (int r = 0; r < 3; ++r) {
+            cudaEventRecord(a);
+            k_bulk<<<nsm, 64, 256 + size_t(S) * NST>>>(src, ne, S, NST, NCP, sink, wrap);
+            cudaEventRecord(b); cudaEventSynchronize(b);
+            float ms; cudaEventElapsedTime(&ms, a, b);
+            if (ms < best) best = ms;
+          }
+          printf("L2 region %llu MiB: bulk S %u NST %2u copies/entry %u in-flight/SM %4u KB: %.3f ms %7.1f GB/s\n",
+                 (unsigned long long)(region >> 20), S, NST, NCP, S * NST / 1024, best, bytes / (best * 1e-3) * 1e-9);
+        }
+      }
+    }
+    CK(cudaGetLastError());
+    return 0;
+  }
   uint8_t *src; uint32_t *sink;
   CK(cudaMalloc(&src, bytes)); CK(cudaMalloc(&sink, 16));
   CK(cudaMemset(src, 1, bytes));
