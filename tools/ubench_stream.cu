@@ -111,6 +111,20 @@ int main(int argc, char **argv) {
         }
       }
     }
+    // the same bytes by LDG.128 from all warps (16 passes over the region)
+    for (int tpb : {256, 1024}) {
+      float best = 1e9;
+      for (int r = 0; r < 3; ++r) {
+        cudaEventRecord(a);
+        for (uint64_t pass = 0; pass < bytes / region; ++pass)
+          k_ldg<<<nsm * (2048 / tpb), tpb>>>(reinterpret_cast<const uint4 *>(src), region / 16, sink);
+        cudaEventRecord(b); cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+      }
+      printf("L2 region %llu MiB: ldg.128 threads %d x %d CTAs/SM: %.3f ms %7.1f GB/s\n",
+             (unsigned long long)(region >> 20), tpb, 2048 / tpb, best, bytes / (best * 1e-3) * 1e-9);
+    }
     CK(cudaGetLastError());
     return 0;
   }
