@@ -74,6 +74,61 @@ __global__ void k_bulk(const uint8_t *__restrict__ src, uint64_t n_entries, uint
   if (acc == 0x12345678u) sink[0] = acc;
 }
 
+// Cluster of 2 CTAs (2 SMs): entry e of the pair's sequence is issued by CTA
+// e % 2 with .multicast::cluster into both CTAs' ring slot; each slot is
+// re-armed by its issuer once both CTAs' consumers released it (remote
+// arrive on the issuer's empty barrier).  Delivered bytes = 2 x the bytes
+// read: does one bulk copy feeding two SMs lift the per-SM ingest ceiling?
+__global__ void __cluster_dims__(2, 1, 1) k_bulk_mc(const uint8_t *__restrict__ src, uint64_t n_entries, uint32_t S,
+                                                    uint32_t NST, uint32_t *sink, uint64_t wrap) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem), *empty = full + 16;
+  uint8_t *buf = smem + 256;
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < NST; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 2); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  uint32_t acc = 0;
+  if (warp == 0 && lane == 0) {  // loader: arm this CTA's full barrier for every entry; issue its own half
+    uint32_t seq = 0;
+    for (uint64_t e = pair; e < n_entries; e += npairs, ++seq) {
+      const uint32_t s = seq % NST, use = seq / NST;
+      if ((seq & 1) == rank && use > 0) {  // own slot: both CTAs released it
+        asm volatile("{\n\t.reg .pred p;\nMW_%=:\n\tmbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t@!p bra MW_%=;\n}"
+                     ::"r"(smem_u32(&empty[s])), "r"((use - 1) & 1) : "memory");
+      }
+      if ((seq & 1) != rank && use > 0)  // peer's slot: re-arm full only after its previous phase completed
+        mbar_wait(&full[s], (use - 1) & 1);
+      mbar_expect_tx(&full[s], S);
+      if ((seq & 1) == rank)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;"
+                     ::"r"(smem_u32(buf + s * S)), "l"(src + (e % wrap) * S), "r"(S), "r"(smem_u32(&full[s])), "h"(uint16_t(3))
+                     : "memory");
+    }
+  } else if (warp == 1) {  // consumer: touch one word, release to the slot's issuer
+    uint32_t seq = 0;
+    for (uint64_t e = pair; e < n_entries; e += npairs, ++seq) {
+      const uint32_t s = seq % NST, use = seq / NST;
+      mbar_wait(&full[s], use & 1);
+      acc += reinterpret_cast<const uint32_t *>(buf + s * S)[lane];
+      __syncwarp();
+      if (lane == 0) {
+        uint32_t remote;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(&empty[s])), "r"(seq & 1));
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+      }
+    }
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (acc == 0x12345678u) sink[0] = acc;
+}
+
 __global__ void k_ldg(const uint4 *__restrict__ src, uint64_t n, uint32_t *sink) {
   uint32_t acc = 0;
   for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n; i += uint64_t(gridDim.x) * blockDim.x) {
@@ -110,6 +165,23 @@ int main(int argc, char **argv) {
                  (unsigned long long)(region >> 20), S, NST, NCP, S * NST / 1024, best, bytes / (best * 1e-3) * 1e-9);
         }
       }
+    }
+    // multicast to CTA pairs: each pair reads 1/npairs of the entries once and delivers them to 2 SMs
+    CK(cudaFuncSetAttribute(k_bulk_mc, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    for (uint32_t NST : {4u, 8u}) {
+      const uint32_t S = 16384;
+      const uint64_t ne = bytes / S, wrap = region / S;
+      float best = 1e9;
+      for (int r = 0; r < 3; ++r) {
+        cudaEventRecord(a);
+        k_bulk_mc<<<nsm, 64, 256 + size_t(S) * NST>>>(src, ne, S, NST, sink, wrap);
+        cudaEventRecord(b); cudaEventSynchronize(b);
+        float ms; cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+      }
+      CK(cudaGetLastError());
+      printf("L2 region %llu MiB: multicast pairs S %u NST %2u: %.3f ms  read %7.1f GB/s  delivered to SMEM %7.1f GB/s\n",
+             (unsigned long long)(region >> 20), S, NST, best, bytes / (best * 1e-3) * 1e-9, 2 * bytes / (best * 1e-3) * 1e-9);
     }
     // the same bytes by LDG.128 from all warps (16 passes over the region)
     for (int tpb : {256, 1024}) {
