@@ -1107,7 +1107,9 @@ int make_tc_plan(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint32_
   if (!allow8) return rc;
   // (a wider window must not trade the small-batch key mapping for the padded one)
   Plan p8;
-  if (make_tc_plan_w(B, log_n, r0, rows, D, p8, false, 8, true, pl.Kr == pl.Kt, xsm) == DPF_OK) pl = p8;
+  if (make_tc_plan_w(B, log_n, r0, rows, D, p8, false, 8, true, pl.Kr == pl.Kt, xsm) == DPF_OK &&
+      (!xsm || p8.m >= pl.m))  // (AES: not at the cost of subtree depth)
+    pl = p8;
   return DPF_OK;
 }
 
@@ -1151,6 +1153,14 @@ int make_tc_plan_w(uint32_t B, uint32_t log_n, uint64_t r0, uint64_t rows, uint3
   const uint32_t Ktp = pl.pair ? mma_n(n_dt_cta, 32) : mma_n(n_dt_cta, 16);
   pl.Kt = pl.pair ? Ktp / 2 : Ktp;
   pl.nsy = (et && W == 2) ? 2u : tc_y_stages(et);
+  // AES: its 64 KB of T-tables leave the DFS stack one level short at 3 y
+  // stages; 2 stages buy the level back (a shallower top BFS, whose AES
+  // blocks run far below the fused kernel's rate)
+  static const bool aes_nsy2 = [] {  // DPF_AES_NSY2=0 keeps 3 stages (A/B)
+    const char *e = getenv("DPF_AES_NSY2");
+    return !(e && atoi(e) == 0);
+  }();
+  if (xsm && !et && aes_nsy2) pl.nsy = 2;
   // Small batches (B < MMA N, single CTA): the MMA keeps N = Kt columns but
   // only Kr = B of them carry keys -- the producer threads map to (real key,
   // node), Ft = 512 / Kr nodes per item (a multiple of 4, so a window is
@@ -1321,8 +1331,10 @@ int launch_tc_kernel(const Plan &pl, const dev::FusedParams &p, cudaStream_t st)
     fn = pl.nsy == 2 ? &dev::fused_eval_tc_kernel<dev::PrfAesTt, kTcNP, 2, 4, false, false, true>
                      : &dev::fused_eval_tc_kernel<dev::PrfAesTt, kTcNP, kTcNSY, 4, false, false, true>;
   else if (pl.prf == DPF_PRF_AES128)
-    fn = pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfAesTt, kTcNP, kTcNSY, 4, true, false>
-                 : &dev::fused_eval_tc_kernel<dev::PrfAesTt, kTcNP, kTcNSY, 4, false, false>;
+    fn = pl.nsy == 2 ? (pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfAesTt, kTcNP, 2, 4, true, false>
+                                : &dev::fused_eval_tc_kernel<dev::PrfAesTt, kTcNP, 2, 4, false, false>)
+                     : (pl.pair ? &dev::fused_eval_tc_kernel<dev::PrfAesTt, kTcNP, kTcNSY, 4, true, false>
+                                : &dev::fused_eval_tc_kernel<dev::PrfAesTt, kTcNP, kTcNSY, 4, false, false>);
   else if (epip && pl.Kr < pl.Kt)  // small-batch key mapping (single CTA)
     fn = pl.nsy == 2 ? &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, 2, 4, false, true, true>
                      : &dev::fused_eval_tc_kernel<dev::PrfChachaEt, kTcNP, kTcNSYEt, 4, false, true, true>;
